@@ -1,0 +1,35 @@
+# Builds the B200-native PBSA library (sm_100a only) and the CPU oracle (test infrastructure).
+#
+#   make            -> paper_2604_21221_b200/_lib/libpbsa_b200.so  +  oracle/_build/liboracle.so
+#   make oracle-ref -> oracle/_ref/libpbsa_ref.so (reference sources, only where /root/reference exists)
+NVCC      ?= /usr/local/cuda/bin/nvcc
+ARCH      := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
+PKG       := paper_2604_21221_b200
+SRC       := $(wildcard $(PKG)/csrc/*.cu)
+HDR       := $(wildcard $(PKG)/csrc/*.h $(PKG)/csrc/*.cuh) include/pbsa_b200.h
+OBJ       := $(patsubst $(PKG)/csrc/%.cu,build/obj/%.o,$(SRC))
+LIB       := $(PKG)/_lib/libpbsa_b200.so
+HOSTCXX   := $(shell test -x /usr/bin/g++ && echo /usr/bin/g++ || echo g++)
+
+all: $(LIB) oracle
+
+build/obj/%.o: $(PKG)/csrc/%.cu $(HDR)
+	@mkdir -p build/obj build/log
+	$(NVCC) $(NVFLAGS) -ccbin $(HOSTCXX) -c $< -o $@ 2> build/log/$*.ptxas.txt || (cat build/log/$*.ptxas.txt; false)
+
+$(LIB): $(OBJ)
+	@mkdir -p $(PKG)/_lib
+	$(NVCC) $(ARCH) -ccbin $(HOSTCXX) -shared -o $@ $(OBJ)
+
+oracle:
+	$(MAKE) -s -C oracle
+
+oracle-ref:
+	$(MAKE) -s -C oracle ref
+
+clean:
+	rm -rf build $(PKG)/_lib
+	$(MAKE) -s -C oracle clean
+
+.PHONY: all oracle oracle-ref clean

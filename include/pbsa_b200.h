@@ -1,0 +1,145 @@
+/*
+ * pbsa_b200.h -- C ABI of the B200-native Persistent Block-Sparse Attention (PBSA) hot path.
+ *
+ * Drop-in boundary for the reference's operator API (/root/reference/SPEC.md modules router,
+ * attention, memory; numeric conventions of /root/reference/proj/include/pbsa/tensor.hpp).  The
+ * reference has no FFI; each entry point below names the reference op it replaces.  Plain
+ * pointers and sizes only: device pointers unless stated, `stream` is a cudaStream_t passed as
+ * void* (NULL = legacy default stream), bf16 tensors are passed as `const void*` / `void*`.
+ *
+ * Layouts (HBM):
+ *   q / o        [units][n_q][d] bf16, n_q = nqb * b, query tokens block-major (blockify.hpp:32-46)
+ *   k/v pool     [units][n_slots][64][d] bf16: one 64-row slot per key block, rows >= b are zero
+ *   krep         [units][n_slots][d] f32: block representative of the block held in each slot
+ *   qc           [units][nqb][d] f32
+ *   slot lists   int32 slot indices per unit (stride given explicitly)
+ *   sel          [units][nqb][k] int32: selected LOCAL block indices per query block, ascending
+ * Every unit (= batch x head) is independent (per-head memory).
+ *
+ * Status codes: 0 ok, 1 invalid argument, 2 CUDA / launch error, 3 unsupported shape.  The
+ * message of the last failure on the calling thread is returned by pbsa_last_error() (mirrors
+ * the std::invalid_argument messages of tensor.cpp / blockify.cpp).  No entry point synchronizes
+ * the stream; nothing allocates device memory except pbsa_mem_create.
+ */
+#ifndef PBSA_B200_H
+#define PBSA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { PBSA_OK = 0, PBSA_EINVAL = 1, PBSA_ECUDA = 2, PBSA_EUNSUPPORTED = 3 };
+
+const char* pbsa_last_error(void);
+int pbsa_version(void);
+
+/* (a) block compression -- replaces router.compress_blocks (mean pooling,
+ * PAPER.md:415), fp64 accumulation in ascending token order, fp32 output.
+ * Block i of unit u is read at x + u*x_unit_stride + idx*x_block_stride (elements, bf16) and its
+ * representative written to reps + u*reps_unit_stride + idx*d, idx = map ? map[u*n_blocks+i] : i. */
+int pbsa_compress(const void* x, int64_t x_unit_stride, int64_t x_block_stride,
+                  const int32_t* map, int n_blocks, int units, int b, int d, float* reps,
+                  int64_t reps_unit_stride, void* stream);
+
+/* (b) coarse scoring + row-wise Top-K -- replaces router.coarse_attention + select_topk
+ * (+ aggregate_scores).
+ * Keys of unit u are krep[u*krep_unit_stride + key_slots[u*key_stride + j]*d], j < n_keys.  The
+ * local window is keys [local_off, local_off + n_local).  Per query block: logits
+ * float(dot64(qc, kc)) * scale; A_L = masked_softmax_rows over the local keys (Eq. 10);
+ * sel = k largest by (A_L desc, local index asc), written ascending.  If s_t != NULL (the k=0
+ * cache-update pass) also A_t = softmax over all n_keys (Eq. 7) and s_t[u*n_keys + j] =
+ * float(sum_i double(A_t[i][j]) / nqb) (Eq. 8).  k == 0 or n_local == 0 skips selection.
+ * workspace: pbsa_score_select_workspace() bytes of device memory. */
+size_t pbsa_score_select_workspace(int units, int nqb, int n_keys);
+int pbsa_score_select(const float* qc, const float* krep, int64_t krep_unit_stride,
+                      const int32_t* key_slots, int key_stride, int n_keys, int local_off,
+                      int n_local, int k, int nqb, int units, int d, float scale, int32_t* sel,
+                      float* s_t, void* workspace, size_t workspace_bytes, void* stream);
+
+/* (c) block-sparse attention forward -- replaces attention.attention_sparse (SPEC.md:367-375,
+ * Eq. 3-5).  Query block i of unit u attends to the dense slots
+ * dense_slots[u*dense_stride + 0..n_dense) (persistent blocks + current chunk, always visible)
+ * and to the selected local blocks local_slots[u*local_stride + sel[(u*nqb+i)*k + 0..k)].
+ * Key rows >= b of a slot are masked.  o = softmax(q k^T * scale) v (bf16 out, fp32 softmax and
+ * accumulators); lse (nullable) [units][n_q] natural-log row log-sum-exp.  d in {64, 128},
+ * 1 <= b <= 64.  k_pool / v_pool: [units][n_slots][64][d]. */
+int pbsa_bsa_fwd(const void* q, const void* k_pool, const void* v_pool, int n_slots,
+                 const int32_t* dense_slots, int dense_stride, int n_dense,
+                 const int32_t* local_slots, int local_stride, int n_local, const int32_t* sel,
+                 int k, int nqb, int b, int d, int units, float scale, void* o, float* lse,
+                 void* stream);
+
+/* (d) persistent memory -- replaces memory.PersistentMemory / LocalWindow / push_chunk /
+ * update_persistent / assemble_kv (Eq. 9).  Device-resident
+ * state for `units` heads: the slot pools, representatives and the P / L / stage slot tables.
+ * Capacities in blocks (C) and chunks (window); sinks = blocks of the first chunk,
+ * counted inside C (requires capacity_c >= blocks_per_chunk).  Block ids are the monotone
+ * stream index chunk*blocks_per_chunk + i. */
+typedef struct pbsa_mem pbsa_mem;
+
+typedef struct pbsa_mem_info {
+    int units, capacity_c, window_chunks, blocks_per_chunk, b, d;
+    int n_slots;          /* capacity_c + window_chunks*blocks_per_chunk + blocks_per_chunk */
+    int n_p, n_sinks, n_l;  /* current persistent / sink / local block counts (same every unit) */
+    int64_t chunks_committed;
+    /* device views (valid until destroy) */
+    void *k_pool, *v_pool;      /* [units][n_slots][64][d] bf16 */
+    float* krep;                /* [units][n_slots][d] */
+    int32_t* dense_slots;       /* [units][dense_stride]: P (sinks id asc, dynamic id asc) ++ stage */
+    int32_t* local_slots;       /* [units][local_stride]: L chunks oldest -> newest */
+    int32_t* key_slots;         /* [units][key_stride]: P ++ L ++ stage (the k=0 scoring order) */
+    int32_t* stage_slots;       /* [units][blocks_per_chunk]: where the current chunk's K/V live */
+    int64_t* p_ids;             /* [units][capacity_c] ids in dense order */
+    float* p_scores;            /* [units][capacity_c] last s_t of each persistent block */
+    int64_t* l_ids;             /* [units][local_stride] */
+    int dense_stride, local_stride, key_stride;
+} pbsa_mem_info;
+
+int pbsa_mem_create(pbsa_mem** out, int units, int capacity_c, int window_chunks,
+                    int blocks_per_chunk, int b, int d);
+int pbsa_mem_destroy(pbsa_mem* m);
+int pbsa_mem_reset(pbsa_mem* m, void* stream);
+int pbsa_mem_get_info(const pbsa_mem* m, pbsa_mem_info* info);
+/* Write the current chunk's K and V ([units][blocks_per_chunk*b][d] bf16, block-major) into the
+ * stage slots and compress K into krep (fused (a)).  Called once per PBSA call. */
+int pbsa_mem_write_chunk(pbsa_mem* m, const void* k_chunk, const void* v_chunk, void* stream);
+/* K4: the k=0 cache update of Alg. 1.  s_t: [units][n_keys] scores in
+ * key_slots order (from pbsa_score_select).  push_chunk(stage) -> evict oldest chunk on
+ * overflow -> update_persistent -> refresh slot tables -> new stage slots. */
+int pbsa_mem_commit(pbsa_mem* m, const float* s_t, void* stream);
+
+/* One full PBSA call of a layer on the current chunk (Alg. 1 line "Apply PBSA with Top-K"):
+ * K1(Q) -> K2 -> K3, and for mode PBSA_MODE_CACHE_UPDATE (the k=0 pass) also s_t and K4.
+ * q [units][blocks_per_chunk*b][d] bf16; o same shape; lse nullable.  k_top = |Omega(q)| in
+ * blocks (clipped to the local window); scale <= 0 selects d^-1/2. */
+enum { PBSA_MODE_DENOISE = 0, PBSA_MODE_CACHE_UPDATE = 1 };
+int pbsa_attend(pbsa_mem* m, const void* q, int k_top, float scale, int mode, void* o,
+                float* lse, void* stream);
+/* last selection of pbsa_attend (device): [units][blocks_per_chunk][k] ascending, and last s_t */
+int pbsa_last_selection(const pbsa_mem* m, const int32_t** sel, int* k, const float** s_t,
+                        int* n_keys);
+
+/* Stage timing with CUDA events recorded on the call's stream (no host sync inside calls).
+ * enable: allocate a pool for max_calls calls and reset the sums; 0 disables.  read: waits for
+ * the last recorded event and returns per-stage sums in ms: [0] KV write (+K compression),
+ * [1] Q compression (a), [2] scoring + Top-K (b), [3] attention (c), [4] memory update (d),
+ * and the number of attend calls / KV writes timed. */
+int pbsa_mem_profile(pbsa_mem* m, int enable, int max_calls);
+int pbsa_mem_profile_read(pbsa_mem* m, double* stage_ms, int* n_attend, int* n_write);
+
+/* cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault) on `stream` (state export for tests) */
+int pbsa_copy(void* dst, const void* src, size_t bytes, void* stream);
+
+/* debug: one 128-row query tile against one 64-row KV slot through the tcgen05 path.
+ * q [128][d], k/v [64][d] bf16 (device); s_out [128][64] f32 = q k^T; o_out [128][d] f32 =
+ * bf16(s_out) v.  Validates descriptors / TMEM layouts. */
+int pbsa_debug_tile(const void* q, const void* k, const void* v, int d, float* s_out,
+                    float* o_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PBSA_B200_H */

@@ -1,0 +1,10 @@
+"""B200-native Persistent Block-Sparse Attention (PBSA), the hot path of Sparse Forcing.
+
+Importing the package loads libpbsa_b200.so (sm_100a kernels behind a C ABI, see
+include/pbsa_b200.h); there is no CPU fallback.
+"""
+from .pbsa import (MODE_CACHE_UPDATE, MODE_DENOISE, Memory, PbsaCudaError, PbsaError,  # noqa: F401
+                   attention_scale, attention_sparse, compress_blocks, debug_tile, score_select,
+                   topk_count)
+
+__version__ = "0.1.0"

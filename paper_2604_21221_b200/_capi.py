@@ -1,0 +1,90 @@
+"""ctypes binding of libpbsa_b200.so (include/pbsa_b200.h).
+
+This is exactly the binding a reference-side maintainer would add; the
+Python API in `pbsa.py` is layered on top of it.  There is no fallback: if the shared library is
+missing or fails to load, importing the package raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libpbsa_b200.so")
+
+PBSA_OK, PBSA_EINVAL, PBSA_ECUDA, PBSA_EUNSUPPORTED = 0, 1, 2, 3
+MODE_DENOISE, MODE_CACHE_UPDATE = 0, 1
+
+_vp, _i32, _i64, _f32 = C.c_void_p, C.c_int, C.c_int64, C.c_float
+
+
+class MemInfo(C.Structure):
+    _fields_ = [
+        ("units", _i32), ("capacity_c", _i32), ("window_chunks", _i32),
+        ("blocks_per_chunk", _i32), ("b", _i32), ("d", _i32), ("n_slots", _i32),
+        ("n_p", _i32), ("n_sinks", _i32), ("n_l", _i32), ("chunks_committed", _i64),
+        ("k_pool", _vp), ("v_pool", _vp), ("krep", _vp), ("dense_slots", _vp),
+        ("local_slots", _vp), ("key_slots", _vp), ("stage_slots", _vp), ("p_ids", _vp),
+        ("p_scores", _vp), ("l_ids", _vp), ("dense_stride", _i32), ("local_stride", _i32),
+        ("key_stride", _i32),
+    ]
+
+
+_SIGS = {
+    "pbsa_last_error": (C.c_char_p, []),
+    "pbsa_version": (_i32, []),
+    "pbsa_compress": (_i32, [_vp, _i64, _i64, _vp, _i32, _i32, _i32, _i32, _vp, _i64, _vp]),
+    "pbsa_score_select_workspace": (C.c_size_t, [_i32, _i32, _i32]),
+    "pbsa_score_select": (_i32, [_vp, _vp, _i64, _vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32,
+                                 _i32, _f32, _vp, _vp, _vp, C.c_size_t, _vp]),
+    "pbsa_bsa_fwd": (_i32, [_vp, _vp, _vp, _i32, _vp, _i32, _i32, _vp, _i32, _i32, _vp, _i32,
+                            _i32, _i32, _i32, _i32, _f32, _vp, _vp, _vp]),
+    "pbsa_mem_create": (_i32, [C.POINTER(_vp), _i32, _i32, _i32, _i32, _i32, _i32]),
+    "pbsa_mem_destroy": (_i32, [_vp]),
+    "pbsa_mem_reset": (_i32, [_vp, _vp]),
+    "pbsa_mem_get_info": (_i32, [_vp, C.POINTER(MemInfo)]),
+    "pbsa_mem_write_chunk": (_i32, [_vp, _vp, _vp, _vp]),
+    "pbsa_mem_commit": (_i32, [_vp, _vp, _vp]),
+    "pbsa_attend": (_i32, [_vp, _vp, _i32, _f32, _i32, _vp, _vp, _vp]),
+    "pbsa_last_selection": (_i32, [_vp, C.POINTER(_vp), C.POINTER(_i32), C.POINTER(_vp),
+                                   C.POINTER(_i32)]),
+    "pbsa_mem_profile": (_i32, [_vp, _i32, _i32]),
+    "pbsa_mem_profile_read": (_i32, [_vp, C.POINTER(C.c_double), C.POINTER(_i32), C.POINTER(_i32)]),
+    "pbsa_copy": (_i32, [_vp, _vp, C.c_size_t, _vp]),
+    "pbsa_debug_tile": (_i32, [_vp, _vp, _vp, _i32, _vp, _vp, _vp]),
+}
+
+EXPORTED = sorted(_SIGS)
+
+
+def load(path: str = LIB_PATH) -> C.CDLL:
+    if not os.path.exists(path):
+        raise ImportError(
+            f"{path} is missing: build the CUDA library first (`make` or "
+            f"`python -c 'import __graft_entry__ as g; g.build()'`). There is no CPU fallback.")
+    lib = C.CDLL(path)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+LIB = load()
+
+
+class PbsaError(ValueError):
+    """Invalid argument / unsupported shape (the reference raises std::invalid_argument)."""
+
+
+class PbsaCudaError(RuntimeError):
+    """CUDA / launch failure."""
+
+
+def check(rc: int) -> None:
+    if rc == PBSA_OK:
+        return
+    msg = LIB.pbsa_last_error().decode()
+    if rc == PBSA_ECUDA:
+        raise PbsaCudaError(msg)
+    raise PbsaError(msg)

@@ -1,0 +1,472 @@
+// capi.cu -- the C ABI (include/pbsa_b200.h): argument checking, error reporting, TMA
+// descriptor encoding, the device-resident memory object and the per-call orchestration.
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+namespace pbsa {
+
+namespace {
+thread_local std::string g_err;
+}
+
+const char* last_error() { return g_err.c_str(); }
+
+int set_error(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+int check_launch(const char* what) {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_error(PBSA_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    return PBSA_OK;
+}
+
+bool encode_tmap_bf16(void* tmap, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                      const uint32_t* box, std::string* err) {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    if (fn == nullptr) {
+        *err = "cuTensorMapEncodeTiled unavailable";
+        return false;
+    }
+    cuuint64_t gd[5], gs[4];
+    cuuint32_t bx[5], es[5];
+    for (int i = 0; i < rank; ++i) {
+        gd[i] = dims[i];
+        bx[i] = box[i];
+        es[i] = 1;
+        if (i + 1 < rank) gs[i] = strides[i];
+    }
+    const CUresult r = fn(reinterpret_cast<CUtensorMap*>(tmap), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                          static_cast<cuuint32_t>(rank), const_cast<void*>(base), gd, gs, bx, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        *err = "cuTensorMapEncodeTiled failed (CUresult " + std::to_string(static_cast<int>(r)) + ")";
+        return false;
+    }
+    return true;
+}
+
+}  // namespace pbsa
+
+using namespace pbsa;
+
+#define PBSA_REQUIRE(cond, msg)                                  \
+    do {                                                         \
+        if (!(cond)) return ::pbsa::set_error(PBSA_EINVAL, msg); \
+    } while (0)
+
+#define PBSA_CUDA(call)                                                                          \
+    do {                                                                                         \
+        const cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess) return ::pbsa::set_error(PBSA_ECUDA, std::string(#call ": ") +    \
+                                                                     cudaGetErrorString(e_));    \
+    } while (0)
+
+struct pbsa_mem {
+    int units = 0, C = 0, W = 0, bpc = 0, b = 0, d = 0, S = 0, Lcap = 0;
+    MemCounts counts{};
+    bf16* k_pool = nullptr;
+    bf16* v_pool = nullptr;
+    float* krep = nullptr;
+    MemDev dev{};
+    float* qc = nullptr;
+    float* s_t = nullptr;
+    float* ws = nullptr;
+    size_t ws_bytes = 0;
+    int32_t* sel = nullptr;
+    int last_k = 0, last_n_keys = 0;
+    // stage profiling: 5 events per attend call, 2 per KV write
+    std::vector<cudaEvent_t> ev_attend, ev_write;
+    int prof_max = 0, prof_attend = 0, prof_write = 0;
+    bool prof_on = false;
+};
+
+namespace {
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int check_d(int d) {
+    if (d != 64 && d != 128) return set_error(PBSA_EUNSUPPORTED, "head dim d must be 64 or 128, got " + std::to_string(d));
+    return PBSA_OK;
+}
+
+void free_events(pbsa_mem* m) {
+    for (cudaEvent_t e : m->ev_attend) cudaEventDestroy(e);
+    for (cudaEvent_t e : m->ev_write) cudaEventDestroy(e);
+    m->ev_attend.clear();
+    m->ev_write.clear();
+    m->prof_on = false;
+    m->prof_max = m->prof_attend = m->prof_write = 0;
+}
+
+// record event i of the current attend call's group (no-op when profiling is off or full)
+void prof_mark(pbsa_mem* m, int i, cudaStream_t s) {
+    if (!m->prof_on || m->prof_attend >= m->prof_max) return;
+    cudaEventRecord(m->ev_attend[static_cast<size_t>(m->prof_attend) * 5 + i], s);
+}
+
+void free_mem(pbsa_mem* m) {
+    free_events(m);
+    void* ptrs[] = {m->k_pool, m->v_pool, m->krep, m->dev.p_slot, m->dev.p_id, m->dev.p_score,
+                    m->dev.l_slot, m->dev.l_id, m->dev.stage, m->dev.free_slot, m->dev.dense,
+                    m->dev.keys, m->qc, m->s_t, m->ws, m->sel};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+}
+
+MemCounts next_counts(const pbsa_mem* m, const MemCounts& c, int* dropped) {
+    MemCounts n = c;
+    n.chunk = c.chunk + 1;
+    *dropped = 0;
+    if (c.n_l + m->bpc > m->Lcap) {
+        const int64_t evicted_chunk = c.chunk - m->W;
+        if (evicted_chunk == 0) {
+            n.n_sinks = m->bpc;
+            n.n_p = m->bpc + (c.n_p - c.n_sinks);
+        } else {
+            const int n_cand = (c.n_p - c.n_sinks) + m->bpc;
+            const int cap = m->C - c.n_sinks;
+            const int keep = n_cand < cap ? n_cand : cap;
+            n.n_p = c.n_sinks + keep;
+            *dropped = n_cand - keep;
+        }
+        n.n_l = c.n_l;
+    } else {
+        n.n_l = c.n_l + m->bpc;
+    }
+    n.n_free = c.n_free + *dropped - m->bpc;
+    return n;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pbsa_last_error(void) { return last_error(); }
+
+int pbsa_version(void) { return 1; }
+
+int pbsa_compress(const void* x, int64_t x_unit_stride, int64_t x_block_stride, const int32_t* map,
+                  int n_blocks, int units, int b, int d, float* reps, int64_t reps_unit_stride,
+                  void* stream) {
+    if (int rc = check_d(d)) return rc;
+    PBSA_REQUIRE(n_blocks >= 0 && units >= 0, "compress: negative counts");
+    PBSA_REQUIRE(b >= 1, "compress: block size b must be >= 1");
+    PBSA_REQUIRE(x != nullptr && reps != nullptr, "compress: null pointer");
+    PBSA_REQUIRE(aligned16(x) && x_unit_stride % 8 == 0 && x_block_stride % 8 == 0,
+                 "compress: x and its strides must be 16-byte aligned");
+    return launch_compress(static_cast<const bf16*>(x), x_unit_stride, x_block_stride, map, n_blocks,
+                           units, b, d, reps, reps_unit_stride, as_stream(stream));
+}
+
+size_t pbsa_score_select_workspace(int units, int nqb, int n_keys) {
+    return score_select_workspace(units, nqb, n_keys);
+}
+
+int pbsa_score_select(const float* qc, const float* krep, int64_t krep_unit_stride,
+                      const int32_t* key_slots, int key_stride, int n_keys, int local_off,
+                      int n_local, int k, int nqb, int units, int d, float scale, int32_t* sel,
+                      float* s_t, void* workspace, size_t workspace_bytes, void* stream) {
+    if (int rc = check_d(d)) return rc;
+    PBSA_REQUIRE(n_keys >= 0 && nqb >= 0 && units >= 0 && k >= 0, "score_select: negative counts");
+    PBSA_REQUIRE(local_off >= 0 && n_local >= 0 && local_off + n_local <= n_keys,
+                 "score_select: local window outside the key list");
+    PBSA_REQUIRE(k <= n_local, "score_select: k exceeds the number of local blocks");
+    PBSA_REQUIRE(k == 0 || sel != nullptr, "score_select: sel is null");
+    PBSA_REQUIRE(s_t == nullptr || n_keys >= 1, "score_select: s_t requested with no keys");
+    PBSA_REQUIRE(key_stride >= n_keys, "score_select: key_stride < n_keys");
+    PBSA_REQUIRE(aligned16(krep) && krep_unit_stride % 4 == 0, "score_select: krep must be 16-byte aligned");
+    if (!(scale > 0.0f)) scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(d)));
+    return launch_score_select(qc, krep, krep_unit_stride, key_slots, key_stride, n_keys, local_off,
+                               n_local, k, nqb, units, d, scale, sel, s_t, workspace, workspace_bytes,
+                               as_stream(stream));
+}
+
+int pbsa_bsa_fwd(const void* q, const void* k_pool, const void* v_pool, int n_slots,
+                 const int32_t* dense_slots, int dense_stride, int n_dense,
+                 const int32_t* local_slots, int local_stride, int n_local, const int32_t* sel,
+                 int k, int nqb, int b, int d, int units, float scale, void* o, float* lse,
+                 void* stream) {
+    if (int rc = check_d(d)) return rc;
+    PBSA_REQUIRE(b >= 1 && b <= 64, "bsa_fwd: block size b must be in [1, 64]");
+    PBSA_REQUIRE(nqb >= 0 && units >= 0 && n_slots >= 1, "bsa_fwd: bad counts");
+    PBSA_REQUIRE(n_dense >= 0 && n_local >= 0 && k >= 0 && k <= n_local, "bsa_fwd: bad visibility counts");
+    PBSA_REQUIRE(n_dense == 0 || (dense_slots != nullptr && dense_stride >= n_dense), "bsa_fwd: dense list");
+    PBSA_REQUIRE(k == 0 || (local_slots != nullptr && sel != nullptr && local_stride >= n_local),
+                 "bsa_fwd: local list / selection");
+    PBSA_REQUIRE(n_slots < (1 << 24) / 64, "bsa_fwd: too many slots per unit");
+    PBSA_REQUIRE(static_cast<int64_t>(units) * n_slots * 64 < (int64_t(1) << 31), "bsa_fwd: pool too large for 32-bit TMA rows");
+    PBSA_REQUIRE(static_cast<int64_t>(units) * nqb < (int64_t(1) << 31), "bsa_fwd: too many query blocks");
+    PBSA_REQUIRE(q && k_pool && v_pool && o, "bsa_fwd: null pointer");
+    PBSA_REQUIRE(aligned16(q) && aligned16(k_pool) && aligned16(v_pool) && aligned16(o),
+                 "bsa_fwd: tensors must be 16-byte aligned");
+    if (!(scale > 0.0f)) scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(d)));
+    return launch_bsa_fwd(static_cast<const bf16*>(q), static_cast<const bf16*>(k_pool),
+                          static_cast<const bf16*>(v_pool), n_slots, dense_slots, dense_stride, n_dense,
+                          local_slots, local_stride, n_local, sel, k, nqb, b, d, units, scale,
+                          static_cast<bf16*>(o), lse, as_stream(stream));
+}
+
+int pbsa_copy(void* dst, const void* src, size_t bytes, void* stream) {
+    PBSA_REQUIRE(bytes == 0 || (dst != nullptr && src != nullptr), "copy: null pointer");
+    if (bytes) PBSA_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, as_stream(stream)));
+    return PBSA_OK;
+}
+
+int pbsa_debug_tile(const void* q, const void* k, const void* v, int d, float* s_out, float* o_out,
+                    void* stream) {
+    if (int rc = check_d(d)) return rc;
+    PBSA_REQUIRE(q && k && v && s_out && o_out, "debug_tile: null pointer");
+    return launch_debug_tile(static_cast<const bf16*>(q), static_cast<const bf16*>(k),
+                             static_cast<const bf16*>(v), d, s_out, o_out, as_stream(stream));
+}
+
+int pbsa_mem_create(pbsa_mem** out, int units, int capacity_c, int window_chunks,
+                    int blocks_per_chunk, int b, int d) {
+    PBSA_REQUIRE(out != nullptr, "mem_create: out is null");
+    *out = nullptr;
+    if (int rc = check_d(d)) return rc;
+    PBSA_REQUIRE(units >= 1, "mem_create: units must be >= 1");
+    PBSA_REQUIRE(blocks_per_chunk >= 1, "mem_create: blocks_per_chunk must be >= 1");
+    PBSA_REQUIRE(window_chunks >= 1, "mem_create: window capacity must be >= 1 chunk");
+    PBSA_REQUIRE(capacity_c >= blocks_per_chunk,
+                 "mem_create: persistent capacity C must hold the sink chunk (C >= blocks_per_chunk)");
+    PBSA_REQUIRE(b >= 1 && b <= 64, "mem_create: block size b must be in [1, 64]");
+    auto* m = new pbsa_mem;
+    m->units = units;
+    m->C = capacity_c;
+    m->W = window_chunks;
+    m->bpc = blocks_per_chunk;
+    m->b = b;
+    m->d = d;
+    m->Lcap = window_chunks * blocks_per_chunk;
+    m->S = capacity_c + m->Lcap + blocks_per_chunk;
+    const size_t U = static_cast<size_t>(units), S = m->S, C = m->C, L = m->Lcap, bpc = m->bpc;
+    auto alloc = [&](void** p, size_t bytes) -> bool { return cudaMalloc(p, bytes ? bytes : 16) == cudaSuccess; };
+    bool ok = alloc(reinterpret_cast<void**>(&m->k_pool), U * S * 64 * d * 2) &&
+              alloc(reinterpret_cast<void**>(&m->v_pool), U * S * 64 * d * 2) &&
+              alloc(reinterpret_cast<void**>(&m->krep), U * S * d * 4) &&
+              alloc(reinterpret_cast<void**>(&m->dev.p_slot), U * C * 4) &&
+              alloc(reinterpret_cast<void**>(&m->dev.p_id), U * C * 8) &&
+              alloc(reinterpret_cast<void**>(&m->dev.p_score), U * C * 4) &&
+              alloc(reinterpret_cast<void**>(&m->dev.l_slot), U * L * 4) &&
+              alloc(reinterpret_cast<void**>(&m->dev.l_id), U * L * 8) &&
+              alloc(reinterpret_cast<void**>(&m->dev.stage), U * bpc * 4) &&
+              alloc(reinterpret_cast<void**>(&m->dev.free_slot), U * S * 4) &&
+              alloc(reinterpret_cast<void**>(&m->dev.dense), U * (C + bpc) * 4) &&
+              alloc(reinterpret_cast<void**>(&m->dev.keys), U * S * 4) &&
+              alloc(reinterpret_cast<void**>(&m->qc), U * bpc * d * 4) &&
+              alloc(reinterpret_cast<void**>(&m->s_t), U * S * 4) &&
+              alloc(reinterpret_cast<void**>(&m->sel), U * bpc * L * 4);
+    if (ok) {
+        m->ws_bytes = score_select_workspace(units, m->bpc, m->S);
+        ok = alloc(reinterpret_cast<void**>(&m->ws), m->ws_bytes);
+    }
+    if (!ok) {
+        free_mem(m);
+        delete m;
+        cudaGetLastError();
+        return set_error(PBSA_ECUDA, "mem_create: out of device memory");
+    }
+    if (int rc = pbsa_mem_reset(m, nullptr)) {
+        free_mem(m);
+        delete m;
+        return rc;
+    }
+    PBSA_CUDA(cudaStreamSynchronize(nullptr));
+    *out = m;
+    return PBSA_OK;
+}
+
+int pbsa_mem_destroy(pbsa_mem* m) {
+    if (m == nullptr) return PBSA_OK;
+    cudaDeviceSynchronize();
+    free_mem(m);
+    delete m;
+    return PBSA_OK;
+}
+
+int pbsa_mem_reset(pbsa_mem* m, void* stream) {
+    PBSA_REQUIRE(m != nullptr, "mem_reset: null memory");
+    cudaStream_t s = as_stream(stream);
+    const size_t U = m->units, S = m->S;
+    PBSA_CUDA(cudaMemsetAsync(m->k_pool, 0, U * S * 64 * m->d * 2, s));
+    PBSA_CUDA(cudaMemsetAsync(m->v_pool, 0, U * S * 64 * m->d * 2, s));
+    PBSA_CUDA(cudaMemsetAsync(m->krep, 0, U * S * m->d * 4, s));
+    m->counts = MemCounts{0, 0, 0, m->S - m->bpc, 0};
+    m->last_k = 0;
+    m->last_n_keys = 0;
+    return launch_mem_init(m->dev, m->units, m->C, m->Lcap, m->bpc, m->S, s);
+}
+
+int pbsa_mem_get_info(const pbsa_mem* m, pbsa_mem_info* info) {
+    PBSA_REQUIRE(m != nullptr && info != nullptr, "mem_get_info: null pointer");
+    std::memset(info, 0, sizeof(*info));
+    info->units = m->units;
+    info->capacity_c = m->C;
+    info->window_chunks = m->W;
+    info->blocks_per_chunk = m->bpc;
+    info->b = m->b;
+    info->d = m->d;
+    info->n_slots = m->S;
+    info->n_p = m->counts.n_p;
+    info->n_sinks = m->counts.n_sinks;
+    info->n_l = m->counts.n_l;
+    info->chunks_committed = m->counts.chunk;
+    info->k_pool = m->k_pool;
+    info->v_pool = m->v_pool;
+    info->krep = m->krep;
+    info->dense_slots = m->dev.dense;
+    info->local_slots = m->dev.l_slot;
+    info->key_slots = m->dev.keys;
+    info->stage_slots = m->dev.stage;
+    info->p_ids = m->dev.p_id;
+    info->p_scores = m->dev.p_score;
+    info->l_ids = m->dev.l_id;
+    info->dense_stride = m->C + m->bpc;
+    info->local_stride = m->Lcap;
+    info->key_stride = m->S;
+    return PBSA_OK;
+}
+
+int pbsa_mem_write_chunk(pbsa_mem* m, const void* k_chunk, const void* v_chunk, void* stream) {
+    PBSA_REQUIRE(m != nullptr && k_chunk != nullptr && v_chunk != nullptr, "mem_write_chunk: null pointer");
+    PBSA_REQUIRE(aligned16(k_chunk) && aligned16(v_chunk), "mem_write_chunk: chunk must be 16-byte aligned");
+    cudaStream_t s = as_stream(stream);
+    const bool prof = m->prof_on && m->prof_write < m->prof_max;
+    if (prof) cudaEventRecord(m->ev_write[static_cast<size_t>(m->prof_write) * 2], s);
+    const int rc = launch_write_chunk(static_cast<const bf16*>(k_chunk), static_cast<const bf16*>(v_chunk),
+                                      m->dev.stage, m->bpc, m->b, m->d, m->units, m->S, m->k_pool, m->v_pool,
+                                      m->krep, s);
+    if (prof) {
+        cudaEventRecord(m->ev_write[static_cast<size_t>(m->prof_write) * 2 + 1], s);
+        ++m->prof_write;
+    }
+    return rc;
+}
+
+int pbsa_mem_profile(pbsa_mem* m, int enable, int max_calls) {
+    PBSA_REQUIRE(m != nullptr, "mem_profile: null memory");
+    free_events(m);
+    if (!enable) return PBSA_OK;
+    PBSA_REQUIRE(max_calls >= 1, "mem_profile: max_calls must be >= 1");
+    m->ev_attend.resize(static_cast<size_t>(max_calls) * 5);
+    m->ev_write.resize(static_cast<size_t>(max_calls) * 2);
+    for (auto& e : m->ev_attend) PBSA_CUDA(cudaEventCreate(&e));
+    for (auto& e : m->ev_write) PBSA_CUDA(cudaEventCreate(&e));
+    m->prof_max = max_calls;
+    m->prof_on = true;
+    return PBSA_OK;
+}
+
+int pbsa_mem_profile_read(pbsa_mem* m, double* stage_ms, int* n_attend, int* n_write) {
+    PBSA_REQUIRE(m != nullptr && stage_ms != nullptr, "mem_profile_read: null pointer");
+    for (int i = 0; i < 5; ++i) stage_ms[i] = 0.0;
+    if (n_attend) *n_attend = m->prof_attend;
+    if (n_write) *n_write = m->prof_write;
+    if (!m->prof_on) return PBSA_OK;
+    for (int c = 0; c < m->prof_write; ++c) {
+        float ms = 0.0f;
+        PBSA_CUDA(cudaEventSynchronize(m->ev_write[static_cast<size_t>(c) * 2 + 1]));
+        PBSA_CUDA(cudaEventElapsedTime(&ms, m->ev_write[static_cast<size_t>(c) * 2], m->ev_write[static_cast<size_t>(c) * 2 + 1]));
+        stage_ms[0] += ms;
+    }
+    for (int c = 0; c < m->prof_attend; ++c) {
+        cudaEvent_t* e = &m->ev_attend[static_cast<size_t>(c) * 5];
+        PBSA_CUDA(cudaEventSynchronize(e[4]));
+        for (int i = 0; i < 4; ++i) {
+            float ms = 0.0f;
+            PBSA_CUDA(cudaEventElapsedTime(&ms, e[i], e[i + 1]));
+            stage_ms[1 + i] += ms;
+        }
+    }
+    return PBSA_OK;
+}
+
+int pbsa_mem_commit(pbsa_mem* m, const float* s_t, void* stream) {
+    PBSA_REQUIRE(m != nullptr && s_t != nullptr, "mem_commit: null pointer");
+    int dropped = 0;
+    const MemCounts nxt = next_counts(m, m->counts, &dropped);
+    PBSA_REQUIRE(nxt.n_free >= 0, "mem_commit: slot pool exhausted (internal geometry error)");
+    const int rc = launch_mem_commit(m->dev, s_t, m->units, m->C, m->Lcap, m->bpc, m->S, m->counts, nxt,
+                                     as_stream(stream));
+    if (rc == PBSA_OK) m->counts = nxt;
+    return rc;
+}
+
+int pbsa_attend(pbsa_mem* m, const void* q, int k_top, float scale, int mode, void* o, float* lse,
+                void* stream) {
+    PBSA_REQUIRE(m != nullptr && q != nullptr && o != nullptr, "attend: null pointer");
+    PBSA_REQUIRE(mode == PBSA_MODE_DENOISE || mode == PBSA_MODE_CACHE_UPDATE, "attend: unknown mode");
+    PBSA_REQUIRE(k_top >= 0, "attend: k_top must be >= 0");
+    PBSA_REQUIRE(aligned16(q) && aligned16(o), "attend: q / o must be 16-byte aligned");
+    cudaStream_t s = as_stream(stream);
+    if (!(scale > 0.0f)) scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(m->d)));
+    const int U = m->units, bpc = m->bpc, b = m->b, d = m->d;
+    const int n_p = m->counts.n_p, n_l = m->counts.n_l;
+    const int k = n_l == 0 ? 0 : (k_top < n_l ? k_top : n_l);
+    prof_mark(m, 0, s);
+    // (a) query-block representatives
+    if (int rc = launch_compress(static_cast<const bf16*>(q), static_cast<int64_t>(bpc) * b * d,
+                                 static_cast<int64_t>(b) * d, nullptr, bpc, U, b, d, m->qc,
+                                 static_cast<int64_t>(bpc) * d, s))
+        return rc;
+    prof_mark(m, 1, s);
+    // (b) coarse scoring + Top-K (+ s_t over P ++ L ++ current at the k=0 pass)
+    const bool update = mode == PBSA_MODE_CACHE_UPDATE;
+    if (update) {
+        const int n_keys = n_p + n_l + bpc;
+        if (int rc = launch_score_select(m->qc, m->krep, static_cast<int64_t>(m->S) * d, m->dev.keys, m->S,
+                                         n_keys, n_p, n_l, k, bpc, U, d, scale, m->sel, m->s_t, m->ws,
+                                         m->ws_bytes, s))
+            return rc;
+        m->last_n_keys = n_keys;
+    } else if (k > 0) {
+        if (int rc = launch_score_select(m->qc, m->krep, static_cast<int64_t>(m->S) * d, m->dev.l_slot, m->Lcap,
+                                         n_l, 0, n_l, k, bpc, U, d, scale, m->sel, nullptr, m->ws,
+                                         m->ws_bytes, s))
+            return rc;
+    }
+    m->last_k = k;
+    prof_mark(m, 2, s);
+    // (c) block-sparse attention over P ++ current (dense) and the selected local blocks
+    if (int rc = launch_bsa_fwd(static_cast<const bf16*>(q), m->k_pool, m->v_pool, m->S, m->dev.dense,
+                                m->C + bpc, n_p + bpc, m->dev.l_slot, m->Lcap, n_l, m->sel, k, bpc, b, d, U,
+                                scale, static_cast<bf16*>(o), lse, s))
+        return rc;
+    prof_mark(m, 3, s);
+    // (d) persistent-memory update after the k=0 pass
+    int rc = PBSA_OK;
+    if (update) rc = pbsa_mem_commit(m, m->s_t, stream);
+    prof_mark(m, 4, s);
+    if (m->prof_on && m->prof_attend < m->prof_max) ++m->prof_attend;
+    return rc;
+}
+
+int pbsa_last_selection(const pbsa_mem* m, const int32_t** sel, int* k, const float** s_t, int* n_keys) {
+    PBSA_REQUIRE(m != nullptr, "last_selection: null memory");
+    if (sel) *sel = m->sel;
+    if (k) *k = m->last_k;
+    if (s_t) *s_t = m->s_t;
+    if (n_keys) *n_keys = m->last_n_keys;
+    return PBSA_OK;
+}
+
+}  // extern "C"

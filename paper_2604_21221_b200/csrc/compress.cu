@@ -1,0 +1,166 @@
+// compress.cu -- K1 block compression (+ the fused current-chunk KV write).
+//
+// Reference op: router.compress_blocks: representative = mean of the b token
+// vectors of a block (average pooling).  Numerics pinned to the oracle
+// (the CPU restatement in oracle/pbsa_oracle.cpp): fp64 sum in ascending token order, one IEEE
+// division by b, cast to fp32 -> bit-exact for any input.
+//
+// Roofline: HBM.  Algorithmic bytes per block = b*d*2 (bf16 read) + d*4 (f32 write).  One warp
+// per block; lane l owns columns [l*C, l*C+C), C = d/32, so each token row is one coalesced
+// 256-byte (d=128) warp load; rows are unrolled 4-deep for memory-level parallelism.  The fp64
+// adds (one per element) stay far below the DADD rate at HBM speed.
+#include "internal.h"
+
+namespace pbsa {
+namespace {
+
+template <int C>
+struct Vec;
+template <>
+struct Vec<4> {
+    using T = uint2;  // 4 x bf16
+};
+template <>
+struct Vec<2> {
+    using T = uint32_t;  // 2 x bf16
+};
+
+template <int C>
+__device__ __forceinline__ void unpack(const typename Vec<C>::T& v, float (&f)[C]) {
+    if constexpr (C == 4) {
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+        float2 a = __bfloat1622float2(h[0]), b = __bfloat1622float2(h[1]);
+        f[0] = a.x; f[1] = a.y; f[2] = b.x; f[3] = b.y;
+    } else {
+        float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v));
+        f[0] = a.x; f[1] = a.y;
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) compress_kernel(const bf16* __restrict__ x, int64_t xu, int64_t xb,
+                                                       const int32_t* __restrict__ map, int nb,
+                                                       int units, int b, float* __restrict__ reps,
+                                                       int64_t ru) {
+    constexpr int C = D / 32;
+    using V = typename Vec<C>::T;
+    const int64_t w = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
+    if (w >= static_cast<int64_t>(nb) * units) return;
+    const int lane = threadIdx.x & 31;
+    const int u = static_cast<int>(w / nb), i = static_cast<int>(w % nb);
+    const int idx = map ? __ldg(map + static_cast<int64_t>(u) * nb + i) : i;
+    const V* src = reinterpret_cast<const V*>(x + u * xu + idx * xb) + lane;
+    double acc[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc[c] = 0.0;
+    int t = 0;
+    for (; t + 4 <= b; t += 4) {
+        V v[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) v[r] = __ldg(src + (t + r) * (D / C));
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            float f[C];
+            unpack<C>(v[r], f);
+#pragma unroll
+            for (int c = 0; c < C; ++c) acc[c] += static_cast<double>(f[c]);
+        }
+    }
+    for (; t < b; ++t) {
+        float f[C];
+        unpack<C>(__ldg(src + t * (D / C)), f);
+#pragma unroll
+        for (int c = 0; c < C; ++c) acc[c] += static_cast<double>(f[c]);
+    }
+    float* dst = reps + u * ru + static_cast<int64_t>(idx) * D + lane * C;
+    const double db = static_cast<double>(b);
+#pragma unroll
+    for (int c = 0; c < C; ++c) dst[c] = __double2float_rn(__ddiv_rn(acc[c], db));
+}
+
+// Writes block i of the current chunk (rows [i*b, i*b+b) of kc / vc) into pool slot stage[u][i]
+// rows [0, b) and its K representative into krep[u][slot].  Pool rows >= b are never written
+// (zeroed at creation), which is what the attention kernel's padding logic relies on.
+template <int D>
+__global__ void __launch_bounds__(256) write_chunk_kernel(const bf16* __restrict__ kc,
+                                                          const bf16* __restrict__ vc,
+                                                          const int32_t* __restrict__ stage, int bpc,
+                                                          int b, int units, int n_slots,
+                                                          bf16* __restrict__ kp, bf16* __restrict__ vp,
+                                                          float* __restrict__ krep) {
+    constexpr int C = D / 32;
+    using V = typename Vec<C>::T;
+    const int64_t w = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
+    if (w >= static_cast<int64_t>(bpc) * units) return;
+    const int lane = threadIdx.x & 31;
+    const int u = static_cast<int>(w / bpc), i = static_cast<int>(w % bpc);
+    const int slot = __ldg(stage + static_cast<int64_t>(u) * bpc + i);
+    const int64_t src_off = (static_cast<int64_t>(u) * bpc + i) * b * D;
+    const int64_t dst_off = (static_cast<int64_t>(u) * n_slots + slot) * 64 * D;
+    const V* ks = reinterpret_cast<const V*>(kc + src_off) + lane;
+    const V* vs = reinterpret_cast<const V*>(vc + src_off) + lane;
+    V* kd = reinterpret_cast<V*>(kp + dst_off) + lane;
+    V* vd = reinterpret_cast<V*>(vp + dst_off) + lane;
+    double acc[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc[c] = 0.0;
+    int t = 0;
+    for (; t + 4 <= b; t += 4) {
+        V kv[4], vv[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            kv[r] = __ldg(ks + (t + r) * (D / C));
+            vv[r] = __ldg(vs + (t + r) * (D / C));
+        }
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            kd[(t + r) * (D / C)] = kv[r];
+            vd[(t + r) * (D / C)] = vv[r];
+            float f[C];
+            unpack<C>(kv[r], f);
+#pragma unroll
+            for (int c = 0; c < C; ++c) acc[c] += static_cast<double>(f[c]);
+        }
+    }
+    for (; t < b; ++t) {
+        V kv = __ldg(ks + t * (D / C));
+        kd[t * (D / C)] = kv;
+        vd[t * (D / C)] = __ldg(vs + t * (D / C));
+        float f[C];
+        unpack<C>(kv, f);
+#pragma unroll
+        for (int c = 0; c < C; ++c) acc[c] += static_cast<double>(f[c]);
+    }
+    float* dst = krep + (static_cast<int64_t>(u) * n_slots + slot) * D + lane * C;
+    const double db = static_cast<double>(b);
+#pragma unroll
+    for (int c = 0; c < C; ++c) dst[c] = __double2float_rn(__ddiv_rn(acc[c], db));
+}
+
+}  // namespace
+
+int launch_compress(const bf16* x, int64_t xu, int64_t xb, const int32_t* map, int nb, int units,
+                    int b, int d, float* reps, int64_t ru, cudaStream_t s) {
+    const int64_t warps = static_cast<int64_t>(nb) * units;
+    if (warps == 0) return 0;
+    const int grid = static_cast<int>((warps + 7) / 8);
+    if (d == 128)
+        compress_kernel<128><<<grid, 256, 0, s>>>(x, xu, xb, map, nb, units, b, reps, ru);
+    else
+        compress_kernel<64><<<grid, 256, 0, s>>>(x, xu, xb, map, nb, units, b, reps, ru);
+    return check_launch("compress_kernel");
+}
+
+int launch_write_chunk(const bf16* kc, const bf16* vc, const int32_t* stage, int bpc, int b, int d,
+                       int units, int n_slots, bf16* kp, bf16* vp, float* krep, cudaStream_t s) {
+    const int64_t warps = static_cast<int64_t>(bpc) * units;
+    if (warps == 0) return 0;
+    const int grid = static_cast<int>((warps + 7) / 8);
+    if (d == 128)
+        write_chunk_kernel<128><<<grid, 256, 0, s>>>(kc, vc, stage, bpc, b, units, n_slots, kp, vp, krep);
+    else
+        write_chunk_kernel<64><<<grid, 256, 0, s>>>(kc, vc, stage, bpc, b, units, n_slots, kp, vp, krep);
+    return check_launch("write_chunk_kernel");
+}
+
+}  // namespace pbsa

@@ -1,0 +1,64 @@
+// internal.h -- shared declarations of the PBSA B200 library (not part of the public ABI).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/pbsa_b200.h"
+
+namespace pbsa {
+
+using bf16 = __nv_bfloat16;
+
+int set_error(int code, const std::string& msg);
+int check_launch(const char* what);
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// K1
+int launch_compress(const bf16* x, int64_t x_unit_stride, int64_t x_block_stride, const int32_t* map,
+                    int n_blocks, int units, int b, int d, float* reps, int64_t reps_unit_stride,
+                    cudaStream_t s);
+int launch_write_chunk(const bf16* kc, const bf16* vc, const int32_t* stage, int bpc, int b, int d,
+                       int units, int n_slots, bf16* k_pool, bf16* v_pool, float* krep,
+                       cudaStream_t s);
+// K2
+size_t score_select_workspace(int units, int nqb, int n_keys);
+int launch_score_select(const float* qc, const float* krep, int64_t krep_unit_stride,
+                        const int32_t* key_slots, int key_stride, int n_keys, int local_off,
+                        int n_local, int k, int nqb, int units, int d, float scale, int32_t* sel,
+                        float* s_t, void* ws, size_t ws_bytes, cudaStream_t s);
+// K3
+int launch_bsa_fwd(const bf16* q, const bf16* k_pool, const bf16* v_pool, int n_slots,
+                   const int32_t* dense, int dense_stride, int n_dense, const int32_t* local,
+                   int local_stride, int n_local, const int32_t* sel, int k, int nqb, int b, int d,
+                   int units, float scale, bf16* o, float* lse, cudaStream_t s);
+int launch_debug_tile(const bf16* q, const bf16* k, const bf16* v, int d, float* s_out,
+                      float* o_out, cudaStream_t s);
+// K4
+struct MemDev {
+    int32_t* p_slot;   // [U][C]
+    int64_t* p_id;     // [U][C]
+    float* p_score;    // [U][C]
+    int32_t* l_slot;   // [U][Lcap]
+    int64_t* l_id;     // [U][Lcap]
+    int32_t* stage;    // [U][bpc]
+    int32_t* free_slot;  // [U][S]
+    int32_t* dense;    // [U][C+bpc]
+    int32_t* keys;     // [U][S]
+};
+struct MemCounts {
+    int n_p, n_sinks, n_l, n_free;
+    int64_t chunk;  // index of the chunk held in the stage slots
+};
+int launch_mem_init(const MemDev& m, int units, int C, int Lcap, int bpc, int S, cudaStream_t s);
+int launch_mem_commit(const MemDev& m, const float* s_t, int units, int C, int Lcap, int bpc, int S,
+                      const MemCounts& cur, const MemCounts& next, cudaStream_t s);
+
+// TMA descriptor encoding through the driver entry point (no -lcuda link dependency)
+bool encode_tmap_bf16(void* tmap, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+                      const uint32_t* box, std::string* err);
+
+}  // namespace pbsa

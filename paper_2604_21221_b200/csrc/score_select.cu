@@ -1,0 +1,261 @@
+// score_select.cu -- K2 coarse scoring, row-wise Top-K selection and score aggregation.
+//
+// Reference ops (Eq. 7-8, Eq. 10-11):
+//   logits  z[i][j] = float(sum_c double(qc[i][c]) * double(kc[j][c]))  (tensor.cpp:34-55, ascending c)
+//                     * scale                                           (fp32 multiply)
+//   A_L     = masked_softmax_rows(z over the local keys)                 (tensor.cpp:57-108)
+//   Omega   = k largest of A_L by (value desc, index asc), emitted ascending
+//   k=0 pass: A_t = softmax over all keys, s_t[j] = float(sum_i double(A_t[i][j]) / nqb)
+// Every rounding step is reproduced exactly (same operation order as the oracle), so the
+// selected indices and s_t are bit-exact with oracle/pbsa_oracle.cpp.  The only transcendental
+// is the fp64 exp; see DESIGN.md "bit-exactness" for the residual-risk argument.
+//
+// Three kernels:
+//   coarse_logits_kernel  thread per key block, R query blocks per CTA (amortises krep reads)
+//   select_kernel         warp per query-block row: softmax (fp64 exp, sequential ascending
+//                         denominator on lane 0 exactly like the oracle), 4-pass 8-bit radix
+//                         select on the fp32 probability bits, ballot compaction of the winners
+//   aggregate_kernel      thread per key block, ascending-row fp64 column sums (k=0 pass only)
+#include <cfloat>
+
+#include "internal.h"
+
+namespace pbsa {
+namespace {
+
+constexpr int kLogitRows = 8;
+
+template <int D, int R>
+__global__ void __launch_bounds__(128) coarse_logits_kernel(
+    const float* __restrict__ qc, const float* __restrict__ krep, int64_t kru,
+    const int32_t* __restrict__ keys, int key_stride, int n_keys, int nqb, float scale,
+    float* __restrict__ logits) {
+    __shared__ float qs[R][D];
+    const int u = blockIdx.y;
+    const int i0 = blockIdx.x * R;
+    const int nr = min(R, nqb - i0);
+    for (int e = threadIdx.x; e < R * D; e += blockDim.x) {
+        const int r = e / D, c = e % D;
+        qs[r][c] = r < nr ? qc[(static_cast<int64_t>(u) * nqb + i0 + r) * D + c] : 0.0f;
+    }
+    __syncthreads();
+    const int j = blockIdx.z * blockDim.x + threadIdx.x;
+    if (j >= n_keys) return;
+    const int slot = __ldg(keys + static_cast<int64_t>(u) * key_stride + j);
+    const float4* kr = reinterpret_cast<const float4*>(krep + u * kru + static_cast<int64_t>(slot) * D);
+    double acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.0;
+#pragma unroll 4
+    for (int c4 = 0; c4 < D / 4; ++c4) {
+        const float4 kv = __ldg(kr + c4);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {  // ascending c per row: x, y, z, w
+            acc[r] = __fma_rn(static_cast<double>(qs[r][4 * c4 + 0]), static_cast<double>(kv.x), acc[r]);
+            acc[r] = __fma_rn(static_cast<double>(qs[r][4 * c4 + 1]), static_cast<double>(kv.y), acc[r]);
+            acc[r] = __fma_rn(static_cast<double>(qs[r][4 * c4 + 2]), static_cast<double>(kv.z), acc[r]);
+            acc[r] = __fma_rn(static_cast<double>(qs[r][4 * c4 + 3]), static_cast<double>(kv.w), acc[r]);
+        }
+    }
+    // fp32 x fp32 products are exact in fp64, so fma == mul-then-add of the oracle.
+    for (int r = 0; r < nr; ++r)
+        logits[(static_cast<int64_t>(u) * nqb + i0 + r) * n_keys + j] =
+            __fmul_rn(__double2float_rn(acc[r]), scale);
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// masked_softmax_rows (no mask) of z[0..n) for one row, by one warp.  e[] is fp64 scratch.
+// Writes the fp32 probabilities' bit patterns to out_bits (or floats to out_f).
+__device__ void warp_softmax(const float* z, int n, double* e, uint32_t* out_bits, float* out_f) {
+    const int lane = threadIdx.x & 31;
+    float m = -FLT_MAX;
+    for (int j = lane; j < n; j += 32) m = fmaxf(m, z[j]);
+    m = warp_max(m);
+    const double dm = static_cast<double>(m);
+    for (int j = lane; j < n; j += 32) e[j] = exp(static_cast<double>(z[j]) - dm);
+    __syncwarp();
+    double denom = 0.0;
+    if (lane == 0) {  // ascending-j fp64 accumulation, exactly as tensor.cpp:96-102
+        for (int j = 0; j < n; ++j) denom = __dadd_rn(denom, e[j]);
+    }
+    denom = __shfl_sync(0xffffffffu, denom, 0);
+    for (int j = lane; j < n; j += 32) {
+        const float p = __double2float_rn(__ddiv_rn(e[j], denom));
+        if (out_bits) out_bits[j] = __float_as_uint(p);
+        if (out_f) out_f[j] = p;
+    }
+    __syncwarp();
+}
+
+// k largest of pb[0..n) (non-negative float bits => unsigned order), ties -> lower index.
+// Writes the winners' indices ascending to out[0..k).
+__device__ void warp_topk(const uint32_t* pb, int n, int k, uint32_t* hist, int32_t* out) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t lt = (1u << lane) - 1u;
+    uint32_t prefix = 0, pmask = 0;
+    int kk = k;  // still to pick at/below the current prefix
+#pragma unroll 1
+    for (int shift = 24; shift >= 0; shift -= 8) {
+#pragma unroll
+        for (int t = 0; t < 8; ++t) hist[lane * 8 + t] = 0;
+        __syncwarp();
+        for (int j = lane; j < n; j += 32) {
+            const uint32_t v = pb[j];
+            if ((v & pmask) == prefix) atomicAdd(&hist[(v >> shift) & 255u], 1u);
+        }
+        __syncwarp();
+        // lane l owns digits [255-8l-7, 255-8l] (lane 0 the largest)
+        uint32_t sum = 0;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) sum += hist[255 - lane * 8 - t];
+        uint32_t incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t excl = incl - sum;
+        const bool mine = excl < static_cast<uint32_t>(kk) && static_cast<uint32_t>(kk) <= incl;
+        uint32_t dgt = 0, above = 0;
+        if (mine) {
+            uint32_t cum = excl;
+            for (int t = 0; t < 8; ++t) {
+                const uint32_t bin = 255 - lane * 8 - t;
+                const uint32_t h = hist[bin];
+                if (cum + h >= static_cast<uint32_t>(kk)) {
+                    dgt = bin;
+                    above = cum;
+                    break;
+                }
+                cum += h;
+            }
+        }
+        const uint32_t who = __ffs(__ballot_sync(0xffffffffu, mine)) - 1;
+        dgt = __shfl_sync(0xffffffffu, dgt, who);
+        above = __shfl_sync(0xffffffffu, above, who);
+        kk -= static_cast<int>(above);
+        prefix |= dgt << shift;
+        pmask |= 255u << shift;
+        __syncwarp();
+    }
+    // prefix = value of the k-th largest element; take every element above it and the first kk
+    // (lowest indices) equal to it.
+    int run = 0, tie_run = 0;
+    for (int base = 0; base < n; base += 32) {
+        const int j = base + lane;
+        const uint32_t v = j < n ? pb[j] : 0u;
+        const bool gt = j < n && v > prefix;
+        const bool eq = j < n && v == prefix;
+        const uint32_t eb = __ballot_sync(0xffffffffu, eq);
+        const int tie_rank = tie_run + __popc(eb & lt);
+        const bool take = gt || (eq && tie_rank < kk);
+        const uint32_t tb = __ballot_sync(0xffffffffu, take);
+        if (take) out[run + __popc(tb & lt)] = j;
+        run += __popc(tb);
+        tie_run += __popc(eb);
+    }
+}
+
+struct SelectParams {
+    const float* logits;  // [U][nqb][n_keys]
+    int n_keys, local_off, n_local, k, nqb, units, rows_per_cta;
+    size_t per_warp;      // bytes of smem per warp (16-aligned)
+    int32_t* sel;         // [U][nqb][k]
+    float* arows;         // [U][nqb][n_keys] or null
+};
+
+__global__ void __launch_bounds__(256) select_kernel(const SelectParams p) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+    const int64_t row = static_cast<int64_t>(blockIdx.x) * p.rows_per_cta + warp;
+    if (warp >= p.rows_per_cta || row >= static_cast<int64_t>(p.units) * p.nqb) return;
+    const int n = p.n_keys;
+    uint8_t* base = smem + p.per_warp * warp;
+    double* e = reinterpret_cast<double*>(base);
+    float* z = reinterpret_cast<float*>(base + static_cast<size_t>(n) * 8);
+    uint32_t* pb = reinterpret_cast<uint32_t*>(base + static_cast<size_t>(n) * 12);
+    uint32_t* hist = pb + p.n_local;
+    const float* src = p.logits + row * n;
+    for (int j = lane; j < n; j += 32) z[j] = src[j];
+    __syncwarp();
+    if (p.k > 0 && p.n_local > 0) {
+        warp_softmax(z + p.local_off, p.n_local, e, pb, nullptr);
+        warp_topk(pb, p.n_local, p.k, hist, p.sel + row * p.k);
+    }
+    if (p.arows != nullptr) warp_softmax(z, n, e, nullptr, p.arows + row * n);
+}
+
+__global__ void aggregate_kernel(const float* __restrict__ arows, int n_keys, int nqb, int units,
+                                 float* __restrict__ s_t) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    const int u = blockIdx.y;
+    if (j >= n_keys) return;
+    const float* a = arows + static_cast<int64_t>(u) * nqb * n_keys + j;
+    double acc = 0.0;
+    for (int i = 0; i < nqb; ++i) acc = __dadd_rn(acc, static_cast<double>(a[static_cast<int64_t>(i) * n_keys]));
+    s_t[static_cast<int64_t>(u) * n_keys + j] = __double2float_rn(__ddiv_rn(acc, static_cast<double>(nqb)));
+}
+
+}  // namespace
+
+size_t score_select_workspace(int units, int nqb, int n_keys) {
+    const size_t one = static_cast<size_t>(units) * nqb * n_keys * sizeof(float);
+    return 2 * one + 256;
+}
+
+int launch_score_select(const float* qc, const float* krep, int64_t kru, const int32_t* keys,
+                        int key_stride, int n_keys, int local_off, int n_local, int k, int nqb,
+                        int units, int d, float scale, int32_t* sel, float* s_t, void* ws,
+                        size_t ws_bytes, cudaStream_t s) {
+    if (units == 0 || nqb == 0 || n_keys == 0) return 0;
+    const bool do_select = k > 0 && n_local > 0;
+    if (!do_select && s_t == nullptr) return 0;
+    if (ws_bytes < score_select_workspace(units, nqb, n_keys))
+        return set_error(PBSA_EINVAL, "score_select: workspace too small");
+    float* logits = static_cast<float*>(ws);
+    float* arows = s_t ? logits + static_cast<size_t>(units) * nqb * n_keys : nullptr;
+    {
+        dim3 grid((nqb + kLogitRows - 1) / kLogitRows, units, (n_keys + 127) / 128);
+        if (d == 128)
+            coarse_logits_kernel<128, kLogitRows><<<grid, 128, 0, s>>>(qc, krep, kru, keys, key_stride,
+                                                                       n_keys, nqb, scale, logits);
+        else
+            coarse_logits_kernel<64, kLogitRows><<<grid, 128, 0, s>>>(qc, krep, kru, keys, key_stride,
+                                                                      n_keys, nqb, scale, logits);
+        if (int rc = check_launch("coarse_logits_kernel")) return rc;
+    }
+    {
+        const size_t per_warp =
+            (static_cast<size_t>(n_keys) * 12 + static_cast<size_t>(n_local) * 4 + 1024 + 15) & ~size_t(15);
+        const size_t budget = 200 * 1024;
+        if (per_warp > budget)
+            return set_error(PBSA_EUNSUPPORTED, "score_select: too many key blocks for one row in smem");
+        int rows = static_cast<int>(budget / per_warp);
+        rows = rows < 1 ? 1 : (rows > 8 ? 8 : rows);
+        SelectParams p{logits, n_keys, local_off, n_local, do_select ? k : 0, nqb, units, rows, per_warp,
+                       sel, arows};
+        const size_t smem = per_warp * rows;
+        static size_t configured = 0;
+        if (smem > 48 * 1024 && smem > configured) {
+            cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            configured = 227 * 1024;
+        }
+        const int64_t total = static_cast<int64_t>(units) * nqb;
+        const int grid = static_cast<int>((total + rows - 1) / rows);
+        select_kernel<<<grid, rows * 32, smem, s>>>(p);
+        if (int rc = check_launch("select_kernel")) return rc;
+    }
+    if (s_t) {
+        dim3 grid((n_keys + 127) / 128, units);
+        aggregate_kernel<<<grid, 128, 0, s>>>(arows, n_keys, nqb, units, s_t);
+        if (int rc = check_launch("aggregate_kernel")) return rc;
+    }
+    return 0;
+}
+
+}  // namespace pbsa

@@ -1,0 +1,266 @@
+"""Host-side mirror of the reference's PBSA operator API over the C ABI.
+
+Names, argument meaning and error behaviour follow /root/reference/SPEC.md (modules router,
+attention, memory) so callers and tests read like the reference's.  Tensors live on the GPU
+(torch is only the device-memory / stream plumbing); every op launches the sm_100a kernels of
+libpbsa_b200.so on the current torch stream.  Invalid arguments raise PbsaError (a ValueError,
+the analogue of the reference's std::invalid_argument), CUDA failures PbsaCudaError.
+
+    compress_blocks     SPEC.md:268  router.compress_blocks          -> K1
+    score_select        SPEC.md:277-303  coarse_attention + select_topk (+ aggregate_scores) -> K2
+    attention_sparse    SPEC.md:367  attention.attention_sparse       -> K3
+    Memory              SPEC.md:160-243  PersistentMemory + LocalWindow, push_chunk,
+                        update_persistent, assemble_kv                 -> K4 (+ fused KV write)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import torch
+
+from . import _capi
+from ._capi import LIB, PbsaCudaError, PbsaError, check  # noqa: F401
+
+__all__ = ["compress_blocks", "score_select", "attention_sparse", "Memory", "attention_scale",
+           "topk_count", "PbsaError", "PbsaCudaError", "debug_tile", "MODE_DENOISE",
+           "MODE_CACHE_UPDATE"]
+
+MODE_DENOISE = _capi.MODE_DENOISE
+MODE_CACHE_UPDATE = _capi.MODE_CACHE_UPDATE
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _need(t: torch.Tensor, dtype, name: str) -> None:
+    if not t.is_cuda:
+        raise PbsaError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise PbsaError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise PbsaError(f"{name} must be contiguous")
+
+
+def attention_scale(d: int) -> float:
+    """AttentionConfig.scale = d^-1/2, rounded to fp32 like the oracle."""
+    return float(torch.tensor(1.0 / math.sqrt(d), dtype=torch.float32))
+
+
+def topk_count(n_local: int, topk_ratio: float) -> int:
+    """k = max(1, ceil(N_l^blk * ratio)); empty local region is an error."""
+    if n_local < 1:
+        raise PbsaError("select_topk: empty local region")
+    if not (0.0 < topk_ratio <= 1.0):
+        raise PbsaError("select_topk: topk_ratio must be in (0,1]")
+    return min(n_local, max(1, math.ceil(n_local * topk_ratio)))
+
+
+def compress_blocks(x: torch.Tensor, block_map: torch.Tensor | None = None,
+                    out: torch.Tensor | None = None) -> torch.Tensor:
+    """Mean-pool each block.  x: [units, n_blocks, b, d] bf16 (or a slot pool
+    [units, n_slots, 64, d] with block_map [units, n_blocks] selecting slots and b given by the
+    pool rows actually holding tokens -- see Memory).  Returns [units, n_blocks, d] f32 (or
+    writes `out` at the mapped rows)."""
+    _need(x, torch.bfloat16, "x")
+    units, nb, b, d = x.shape
+    if block_map is None:
+        if out is None:
+            out = torch.empty(units, nb, d, device=x.device, dtype=torch.float32)
+        check(LIB.pbsa_compress(x.data_ptr(), nb * b * d, b * d, None, nb, units, b, d,
+                                out.data_ptr(), out.shape[1] * d, _stream()))
+        return out
+    raise PbsaError("compress_blocks: use Memory for slot-mapped compression")
+
+
+def score_select(qc: torch.Tensor, krep: torch.Tensor, key_slots: torch.Tensor, local_off: int,
+                 n_local: int, k: int, scale: float | None = None, n_keys: int | None = None,
+                 want_scores: bool = False):
+    """Coarse attention + row-wise Top-K (+ Eq. 8 scores).
+
+    qc [units, nqb, d] f32; krep [units, n_slots, d] f32 (block representative per slot);
+    key_slots [units, key_stride] int32 -- the first n_keys entries are the key blocks, of which
+    [local_off, local_off+n_local) form the local window.  Returns sel [units, nqb, k] int32
+    (local indices, ascending) and, if want_scores, s_t [units, n_keys] f32."""
+    _need(qc, torch.float32, "qc")
+    _need(krep, torch.float32, "krep")
+    _need(key_slots, torch.int32, "key_slots")
+    units, nqb, d = qc.shape
+    n_keys = key_slots.shape[1] if n_keys is None else n_keys
+    scale = attention_scale(d) if scale is None else scale
+    sel = torch.empty(units, nqb, max(k, 1), device=qc.device, dtype=torch.int32)
+    s_t = torch.empty(units, n_keys, device=qc.device, dtype=torch.float32) if want_scores else None
+    ws_bytes = LIB.pbsa_score_select_workspace(units, nqb, n_keys)
+    ws = torch.empty(ws_bytes, device=qc.device, dtype=torch.uint8)
+    check(LIB.pbsa_score_select(qc.data_ptr(), krep.data_ptr(), krep.shape[1] * d,
+                                key_slots.data_ptr(), key_slots.shape[1], n_keys, local_off, n_local,
+                                k, nqb, units, d, scale, sel.data_ptr(), _ptr(s_t), ws.data_ptr(),
+                                ws_bytes, _stream()))
+    sel = sel[:, :, :k]
+    return (sel, s_t) if want_scores else sel
+
+
+def attention_sparse(q: torch.Tensor, k_pool: torch.Tensor, v_pool: torch.Tensor,
+                     dense_slots: torch.Tensor | None, local_slots: torch.Tensor | None,
+                     sel: torch.Tensor | None, b: int, scale: float | None = None,
+                     n_dense: int | None = None, n_local: int | None = None,
+                     want_lse: bool = False):
+    """Block-sparse attention forward.
+
+    q [units, nqb*b, d] bf16 (query tokens block-major); k_pool / v_pool [units, n_slots, 64, d]
+    bf16 with rows >= b zero; dense_slots [units, >=n_dense] int32 (persistent + current chunk,
+    visible to every query block); local_slots [units, >=n_local] int32; sel [units, nqb, k]
+    int32 ascending local indices.  Returns o [units, nqb*b, d] bf16 (and lse [units, nqb*b])."""
+    _need(q, torch.bfloat16, "q")
+    _need(k_pool, torch.bfloat16, "k_pool")
+    _need(v_pool, torch.bfloat16, "v_pool")
+    units, nq, d = q.shape
+    if nq % b:
+        raise PbsaError(f"attention_sparse: n_q ({nq}) not divisible by b ({b})")
+    nqb = nq // b
+    n_slots = k_pool.shape[1]
+    if k_pool.shape != (units, n_slots, 64, d) or v_pool.shape != k_pool.shape:
+        raise PbsaError("attention_sparse: pools must be [units, n_slots, 64, d]")
+    nd = 0 if dense_slots is None else (dense_slots.shape[1] if n_dense is None else n_dense)
+    nl = 0 if local_slots is None else (local_slots.shape[1] if n_local is None else n_local)
+    k = 0 if sel is None else sel.shape[2]
+    for name, t in (("dense_slots", dense_slots), ("local_slots", local_slots), ("sel", sel)):
+        if t is not None:
+            _need(t, torch.int32, name)
+    o = torch.empty_like(q)
+    lse = torch.empty(units, nq, device=q.device, dtype=torch.float32) if want_lse else None
+    scale = attention_scale(d) if scale is None else scale
+    check(LIB.pbsa_bsa_fwd(q.data_ptr(), k_pool.data_ptr(), v_pool.data_ptr(), n_slots,
+                           _ptr(dense_slots), 0 if dense_slots is None else dense_slots.shape[1], nd,
+                           _ptr(local_slots), 0 if local_slots is None else local_slots.shape[1], nl,
+                           _ptr(sel), k, nqb, b, d, units, scale, o.data_ptr(), _ptr(lse), _stream()))
+    return (o, lse) if want_lse else o
+
+
+def debug_tile(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor):
+    """One 128x64 tile through the tcgen05 path: returns (q k^T f32, bf16(q k^T) v f32)."""
+    d = q.shape[1]
+    s = torch.empty(128, 64, device=q.device, dtype=torch.float32)
+    o = torch.empty(128, d, device=q.device, dtype=torch.float32)
+    check(LIB.pbsa_debug_tile(q.data_ptr(), k.data_ptr(), v.data_ptr(), d, s.data_ptr(), o.data_ptr(),
+                              _stream()))
+    return s, o
+
+
+class Memory:
+    """Device-resident PBSA memory for `units` heads: PersistentMemory (capacity C blocks, sinks =
+    first chunk) + LocalWindow (window_chunks chunks) + the K/V slot pool."""
+
+    def __init__(self, units: int, capacity_c: int, window_chunks: int, blocks_per_chunk: int,
+                 b: int, d: int):
+        h = C.c_void_p()
+        check(LIB.pbsa_mem_create(C.byref(h), units, capacity_c, window_chunks, blocks_per_chunk,
+                                  b, d))
+        self._h = h
+        self.units, self.capacity_c, self.window_chunks = units, capacity_c, window_chunks
+        self.blocks_per_chunk, self.b, self.d = blocks_per_chunk, b, d
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            LIB.pbsa_mem_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- state ---------------------------------------------------------------------------
+    def info(self) -> _capi.MemInfo:
+        inf = _capi.MemInfo()
+        check(LIB.pbsa_mem_get_info(self._h, C.byref(inf)))
+        return inf
+
+    def reset(self) -> None:
+        check(LIB.pbsa_mem_reset(self._h, _stream()))
+
+    def _view(self, ptr: int, shape, dtype) -> torch.Tensor:
+        """Copy a device array of the state into a fresh tensor (for inspection / tests)."""
+        n = 1
+        for s in shape:
+            n *= s
+        esz = torch.empty(0, dtype=dtype).element_size()
+        out = torch.empty(shape, dtype=dtype, device="cuda")
+        if n:
+            check(LIB.pbsa_copy(out.data_ptr(), ptr, n * esz, _stream()))
+        return out
+
+    def assemble(self):
+        """assemble_kv as ids: (persistent ids [units, n_p] in order sinks id asc,
+        dynamic id asc; local ids [units, n_l] oldest -> newest)."""
+        inf = self.info()
+        p = self._view(inf.p_ids, (self.units, self.capacity_c), torch.int64)[:, :inf.n_p]
+        l_ = self._view(inf.l_ids, (self.units, inf.local_stride), torch.int64)[:, :inf.n_l]
+        return p, l_
+
+    def slot_tables(self):
+        inf = self.info()
+        dense = self._view(inf.dense_slots, (self.units, inf.dense_stride), torch.int32)
+        local = self._view(inf.local_slots, (self.units, inf.local_stride), torch.int32)
+        keys = self._view(inf.key_slots, (self.units, inf.key_stride), torch.int32)
+        stage = self._view(inf.stage_slots, (self.units, self.blocks_per_chunk), torch.int32)
+        return dense, local, keys, stage
+
+    def pools(self):
+        inf = self.info()
+        shp = (self.units, inf.n_slots, 64, self.d)
+        k = self._view(inf.k_pool, shp, torch.bfloat16)
+        v = self._view(inf.v_pool, shp, torch.bfloat16)
+        kr = self._view(inf.krep, (self.units, inf.n_slots, self.d), torch.float32)
+        return k, v, kr
+
+    # ---- hot path ------------------------------------------------------------------------
+    def write_chunk(self, k_chunk: torch.Tensor, v_chunk: torch.Tensor) -> None:
+        """The current chunk's K/V ([units, blocks_per_chunk*b, d] bf16) into the stage slots (+K1)."""
+        for name, t in (("k_chunk", k_chunk), ("v_chunk", v_chunk)):
+            _need(t, torch.bfloat16, name)
+            if t.shape != (self.units, self.blocks_per_chunk * self.b, self.d):
+                raise PbsaError(f"{name}: expected shape {(self.units, self.blocks_per_chunk * self.b, self.d)}")
+        check(LIB.pbsa_mem_write_chunk(self._h, k_chunk.data_ptr(), v_chunk.data_ptr(), _stream()))
+
+    def attend(self, q: torch.Tensor, k_top: int, mode: int = MODE_DENOISE, scale: float | None = None,
+               out: torch.Tensor | None = None, want_lse: bool = False):
+        """One PBSA call (Alg. 1 "Apply PBSA with Top-K"); mode MODE_CACHE_UPDATE = the k=0 pass
+        that also scores all key blocks and updates P / L."""
+        _need(q, torch.bfloat16, "q")
+        if q.shape != (self.units, self.blocks_per_chunk * self.b, self.d):
+            raise PbsaError("attend: q must be [units, blocks_per_chunk*b, d]")
+        o = torch.empty_like(q) if out is None else out
+        lse = torch.empty(q.shape[:2], device=q.device, dtype=torch.float32) if want_lse else None
+        check(LIB.pbsa_attend(self._h, q.data_ptr(), int(k_top), 0.0 if scale is None else float(scale),
+                              int(mode), o.data_ptr(), _ptr(lse), _stream()))
+        return (o, lse) if want_lse else o
+
+    def commit(self, s_t: torch.Tensor) -> None:
+        _need(s_t, torch.float32, "s_t")
+        check(LIB.pbsa_mem_commit(self._h, s_t.data_ptr(), _stream()))
+
+    def profile(self, enable: bool = True, max_calls: int = 4096) -> None:
+        """Per-stage CUDA-event timing of subsequent calls (see pbsa_mem_profile)."""
+        check(LIB.pbsa_mem_profile(self._h, int(enable), int(max_calls)))
+
+    def profile_read(self) -> dict:
+        ms = (C.c_double * 5)()
+        na, nw = C.c_int(), C.c_int()
+        check(LIB.pbsa_mem_profile_read(self._h, ms, C.byref(na), C.byref(nw)))
+        keys = ["kv_write", "compress_q", "score_select", "bsa_fwd", "mem_update"]
+        return {"ms": dict(zip(keys, list(ms))), "attend_calls": na.value, "kv_writes": nw.value}
+
+    def last_selection(self):
+        sel, k, st, nk = C.c_void_p(), C.c_int(), C.c_void_p(), C.c_int()
+        check(LIB.pbsa_last_selection(self._h, C.byref(sel), C.byref(k), C.byref(st), C.byref(nk)))
+        selt = self._view(sel.value, (self.units, self.blocks_per_chunk, max(k.value, 0)), torch.int32) \
+            if k.value else None
+        stt = self._view(st.value, (self.units, nk.value), torch.float32) if nk.value else None
+        return selt, stt

@@ -1,0 +1,64 @@
+"""CPU-only checks of the drop-in boundary: the C-ABI library loads (no GPU needed) and exports
+every symbol include/pbsa_b200.h declares; the Python binding covers exactly that set; the host
+API validates arguments before touching the device."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "pbsa_b200.h")
+LIB = os.path.join(ROOT, "paper_2604_21221_b200", "_lib", "libpbsa_b200.so")
+
+
+def declared():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(pbsa_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declares_the_hot_path():
+    names = declared()
+    for must in ["pbsa_compress", "pbsa_score_select", "pbsa_bsa_fwd", "pbsa_mem_create",
+                 "pbsa_mem_commit", "pbsa_mem_write_chunk", "pbsa_attend", "pbsa_last_error"]:
+        assert must in names
+
+
+@pytest.mark.skipif(not os.path.exists(LIB), reason="library not built")
+def test_library_exports_every_declared_symbol():
+    lib = C.CDLL(LIB)
+    missing = [n for n in declared() if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+@pytest.mark.skipif(not os.path.exists(LIB), reason="library not built")
+def test_python_binding_matches_header():
+    from paper_2604_21221_b200 import _capi
+    assert sorted(_capi.EXPORTED) == declared()
+
+
+@pytest.mark.skipif(not os.path.exists(LIB), reason="library not built")
+def test_argument_errors_need_no_gpu():
+    from paper_2604_21221_b200 import _capi
+    lib = _capi.LIB
+    h = C.c_void_p()
+    assert lib.pbsa_mem_create(C.byref(h), 1, 4, 1, 8, 60, 128) == _capi.PBSA_EINVAL
+    assert b"sink chunk" in lib.pbsa_last_error()
+    assert lib.pbsa_mem_create(C.byref(h), 1, 8, 1, 8, 60, 96) == _capi.PBSA_EUNSUPPORTED
+    rc = lib.pbsa_bsa_fwd(None, None, None, 4, None, 0, 0, None, 0, 0, None, 0, 1, 65, 128, 1,
+                          0.0, None, None, None)
+    assert rc == _capi.PBSA_EINVAL and b"block size" in lib.pbsa_last_error()
+    rc = lib.pbsa_score_select(None, None, 0, None, 4, 4, 0, 4, 5, 1, 1, 128, 0.0, None, None,
+                               None, 0, None)
+    assert rc == _capi.PBSA_EINVAL and b"k exceeds" in lib.pbsa_last_error()
+
+
+def test_product_package_does_not_import_the_oracle():
+    pkg = os.path.join(ROOT, "paper_2604_21221_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                text = open(os.path.join(dirpath, f)).read()
+                for pat in (r"^\s*(from|import)\s+oracle", r"liboracle", r"\borc_[a-z]", r"_ref/"):
+                    assert not re.search(pat, text, flags=re.M), (f, pat)

@@ -1,0 +1,257 @@
+"""GPU parity: every kernel of the PBSA hot path against the CPU oracle, through the C ABI.
+
+Bars (BASELINE.json north_star): selected block indices and updated memory-block ids bit-exact,
+s_t bit-exact, compression bit-exact; attention output max-abs <= 2e-2 and mean-abs <= 2e-3 vs
+the fp32 oracle on the same bf16-rounded inputs.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as orc
+from tests.pbsa_oracle_compose import bf16_round, check_attention, normal_bf16
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pb():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2604_21221_b200 as pb
+    return pb
+
+
+def dev(x, dtype=torch.bfloat16):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(device="cuda", dtype=dtype)
+
+
+def bits(a):
+    return np.ascontiguousarray(a, np.float32).view(np.uint32)
+
+
+# ------------------------------------------------------------------ tcgen05 building blocks
+@pytest.mark.parametrize("d", [64, 128])
+def test_debug_tile_mma_layouts(pb, d):
+    g = torch.Generator(device="cpu").manual_seed(d)
+    q = torch.randn(128, d, generator=g).bfloat16().cuda()
+    k = torch.randn(64, d, generator=g).bfloat16().cuda()
+    v = torch.randn(64, d, generator=g).bfloat16().cuda()
+    s, o = pb.debug_tile(q, k, v)
+    torch.cuda.synchronize()
+    s_ref = q.float() @ k.float().T
+    assert torch.allclose(s, s_ref, atol=1e-3, rtol=1e-4), (s - s_ref).abs().max()
+    o_ref = s.bfloat16().float() @ v.float()
+    assert torch.allclose(o, o_ref, atol=1e-2, rtol=1e-3), (o - o_ref).abs().max()
+
+
+# ------------------------------------------------------------------ (a) compression
+@pytest.mark.parametrize("d,b", [(128, 60), (64, 64), (128, 1), (64, 13)])
+def test_compress_bitexact(pb, d, b):
+    units, nb = 3, 11
+    x = normal_bf16(100 + b, (units, nb, b, d)) * np.float32(3.0)
+    x[1, 2] = 7.25  # identical tokens -> representative equals the token
+    got = pb.compress_blocks(dev(x)).cpu().numpy()
+    for u in range(units):
+        want = orc.compress_blocks(x[u])
+        assert np.array_equal(bits(got[u]), bits(want))
+    assert np.all(got[1, 2] == 7.25)
+
+
+# ------------------------------------------------------------------ (b) scoring + Top-K
+def _score_case(pb, units, nqb, n_p, n_l, n_c, d, k, seed, ties=False, zero_q=False):
+    g = np.random.default_rng(seed)
+    n_slots = n_p + n_l + n_c + 5
+    n_keys = n_p + n_l + n_c
+    qc = (g.standard_normal((units, nqb, d)) * 0.5).astype(np.float32)
+    if zero_q:
+        qc[:] = 0
+    krep = g.standard_normal((units, n_slots, d)).astype(np.float32)
+    if ties:  # duplicated representatives -> exactly tied probabilities
+        krep[:, 1::3] = krep[:, 0:1]
+    keys = np.stack([g.permutation(n_slots)[:n_keys] for _ in range(units)]).astype(np.int32)
+    sel, s_t = pb.score_select(dev(qc, torch.float32), dev(krep, torch.float32), dev(keys, torch.int32),
+                               n_p, n_l, k, want_scores=True)
+    sel, s_t = sel.cpu().numpy(), s_t.cpu().numpy()
+    for u in range(units):
+        kc = krep[u][keys[u]]
+        a_l = orc.coarse_attention(qc[u], kc[n_p:n_p + n_l])
+        assert np.array_equal(sel[u], orc.select_topk(a_l, k)), f"unit {u}"
+        want = orc.aggregate_scores(orc.coarse_attention(qc[u], kc))
+        assert np.array_equal(bits(s_t[u]), bits(want)), f"unit {u}"
+    return sel
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_score_select_bitexact_small(pb, d):
+    _score_case(pb, 3, 7, 8, 24, 8, d, 5, seed=d)
+
+
+def test_score_select_bitexact_config2_shape(pb):
+    _score_case(pb, 2, 78, 156, 312, 78, 128, 78, seed=7)
+
+
+def test_score_select_ties_lower_index(pb):
+    _score_case(pb, 2, 9, 4, 30, 4, 128, 7, seed=3, ties=True)
+    sel = _score_case(pb, 1, 3, 2, 20, 2, 64, 6, seed=4, zero_q=True)  # uniform rows
+    assert np.array_equal(sel[0], np.tile(np.arange(6), (3, 1)))
+
+
+def test_score_select_k_equals_local(pb):
+    _score_case(pb, 2, 5, 3, 9, 3, 128, 9, seed=11)
+
+
+def test_score_select_large_window(pb):
+    """config-5-like window (231 frames x 26 blocks) on a few rows."""
+    _score_case(pb, 1, 4, 156, 6006, 78, 128, 1502, seed=12)
+
+
+# ------------------------------------------------------------------ (c) block-sparse attention
+def _bsa_case(pb, units, nqb, b, d, n_dense, n_local, k, seed, scale_q=1.0):
+    g = np.random.default_rng(seed)
+    n_slots = n_dense + n_local + 3
+    kp = np.zeros((units, n_slots, 64, d), np.float32)
+    vp = np.zeros((units, n_slots, 64, d), np.float32)
+    kp[:, :, :b] = normal_bf16(seed + 1, (units, n_slots, b, d))
+    vp[:, :, :b] = normal_bf16(seed + 2, (units, n_slots, b, d))
+    q = normal_bf16(seed + 3, (units, nqb * b, d)) * np.float32(scale_q)
+    q = bf16_round(q)
+    perm = np.stack([g.permutation(n_slots) for _ in range(units)]).astype(np.int32)
+    dense = np.ascontiguousarray(perm[:, :n_dense])
+    local = np.ascontiguousarray(perm[:, n_dense:n_dense + n_local])
+    sel = np.stack([np.stack([np.sort(g.choice(n_local, k, replace=False)) for _ in range(nqb)])
+                    for _ in range(units)]).astype(np.int32) if k else None
+    o = pb.attention_sparse(dev(q), dev(kp), dev(vp), dev(dense, torch.int32) if n_dense else None,
+                            dev(local, torch.int32) if n_local else None,
+                            dev(sel, torch.int32) if k else None, b).float().cpu().numpy()
+    for u in range(units):
+        vis = [np.concatenate([dense[u], local[u][sel[u][i]] if k else np.zeros(0, np.int32)])
+               for i in range(nqb)]
+        want = orc.attention_sparse(q[u].reshape(nqb, b, d), kp[u][:, :b], vp[u][:, :b],
+                                    np.stack(vis).astype(np.int32))
+        check_attention(o[u].reshape(nqb, b, d), want)
+
+
+@pytest.mark.parametrize("d,b", [(128, 60), (64, 64), (128, 64), (64, 60), (128, 17)])
+def test_bsa_fwd_parity(pb, d, b):
+    _bsa_case(pb, 2, 5, b, d, 6, 16, 4, seed=d + b)
+
+
+def test_bsa_fwd_dense_only_and_full_local(pb):
+    _bsa_case(pb, 2, 4, 60, 128, 9, 0, 0, seed=1)     # first chunk: no local window
+    _bsa_case(pb, 1, 3, 60, 128, 0, 10, 10, seed=2)   # k = N_l (full visibility), no P
+    _bsa_case(pb, 1, 1, 60, 64, 3, 5, 2, seed=3)      # single query block (half tile)
+
+
+def test_bsa_fwd_peaky_inputs(pb):
+    """Q x 4: larger logits exercise the lazy-rescale path (survey: 'peaky variant')."""
+    _bsa_case(pb, 2, 6, 60, 128, 12, 24, 6, seed=5, scale_q=4.0)
+
+
+def test_bsa_fwd_long_list(pb):
+    _bsa_case(pb, 1, 4, 60, 128, 234, 312, 78, seed=9)
+
+
+# ------------------------------------------------------------------ (d) memory + full calls
+def run_rollout(pb, units, d, b, bpc, C, W, n_chunks, k_top, seed, denoise_steps=1, check_qb=None):
+    """Alg. 1 over n_chunks chunks, every PBSA call checked against the oracle."""
+    mem = pb.Memory(units, C, W, bpc, b, d)
+    oms = [orc.Memory(C, W) for _ in range(units)]
+    kst, vst = {}, {}  # (u, id) -> [b, d] f32 of committed blocks
+    stats = []
+    for c in range(n_chunks):
+        ids = np.arange(c * bpc, (c + 1) * bpc, dtype=np.int64)
+        for step in range(denoise_steps + 1):
+            update = step == denoise_steps
+            base = seed * 1000003 + c * 17 + step
+            q = normal_bf16(base, (units, bpc * b, d))
+            kc = normal_bf16(base + 7, (units, bpc * b, d))
+            vc = normal_bf16(base + 13, (units, bpc * b, d))
+            mem.write_chunk(dev(kc), dev(vc))
+            o = mem.attend(dev(q), k_top, pb.MODE_CACHE_UPDATE if update else pb.MODE_DENOISE)
+            sel_gpu, st_gpu = mem.last_selection()
+            o = o.float().cpu().numpy()
+            sel_gpu = None if sel_gpu is None else sel_gpu.cpu().numpy()
+            st_gpu = None if st_gpu is None else st_gpu.cpu().numpy()
+            for u in range(units):
+                p_ids, _, n_p, n_l = oms[u].assemble()
+                l_ids = p_ids[n_p:]
+                p_ids = p_ids[:n_p]
+                qb = q[u].reshape(bpc, b, d)
+                cur_k = kc[u].reshape(bpc, b, d)
+                cur_v = vc[u].reshape(bpc, b, d)
+                qc = orc.compress_blocks(qb)
+                k = min(k_top, n_l)
+                sel = np.zeros((bpc, 0), np.int32)
+                if k > 0:
+                    kc_l = orc.compress_blocks(np.stack([kst[(u, i)] for i in l_ids]))
+                    sel = orc.select_topk(orc.coarse_attention(qc, kc_l), k)
+                    assert np.array_equal(sel_gpu[u], sel), f"chunk {c} step {step} unit {u}: Top-K"
+                store_k = np.concatenate([np.stack([kst[(u, i)] for i in p_ids]) if n_p else
+                                          np.zeros((0, b, d), np.float32), cur_k,
+                                          np.stack([kst[(u, i)] for i in l_ids]) if n_l else
+                                          np.zeros((0, b, d), np.float32)])
+                store_v = np.concatenate([np.stack([vst[(u, i)] for i in p_ids]) if n_p else
+                                          np.zeros((0, b, d), np.float32), cur_v,
+                                          np.stack([vst[(u, i)] for i in l_ids]) if n_l else
+                                          np.zeros((0, b, d), np.float32)])
+                dense = np.arange(n_p + bpc)
+                vis = np.stack([np.concatenate([dense, n_p + bpc + sel[i]]) for i in range(bpc)]).astype(np.int32)
+                qmask = None
+                if check_qb is not None:
+                    qmask = np.zeros(bpc, np.uint8)
+                    qmask[check_qb] = 1
+                want = orc.attention_sparse(qb, store_k, store_v, vis, qmask=qmask)
+                rows = slice(None) if check_qb is None else check_qb
+                stats.append(check_attention(o[u].reshape(bpc, b, d)[rows], want[rows]))
+                if update:
+                    keys_k = np.concatenate([store_k[:n_p], store_k[n_p + bpc:], cur_k])
+                    key_ids = np.concatenate([p_ids, l_ids, ids])
+                    s_ref = orc.aggregate_scores(orc.coarse_attention(qc, orc.compress_blocks(keys_k)))
+                    assert np.array_equal(bits(st_gpu[u][:len(key_ids)]), bits(s_ref)), f"chunk {c} unit {u}: s_t"
+                    ev = oms[u].push_chunk(ids)
+                    oms[u].update_persistent(ev, key_ids, s_ref)
+                    for i in range(bpc):
+                        kst[(u, ids[i])] = cur_k[i]
+                        vst[(u, ids[i])] = cur_v[i]
+        # after the k=0 pass: P and L block ids bit-exact (SPEC.md:209-217 order)
+        gp, gl = mem.assemble()
+        gp, gl = gp.cpu().numpy(), gl.cpu().numpy()
+        for u in range(units):
+            a_ids, _, n_p, n_l = oms[u].assemble()
+            assert np.array_equal(gp[u], a_ids[:n_p]), f"chunk {c} unit {u}: persistent ids"
+            assert np.array_equal(gl[u], a_ids[n_p:]), f"chunk {c} unit {u}: local ids"
+    mem.close()
+    return stats
+
+
+@pytest.mark.parametrize("d", [64, 128])
+def test_rollout_small(pb, d):
+    # 6-block chunks, P = 2 chunks (one of sinks), window 2 chunks, 8 chunks -> 5 evictions
+    run_rollout(pb, units=3, d=d, b=60, bpc=6, C=12, W=2, n_chunks=8, k_top=3, seed=d)
+
+
+def test_rollout_config1(pb):
+    """Config 1 (BASELINE.json): d=64, b=64 = (1,8,8) on 16x16 frames (4 blocks/frame), 2-frame
+    chunks (8 query blocks), P = 2 frames (the sink chunk), L = 4 frames, top-k 8."""
+    run_rollout(pb, units=1, d=64, b=64, bpc=8, C=8, W=2, n_chunks=6, k_top=8, seed=1, denoise_steps=2)
+
+
+def test_rollout_config2_full_size(pb):
+    """Config 2 (Wan-1.3B layer): 12 heads, d=128, 60-token blocks, 78 blocks per 3-frame chunk,
+    P = 6 frames (156), L = 12 frames (312), top-k 78.  7 chunks reach steady state (sinks +
+    a full dynamic set + evictions); indices and ids checked everywhere, attention on sampled
+    query blocks."""
+    run_rollout(pb, units=12, d=128, b=60, bpc=78, C=156, W=4, n_chunks=7, k_top=78, seed=2,
+                denoise_steps=0, check_qb=np.array([0, 1, 40, 77]))
+
+
+def test_errors_are_loud(pb):
+    with pytest.raises(pb.PbsaError):
+        pb.Memory(1, 4, 1, 8, 60, 128)  # C < blocks_per_chunk
+    with pytest.raises(pb.PbsaError):
+        pb.Memory(1, 8, 1, 8, 60, 96)  # unsupported head dim
+    q = torch.zeros(1, 60, 128, dtype=torch.bfloat16, device="cuda")
+    kp = torch.zeros(1, 4, 64, 128, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(pb.PbsaError):
+        pb.attention_sparse(q, kp, kp, None, None, None, 61)
