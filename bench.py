@@ -1,0 +1,379 @@
+#!/usr/bin/env python
+"""bench.py -- PBSA per-chunk decode latency and effective TFLOP/s at Wan-1.3B shape.
+
+Workload (BASELINE.json configs[1], "config 2"): one Wan2.1-1.3B-shaped attention layer, 12 heads,
+head_dim 128, 1560 tokens per latent frame in 60-token (1,15,4) blocks (26 blocks/frame),
+3-frame chunks (78 query blocks = 4680 queries), 21-frame KV cache = persistent 6 frames (156
+blocks, the first chunk as sinks) + local window 12 frames (312 blocks) + current chunk 3 frames,
+row-wise Top-K k = 78 blocks (25 %), bf16 Q/K/V.  One STEP = one chunk of Alg. 1 at steady state:
+T = 4 denoise PBSA calls + 1 k=0 cache-update call (K1 Q compression, KV write + K compression,
+K2 scoring/Top-K (+ s_t), K3 block-sparse attention, K4 memory update).
+
+Multi-GPU: one process per GPU; every rank owns an independent batch element (12 heads) -- heads
+and batch shard with no data-path collective ("scaling": "weak"); timing is the max over ranks.
+
+Output: ONE JSON line on rank 0 (see README / DESIGN.md section 6 for every key).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PBSA per-chunk decode latency (ms) and effective TFLOP/s at Wan-1.3B shape, 1/2/4/8 GPU"
+GEOM = dict(heads=12, d=128, b=60, bpc=78, C=156, W=4, k_top=78, T=4)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--k-top", type=int, default=GEOM["k_top"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--out", default=None, help="also append the JSON line to this file")
+    return ap.parse_args()
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        p = json.load(open(path))
+        return {"bf16": p["bf16_tflops"], "bf16_sustained": p.get("bf16_tflops_sustained", p["bf16_tflops"]),
+                "hbm": p["hbm_gbs"], "source": "measured (MEASURED_PEAKS.json)"}
+    return {"bf16": 1590.0, "bf16_sustained": 1400.0, "hbm": 6650.0,
+            "source": "fallback (B200_PROFILING.md)"}
+
+
+def config_block(k_top, n_gpus):
+    g = GEOM
+    return {"workload": "config2: Wan2.1-1.3B attention layer, 1 chunk = 4 denoise + 1 k=0 PBSA calls",
+            "heads_per_gpu": g["heads"], "batch_per_gpu": 1, "global_batch": n_gpus, "head_dim": g["d"],
+            "block_tokens": g["b"], "block_shape": [1, 15, 4], "tokens_per_frame": 1560,
+            "chunk_frames": 3, "query_tokens_per_chunk": g["bpc"] * g["b"],
+            "kv_cache_frames": {"persistent": 6, "local": 12, "current": 3}, "top_k_blocks": k_top,
+            "parallelism": f"batch/head-partitioned x{n_gpus}, no data-path collective",
+            "l2": "inputs larger than L2: KV slot pool 215 MB per GPU (> 126 MB L2), fresh Q/K/V per call"}
+
+
+# ------------------------------------------------------------------------------ reference arm
+def cpu_sample(n_qb=4, seed=0):
+    """Bounded sample of the same workload on the oracle (the reference CPU path restated): one
+    head, n_qb query blocks of one denoise PBSA call at steady state -- each query block visits
+    156 persistent + 78 current + 78 selected local blocks of 60 tokens, d = 128; plus the coarse
+    scoring / Top-K of those rows."""
+    import numpy as np
+    from oracle import oracle as orc
+    g = GEOM
+    rng = np.random.default_rng(seed)
+    n_store = g["C"] + g["bpc"] + g["W"] * g["bpc"]
+    kst = rng.standard_normal((n_store, g["b"], g["d"])).astype(np.float32)
+    vst = rng.standard_normal((n_store, g["b"], g["d"])).astype(np.float32)
+    q = rng.standard_normal((n_qb, g["b"], g["d"])).astype(np.float32)
+    n_dense = g["C"] + g["bpc"]
+    n_local = g["W"] * g["bpc"]
+
+    def run():
+        qc = orc.compress_blocks(q)
+        kc = orc.compress_blocks(kst[n_dense:])
+        sel = orc.select_topk(orc.coarse_attention(qc, kc), g["k_top"])
+        vis = np.concatenate([np.tile(np.arange(n_dense), (n_qb, 1)), n_dense + sel], 1).astype(np.int32)
+        orc.attention_sparse(q, kst, vst, vis)
+        return n_local
+
+    flops = 4.0 * n_qb * g["b"] * (n_dense + g["k_top"]) * g["b"] * g["d"]
+    desc = (f"1 of {g['heads']} heads, {n_qb} of {g['bpc']} query blocks of one denoise call "
+            f"(Top-K scoring over {n_local} local blocks + attention over {n_dense + g['k_top']} blocks)")
+    return run, flops, desc, orc.num_threads()
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    run, flops, desc, cores = cpu_sample()
+    for _ in range(max(args.warmup, 1)):
+        run()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        run()
+    dt = (time.perf_counter() - t0) / args.steps
+    val = flops / dt / 1e12
+    line = {"metric": METRIC, "value": val, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32 (fp64 accumulation)", "data": "synthetic N(0,1)",
+            "config": config_block(args.k_top, args.gpus), "impl": "reference",
+            "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": cores, "kind": "port",
+                             "sample": desc},
+            "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": "the reference ships no implementation of the PBSA path (SURVEY.md section 0); "
+                    "the CPU restatement oracle/ built on the reference's numeric conventions is timed"}
+    emit(line, args)
+    return 0
+
+
+# ------------------------------------------------------------------------------ clocks sampler
+class Clocks:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.rows = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={','.join(self.FIELDS)}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.idx)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        if not self.rows:
+            return None
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = sorted({n for r in self.rows for n, v in zip(self.NAMES, r[2:]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def emit(line, args):
+    s = json.dumps(line)
+    print(s, flush=True)
+    if args.out:
+        with open(args.out, "a") as f:
+            f.write(s + "\n")
+
+
+# ------------------------------------------------------------------------------ our arm
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2604_21221_b200 as pb
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    g = GEOM
+    U, d, b, bpc, C, W, T = g["heads"], g["d"], g["b"], g["bpc"], g["C"], g["W"], g["T"]
+    k_top = args.k_top
+    nq = bpc * b
+    peaks = load_peaks()
+
+    mem = pb.Memory(U, C, W, bpc, b, d)
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+
+    def inputs():
+        return [torch.randn(U, nq, d, device=dev, dtype=torch.float32, generator=gen).to(torch.bfloat16)
+                for _ in range(3)]
+
+    n_sets = 2 * (T + 1)  # two chunks' worth of fresh Q/K/V, rotated
+    sets = [inputs() for _ in range(n_sets)]
+    out = torch.empty(U, nq, d, device=dev, dtype=torch.bfloat16)
+
+    def chunk_step(i):
+        for j in range(T + 1):
+            q, kk, vv = sets[(i * (T + 1) + j) % n_sets]
+            mem.write_chunk(kk, vv)
+            mem.attend(q, k_top, pb.MODE_CACHE_UPDATE if j == T else pb.MODE_DENOISE, out=out)
+
+    # fill the memory to steady state (sinks + full dynamic set + full window), untimed
+    i = 0
+    while True:
+        inf = mem.info()
+        if inf.n_p == C and inf.n_l == W * bpc and inf.chunks_committed > W + 2:
+            break
+        q, kk, vv = sets[i % n_sets]
+        mem.write_chunk(kk, vv)
+        mem.attend(q, k_top, pb.MODE_CACHE_UPDATE, out=out)
+        i += 1
+    for w in range(args.warmup):
+        chunk_step(w)
+    torch.cuda.synchronize()
+
+    inf = mem.info()
+    n_dense = inf.n_p + bpc
+    k_eff = min(k_top, inf.n_l)
+    alg_flops_call = 4.0 * b * d * (n_dense + k_eff) * b * bpc * U  # valid tokens only
+    alg_flops_step = (T + 1) * alg_flops_call
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    stream = torch.cuda.current_stream()
+    clocks = Clocks(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local_rank)).split(",")[0])
+                    if os.environ.get("CUDA_VISIBLE_DEVICES", "").isdigit() else local_rank)
+    clocks.start()
+    time.sleep(0.3)
+
+    # ---------------------------------------------------------------- timed: device-resident
+    mem.profile(True, max_calls=(T + 1) * args.steps + 8)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for s in range(args.steps):
+        chunk_step(s)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms_total = max_over_ranks(e0.elapsed_time(e1))
+    prof = mem.profile_read()
+    mem.profile(False)
+    ms_step = ms_total / args.steps
+    value = world * alg_flops_step / (ms_step * 1e-3) / 1e12
+
+    # executed FLOPs of K3 from the union lists of the last call
+    sel, _ = mem.last_selection()
+    exec_flops_call = None
+    if sel is not None:
+        s_np = sel.cpu().numpy()
+        total_blocks = 0
+        for u in range(U):
+            for t in range(0, bpc, 2):
+                un = set(s_np[u, t].tolist()) | (set(s_np[u, t + 1].tolist()) if t + 1 < bpc else set())
+                total_blocks += n_dense + len(un)
+        exec_flops_call = 4.0 * 128 * 64 * d * total_blocks
+    n_calls = prof["attend_calls"]
+    k3_ms = prof["ms"]["bsa_fwd"] / max(n_calls, 1)
+    k3_alg = alg_flops_call / (k3_ms * 1e-3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "bsa_fwd_traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+    roofline = {"bound": "tensor", "kernel": "bsa_fwd_kernel (K3)", "achieved": k3_alg,
+                "peak": peaks["bf16_sustained"], "unit": "TFLOP/s", "frac": k3_alg / peaks["bf16_sustained"],
+                "traffic": traffic, "peak_kind": "sustained bf16 (kernel timed inside the chunk step), "
+                + peaks["source"], "frac_of_burst": k3_alg / peaks["bf16"],
+                "avg_launch_ms": k3_ms, "algorithmic_flops_per_launch": alg_flops_call}
+    if exec_flops_call:
+        roofline["executed_flops_per_launch"] = exec_flops_call
+        roofline["achieved_executed"] = exec_flops_call / (k3_ms * 1e-3) / 1e12
+        roofline["frac_executed"] = roofline["achieved_executed"] / peaks["bf16_sustained"]
+    stage_share = {k: v / ms_total for k, v in prof["ms"].items()}
+
+    # ---------------------------------------------------------------- timed: end to end (host buffers)
+    e2e = None
+    if not args.no_e2e:
+        host = [[t.cpu().pin_memory() for t in st] for st in sets[: T + 1]]
+        ho = torch.empty(U, nq, d, dtype=torch.bfloat16).pin_memory()
+        dq, dk, dv = (torch.empty(U, nq, d, device=dev, dtype=torch.bfloat16) for _ in range(3))
+        h2d = 3 * U * nq * d * 2 * (T + 1)
+        d2h = U * nq * d * 2 * (T + 1)
+        e2e_steps = max(1, min(args.steps, 50))
+
+        def e2e_step():
+            for j in range(T + 1):
+                hq, hk, hv = host[j]
+                dq.copy_(hq, non_blocking=True)
+                dk.copy_(hk, non_blocking=True)
+                dv.copy_(hv, non_blocking=True)
+                mem.write_chunk(dk, dv)
+                mem.attend(dq, k_top, pb.MODE_CACHE_UPDATE if j == T else pb.MODE_DENOISE, out=out)
+                ho.copy_(out, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ms_e2e = max_over_ranks(e0.elapsed_time(e1)) / e2e_steps
+        e2e = {"value": world * alg_flops_step / (ms_e2e * 1e-3) / 1e12, "unit": "TFLOP/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e,
+               "steps": e2e_steps, "api": "paper_2604_21221_b200.Memory.write_chunk/attend "
+               "(-> pbsa_mem_write_chunk / pbsa_attend) with pinned host Q/K/V in, O out"}
+    clk = clocks.stop()
+
+    # ---------------------------------------------------------------- CPU baseline (rank 0, N=1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        run, flops, desc, cores = cpu_sample()
+        run()
+        reps = []
+        t_end = time.perf_counter() + 10.0
+        while time.perf_counter() < t_end or len(reps) < 3:
+            t0 = time.perf_counter()
+            run()
+            reps.append(time.perf_counter() - t0)
+        cpu = {"value": flops / statistics.median(reps) / 1e12, "unit": "TFLOP/s", "cores": cores,
+               "kind": "port", "sample": desc + f"; median of {len(reps)} reps"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "chunk_latency_ms": ms_step,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic N(0,1) bf16 Q/K/V, fresh per call",
+                "config": config_block(k_top, world),
+                "algorithmic_tflop_per_step": world * alg_flops_step / 1e12,
+                "gpu_launches": args.steps * (T * 5 + 7),
+                "roofline": roofline, "stage_share_of_step": stage_share, "cpu_baseline": cpu,
+                "e2e": e2e, "clocks": clk, "impl": "ours"}
+        emit(line, args)
+    mem.close()
+    return 0
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        return run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -66,7 +66,7 @@ struct Layout {
     }
 };
 
-template <int D, int NSK, int NSV>
+template <int D, int NSK, int NSV, int B>
 __global__ void __launch_bounds__(kThreads, 2)
     bsa_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                    const __grid_constant__ CUtensorMap tm_v, const BsaParams p) {
@@ -121,6 +121,19 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int t = threadIdx.x - 64;
         const int sel_rows = has2 ? 2 : 1;
         for (int w = t; w < 2 * p.bm_words; w += 128) bm[w] = 0u;
+        // zero the query padding rows (rows >= b of each half, the whole upper half without a
+        // second query block) so their S rows stay finite; TMA only writes rows < b
+        {
+            const int pad = 64 - p.b;
+            const int rows_pad = has2 ? 2 * pad : pad + 64;
+            for (int e = t; e < rows_pad * L::kHalves * 8; e += 128) {
+                const int chunk = e & 7, rh = e >> 3;
+                const int h = rh % L::kHalves, pr = rh / L::kHalves;
+                const int row = pr < pad ? p.b + pr : (has2 ? 64 + p.b + (pr - pad) : 64 + (pr - pad));
+                *reinterpret_cast<uint4*>(q_smem + h * 16384 + row * 128 + chunk * 16) = make_uint4(0, 0, 0, 0);
+            }
+            fence_proxy_async_smem();
+        }
         named_bar_sync(1, 128);
         if (p.k > 0 && p.n_local > 0) {
             for (int e = t; e < sel_rows * p.k; e += 128) {
@@ -256,59 +269,92 @@ __global__ void __launch_bounds__(kThreads, 2)
                 ++o_waited[bb];
             }
         };
+        // columns >= BB of a slot are padding (compile-time for the common block sizes)
+        constexpr int BB = B > 0 ? B : 64;
+        const int bcols = B > 0 ? B : p.b;
+        const float2 scl2 = make_float2(p.scale_log2, p.scale_log2);
         for (int j = 0; j < n; ++j) {
             const int buf = j & 1;
             mbar_wait(s_full + buf, (j >> 1) & 1);
             tc_fence_after();
             pv_done(j - 2);  // already complete: S_j was committed after PV_{j-2}
             const uint32_t t_s = t_o + L::kSColBase + buf * 64;
-            uint32_t sr[64];
-            tmem_ld32(t_s, *reinterpret_cast<uint32_t(*)[32]>(sr));
-            tmem_ld32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
-            tmem_wait_ld();
-            const bool vis = valid && ((list[j] >> (24 + half)) & 1);
-            float mx = -INFINITY;
-            if (vis) {
-#pragma unroll
-                for (int c = 0; c < 64; ++c)
-                    if (c < p.b) mx = fmaxf(mx, __uint_as_float(sr[c]));
-                mx *= p.scale_log2;
-            }
-            float factor = 1.0f;
-            bool resc = false;
-            if (mx > m) {
-                if (m == -INFINITY) {
-                    m = mx;  // first visible block for this row: O row is still zero
-                } else if (mx > m + kRescaleThreshold) {
-                    factor = exp2f(m - mx);
-                    m = mx;
-                    resc = true;
-                }
-            }
-            if (__any_sync(0xffffffffu, resc)) {
-                pv_done(j - 1);
-                tc_fence_after();
-#pragma unroll 1
-                for (int c0 = 0; c0 < D; c0 += 32) {
-                    uint32_t ov[32];
-                    tmem_ld32(t_o + c0, ov);
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int c = 0; c < 32; ++c) ov[c] = __float_as_uint(__uint_as_float(ov[c]) * factor);
-                    tmem_st32(t_o + c0, ov);
-                }
-                l *= factor;
-            }
             uint32_t pk[32];
+            // rows of one warp all lie in one half -> visibility is warp-uniform
+            const bool vis = (list[j] >> (24 + half)) & 1;
+            if (vis) {
+                uint32_t sr[64];
+                tmem_ld32(t_s, *reinterpret_cast<uint32_t(*)[32]>(sr));
+                tmem_ld32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
+                tmem_wait_ld();
+                float sv[64];
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
-                float p0 = 0.0f, p1 = 0.0f;
-                if (vis) {
-                    if (2 * c < p.b) p0 = exp2f(fmaf(__uint_as_float(sr[2 * c]), p.scale_log2, -m));
-                    if (2 * c + 1 < p.b) p1 = exp2f(fmaf(__uint_as_float(sr[2 * c + 1]), p.scale_log2, -m));
+                for (int c = 0; c < 64; ++c) {
+                    sv[c] = __uint_as_float(sr[c]);
+                    if (B == 0 && c >= bcols) sv[c] = -INFINITY;  // generic block size
                 }
-                l += p0 + p1;
-                pk[c] = pack_bf16x2(p0, p1);
+                // row max over the valid columns: FMNMX3 tree
+                float mx4[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    float a = -INFINITY;
+#pragma unroll
+                    for (int c = t * 16; c < t * 16 + 16; c += 2) {
+                        if (c + 1 < BB) a = fmax3(a, sv[c], sv[c + 1]);
+                        else if (c < BB) a = fmaxf(a, sv[c]);
+                    }
+                    mx4[t] = a;
+                }
+                float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * p.scale_log2;
+                if (!valid) mx = -INFINITY;
+                float factor = 1.0f;
+                bool resc = false;
+                if (mx > m) {
+                    if (m == -INFINITY) {
+                        m = mx;  // first visible block for this row: its O row is still zero
+                    } else if (mx > m + kRescaleThreshold) {
+                        factor = exp2_approx(m - mx);
+                        m = mx;
+                        resc = true;
+                    }
+                }
+                if (__any_sync(0xffffffffu, resc)) {
+                    pv_done(j - 1);
+                    tc_fence_after();
+#pragma unroll 1
+                    for (int c0 = 0; c0 < D; c0 += 32) {
+                        uint32_t ov[32];
+                        tmem_ld32(t_o + c0, ov);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int c = 0; c < 32; ++c) ov[c] = __float_as_uint(__uint_as_float(ov[c]) * factor);
+                        tmem_st32(t_o + c0, ov);
+                    }
+                    l *= factor;
+                }
+                // p = 2^(s*scale_log2 - m); padding rows get bias -inf -> p = 0
+                const float bias = valid ? -m : -INFINITY;
+                const float2 bias2 = make_float2(bias, bias);
+                float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                                 make_float2(0.f, 0.f)};
+#pragma unroll
+                for (int c2 = 0; c2 < 32; ++c2) {
+                    const float2 x = __ffma2_rn(make_float2(sv[2 * c2], sv[2 * c2 + 1]), scl2, bias2);
+                    float2 e;
+                    e.x = (2 * c2 < BB) ? exp2_approx(x.x) : 0.0f;
+                    e.y = (2 * c2 + 1 < BB) ? exp2_approx(x.y) : 0.0f;
+                    if (B == 0) {
+                        if (2 * c2 >= bcols) e.x = 0.0f;
+                        if (2 * c2 + 1 >= bcols) e.y = 0.0f;
+                    }
+                    acc[c2 & 3] = __fadd2_rn(acc[c2 & 3], e);
+                    pk[c2] = pack_bf16x2(e.x, e.y);
+                }
+                const float2 s01 = __fadd2_rn(__fadd2_rn(acc[0], acc[1]), __fadd2_rn(acc[2], acc[3]));
+                l += s01.x + s01.y;
+            } else {
+#pragma unroll
+                for (int c = 0; c < 32; ++c) pk[c] = 0u;
             }
             tmem_st32(t_s, pk);
             tmem_wait_st();
@@ -438,7 +484,7 @@ __global__ void __launch_bounds__(128, 1)
     }
 }
 
-template <int D, int NSK, int NSV>
+template <int D, int NSK, int NSV, int B>
 int launch_impl(const bf16* q, const bf16* kp, const bf16* vp, const BsaParams& p, cudaStream_t s) {
     using L = Layout<D, NSK, NSV>;
     alignas(64) CUtensorMap tq, tk, tv;
@@ -465,11 +511,11 @@ int launch_impl(const bf16* q, const bf16* kp, const bf16* vp, const BsaParams& 
         return set_error(PBSA_EUNSUPPORTED, "bsa_fwd: visible list too long for shared memory");
     static bool configured = false;
     if (!configured) {
-        cudaFuncSetAttribute(bsa_fwd_kernel<D, NSK, NSV>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(bsa_fwd_kernel<D, NSK, NSV, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         configured = true;
     }
     dim3 grid((p.nqb + 1) / 2, p.units);
-    bsa_fwd_kernel<D, NSK, NSV><<<grid, kThreads, smem, s>>>(tq, tk, tv, p);
+    bsa_fwd_kernel<D, NSK, NSV, B><<<grid, kThreads, smem, s>>>(tq, tk, tv, p);
     return check_launch("bsa_fwd_kernel");
 }
 
@@ -515,8 +561,14 @@ int launch_bsa_fwd(const bf16* q, const bf16* k_pool, const bf16* v_pool, int n_
     p.bm_words = (n_local + 31) / 32 + 1;
     p.max_list = n_dense + (p.k > 0 ? (2 * p.k < n_local ? 2 * p.k : n_local) : 0);
     if (units == 0 || nqb == 0) return 0;
-    if (d == 128) return launch_impl<128, 2, 2>(q, k_pool, v_pool, p, s);
-    return launch_impl<64, 3, 3>(q, k_pool, v_pool, p, s);
+    if (d == 128) {
+        if (b == 60) return launch_impl<128, 2, 2, 60>(q, k_pool, v_pool, p, s);
+        if (b == 64) return launch_impl<128, 2, 2, 64>(q, k_pool, v_pool, p, s);
+        return launch_impl<128, 2, 2, 0>(q, k_pool, v_pool, p, s);
+    }
+    if (b == 60) return launch_impl<64, 3, 3, 60>(q, k_pool, v_pool, p, s);
+    if (b == 64) return launch_impl<64, 3, 3, 64>(q, k_pool, v_pool, p, s);
+    return launch_impl<64, 3, 3, 0>(q, k_pool, v_pool, p, s);
 }
 
 int launch_debug_tile(const bf16* q, const bf16* k, const bf16* v, int d, float* s_out, float* o_out,
