@@ -23,6 +23,7 @@
 //
 // Roofline: tensor core.  Executed FLOPs per tile = 4 * 128 * 64 * d * |union list|.
 #include <cfloat>
+#include <cstdlib>
 
 #include "internal.h"
 #include "ptx.cuh"
@@ -46,6 +47,7 @@ struct BsaParams {
     float* lse;
     float scale_log2;
     int max_list, bm_words;
+    int ablate;  // perf experiments only (PBSA_ABLATE): 1 = softmax writes P=0 without computing
 };
 
 template <int D, int NSK, int NSV>
@@ -281,7 +283,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             const uint32_t t_s = t_o + L::kSColBase + buf * 64;
             uint32_t pk[32];
             // rows of one warp all lie in one half -> visibility is warp-uniform
-            const bool vis = (list[j] >> (24 + half)) & 1;
+            const bool vis = ((list[j] >> (24 + half)) & 1) && p.ablate != 1;
             if (vis) {
                 uint32_t sr[64];
                 tmem_ld32(t_s, *reinterpret_cast<uint32_t(*)[32]>(sr));
@@ -558,6 +560,10 @@ int launch_bsa_fwd(const bf16* q, const bf16* k_pool, const bf16* v_pool, int n_
     p.o = o;
     p.lse = lse;
     p.scale_log2 = scale * 1.4426950408889634f;
+    {
+        static const int ablate = getenv("PBSA_ABLATE") ? atoi(getenv("PBSA_ABLATE")) : 0;
+        p.ablate = ablate;
+    }
     p.bm_words = (n_local + 31) / 32 + 1;
     p.max_list = n_dense + (p.k > 0 ? (2 * p.k < n_local ? 2 * p.k : n_local) : 0);
     if (units == 0 || nqb == 0) return 0;

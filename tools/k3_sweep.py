@@ -1,0 +1,44 @@
+#!/usr/bin/env python
+"""K3 microbenchmark at the config-2 geometry (12 heads, 78 query blocks of 60, 546-slot pools,
+234 dense + top-78 of 312 local blocks).  Prints ms / launch and TFLOP/s (algorithmic and executed).
+PBSA_ABLATE=1 makes the softmax warps skip their math (pipeline / tensor-core upper bound)."""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2604_21221_b200 as pb  # noqa: E402
+
+U, nqb, b, d, S, nd, nl, k = 12, 78, 60, 128, 546, 234, 312, 78
+g = torch.Generator(device="cuda").manual_seed(0)
+kp = torch.zeros(U, S, 64, d, device="cuda", dtype=torch.bfloat16)
+vp = torch.zeros_like(kp)
+kp[:, :, :b] = torch.randn(U, S, b, d, device="cuda", generator=g).bfloat16()
+vp[:, :, :b] = torch.randn(U, S, b, d, device="cuda", generator=g).bfloat16()
+q = torch.randn(U, nqb * b, d, device="cuda", generator=g).bfloat16()
+perm = torch.stack([torch.randperm(S, device="cuda", generator=g) for _ in range(U)]).int()
+dense = perm[:, :nd].contiguous()
+local = perm[:, nd:nd + nl].contiguous()
+sel = torch.stack([torch.stack([torch.randperm(nl, device="cuda", generator=g)[:k].sort().values
+                                for _ in range(nqb)]) for _ in range(U)]).int().contiguous()
+alg = 4.0 * b * d * (nd + k) * b * nqb * U
+un = 0
+sc = sel.cpu()
+for u in range(U):
+    for t in range(0, nqb, 2):
+        un += nd + len(set(sc[u, t].tolist()) | set(sc[u, t + 1].tolist()))
+exe = 4.0 * 128 * 64 * d * un
+for _ in range(3):
+    pb.attention_sparse(q, kp, vp, dense, local, sel, b)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+reps = 20
+e0.record()
+for _ in range(reps):
+    pb.attention_sparse(q, kp, vp, dense, local, sel, b)
+e1.record()
+torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / reps
+print(f"ablate={os.environ.get('PBSA_ABLATE', '0')} ms={ms:.4f} alg_TFLOPs={alg / ms / 1e9:.1f} "
+      f"exec_TFLOPs={exe / ms / 1e9:.1f} exec/alg={exe / alg:.3f}")
