@@ -12,7 +12,7 @@ OBJ       := $(patsubst $(PKG)/csrc/%.cu,build/obj/%.o,$(SRC))
 LIB       := $(PKG)/_lib/libpbsa_b200.so
 HOSTCXX   := $(shell test -x /usr/bin/g++ && echo /usr/bin/g++ || echo g++)
 
-all: $(LIB) oracle
+all: $(LIB) oracle cpp-test
 
 build/obj/%.o: $(PKG)/csrc/%.cu $(HDR)
 	@mkdir -p build/obj build/log
@@ -33,3 +33,13 @@ clean:
 	$(MAKE) -s -C oracle clean
 
 .PHONY: all oracle oracle-ref clean
+
+# C++ drop-in API check (host code over the C ABI; runs on a GPU box via tests/test_cpp_api.py)
+cpp-test: build/test_pbsa_cpp
+
+build/test_pbsa_cpp: tests/cpp/test_pbsa_cpp.cpp include/pbsa/pbsa_b200.hpp include/pbsa/tensor.hpp $(LIB)
+	@mkdir -p build
+	$(NVCC) $(ARCH) -std=c++20 -O2 -ccbin $(HOSTCXX) -Iinclude tests/cpp/test_pbsa_cpp.cpp -o $@ \
+	  -L$(PKG)/_lib -lpbsa_b200 -Xlinker -rpath -Xlinker '$$ORIGIN/../$(PKG)/_lib'
+
+.PHONY: cpp-test

@@ -226,16 +226,10 @@ def run_ours(args, rank, world, local_rank):
     alg_flops_call = 4.0 * b * d * (n_dense + k_eff) * b * bpc * U  # valid tokens only
     alg_flops_step = (T + 1) * alg_flops_call
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
+    from paper_2604_21221_b200.parallel import barrier, max_over_ranks as _max
 
     def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return _max(x, dev)
 
     stream = torch.cuda.current_stream()
     clocks = Clocks(int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local_rank)).split(",")[0])
