@@ -193,7 +193,7 @@ inline DenseMatrix attention_sparse(const BlockedTensor& q_blocks, const Blocked
                                local_blocks.empty() ? nullptr : dl.p, static_cast<int>(local_blocks.size()),
                                static_cast<int>(local_blocks.size()), sel.empty() ? nullptr : ds.p, static_cast<int>(k),
                                static_cast<int>(nqb), static_cast<int>(b), static_cast<int>(d), 1,
-                               static_cast<float>(cfg.scale), dout.p, nullptr, nullptr));
+                               static_cast<float>(cfg.scale), dout.p, nullptr, nullptr, 0, nullptr));
     std::vector<uint16_t> h(nqb * b * d);
     dout.download(h.data(), h.size());
     DenseMatrix out(nqb * b, d);

@@ -65,12 +65,16 @@ int pbsa_score_select(const float* qc, const float* krep, int64_t krep_unit_stri
  * and to the selected local blocks local_slots[u*local_stride + sel[(u*nqb+i)*k + 0..k)].
  * Key rows >= b of a slot are masked.  o = softmax(q k^T * scale) v (bf16 out, fp32 softmax and
  * accumulators); lse (nullable) [units][n_q] natural-log row log-sum-exp.  d in {64, 128},
- * 1 <= b <= 64.  k_pool / v_pool: [units][n_slots][64][d]. */
+ * 1 <= b <= 64.  k_pool / v_pool: [units][n_slots][64][d].
+ * workspace (nullable): pbsa_bsa_fwd_workspace() bytes, ZERO-INITIALISED ONCE by the caller (the
+ * kernel leaves it zeroed); with it the launch is a persistent stream-K schedule (tiles split
+ * across CTAs and merged), without it every CTA takes whole 128-row tiles. */
+size_t pbsa_bsa_fwd_workspace(int units, int nqb, int d);
 int pbsa_bsa_fwd(const void* q, const void* k_pool, const void* v_pool, int n_slots,
                  const int32_t* dense_slots, int dense_stride, int n_dense,
                  const int32_t* local_slots, int local_stride, int n_local, const int32_t* sel,
                  int k, int nqb, int b, int d, int units, float scale, void* o, float* lse,
-                 void* stream);
+                 void* workspace, size_t workspace_bytes, void* stream);
 
 /* (d) persistent memory -- replaces memory.PersistentMemory / LocalWindow / push_chunk /
  * update_persistent / assemble_kv (Eq. 9).  Device-resident

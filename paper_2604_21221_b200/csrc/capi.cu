@@ -91,6 +91,8 @@ struct pbsa_mem {
     float* ws = nullptr;
     size_t ws_bytes = 0;
     int32_t* sel = nullptr;
+    void* k3ws = nullptr;
+    size_t k3ws_bytes = 0;
     int last_k = 0, last_n_keys = 0;
     // stage profiling: 5 events per attend call, 2 per KV write
     std::vector<cudaEvent_t> ev_attend, ev_write;
@@ -126,7 +128,7 @@ void free_mem(pbsa_mem* m) {
     free_events(m);
     void* ptrs[] = {m->k_pool, m->v_pool, m->krep, m->dev.p_slot, m->dev.p_id, m->dev.p_score,
                     m->dev.l_slot, m->dev.l_id, m->dev.stage, m->dev.free_slot, m->dev.dense,
-                    m->dev.keys, m->qc, m->s_t, m->ws, m->sel};
+                    m->dev.keys, m->qc, m->s_t, m->ws, m->sel, m->k3ws};
     for (void* p : ptrs)
         if (p) cudaFree(p);
 }
@@ -199,11 +201,16 @@ int pbsa_score_select(const float* qc, const float* krep, int64_t krep_unit_stri
                                as_stream(stream));
 }
 
+size_t pbsa_bsa_fwd_workspace(int units, int nqb, int d) {
+    if (units < 0 || nqb < 0 || (d != 64 && d != 128)) return 0;
+    return bsa_fwd_workspace(units, nqb, d);
+}
+
 int pbsa_bsa_fwd(const void* q, const void* k_pool, const void* v_pool, int n_slots,
                  const int32_t* dense_slots, int dense_stride, int n_dense,
                  const int32_t* local_slots, int local_stride, int n_local, const int32_t* sel,
                  int k, int nqb, int b, int d, int units, float scale, void* o, float* lse,
-                 void* stream) {
+                 void* workspace, size_t workspace_bytes, void* stream) {
     if (int rc = check_d(d)) return rc;
     PBSA_REQUIRE(b >= 1 && b <= 64, "bsa_fwd: block size b must be in [1, 64]");
     PBSA_REQUIRE(nqb >= 0 && units >= 0 && n_slots >= 1, "bsa_fwd: bad counts");
@@ -221,7 +228,7 @@ int pbsa_bsa_fwd(const void* q, const void* k_pool, const void* v_pool, int n_sl
     return launch_bsa_fwd(static_cast<const bf16*>(q), static_cast<const bf16*>(k_pool),
                           static_cast<const bf16*>(v_pool), n_slots, dense_slots, dense_stride, n_dense,
                           local_slots, local_stride, n_local, sel, k, nqb, b, d, units, scale,
-                          static_cast<bf16*>(o), lse, as_stream(stream));
+                          static_cast<bf16*>(o), lse, workspace, workspace_bytes, as_stream(stream));
 }
 
 int pbsa_copy(void* dst, const void* src, size_t bytes, void* stream) {
@@ -277,7 +284,9 @@ int pbsa_mem_create(pbsa_mem** out, int units, int capacity_c, int window_chunks
               alloc(reinterpret_cast<void**>(&m->sel), U * bpc * L * 4);
     if (ok) {
         m->ws_bytes = score_select_workspace(units, m->bpc, m->S);
-        ok = alloc(reinterpret_cast<void**>(&m->ws), m->ws_bytes);
+        m->k3ws_bytes = bsa_fwd_workspace(units, m->bpc, d);
+        ok = alloc(reinterpret_cast<void**>(&m->ws), m->ws_bytes) && alloc(&m->k3ws, m->k3ws_bytes) &&
+             cudaMemset(m->k3ws, 0, m->k3ws_bytes) == cudaSuccess;
     }
     if (!ok) {
         free_mem(m);
@@ -449,7 +458,7 @@ int pbsa_attend(pbsa_mem* m, const void* q, int k_top, float scale, int mode, vo
     // (c) block-sparse attention over P ++ current (dense) and the selected local blocks
     if (int rc = launch_bsa_fwd(static_cast<const bf16*>(q), m->k_pool, m->v_pool, m->S, m->dev.dense,
                                 m->C + bpc, n_p + bpc, m->dev.l_slot, m->Lcap, n_l, m->sel, k, bpc, b, d, U,
-                                scale, static_cast<bf16*>(o), lse, s))
+                                scale, static_cast<bf16*>(o), lse, m->k3ws, m->k3ws_bytes, s))
         return rc;
     prof_mark(m, 3, s);
     // (d) persistent-memory update after the k=0 pass

@@ -34,7 +34,8 @@ int launch_score_select(const float* qc, const float* krep, int64_t krep_unit_st
 int launch_bsa_fwd(const bf16* q, const bf16* k_pool, const bf16* v_pool, int n_slots,
                    const int32_t* dense, int dense_stride, int n_dense, const int32_t* local,
                    int local_stride, int n_local, const int32_t* sel, int k, int nqb, int b, int d,
-                   int units, float scale, bf16* o, float* lse, cudaStream_t s);
+                   int units, float scale, bf16* o, float* lse, void* ws, size_t ws_bytes, cudaStream_t s);
+size_t bsa_fwd_workspace(int units, int nqb, int d);
 int launch_debug_tile(const bf16* q, const bf16* k, const bf16* v, int d, float* s_out,
                       float* o_out, cudaStream_t s);
 // K4

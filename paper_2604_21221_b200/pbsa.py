@@ -109,7 +109,7 @@ def attention_sparse(q: torch.Tensor, k_pool: torch.Tensor, v_pool: torch.Tensor
                      dense_slots: torch.Tensor | None, local_slots: torch.Tensor | None,
                      sel: torch.Tensor | None, b: int, scale: float | None = None,
                      n_dense: int | None = None, n_local: int | None = None,
-                     want_lse: bool = False):
+                     want_lse: bool = False, stream_k: bool = True):
     """Block-sparse attention forward.
 
     q [units, nqb*b, d] bf16 (query tokens block-major); k_pool / v_pool [units, n_slots, 64, d]
@@ -135,11 +135,27 @@ def attention_sparse(q: torch.Tensor, k_pool: torch.Tensor, v_pool: torch.Tensor
     o = torch.empty_like(q)
     lse = torch.empty(units, nq, device=q.device, dtype=torch.float32) if want_lse else None
     scale = attention_scale(d) if scale is None else scale
+    ws_bytes = LIB.pbsa_bsa_fwd_workspace(units, nqb, d) if stream_k else 0
+    ws = _workspace(ws_bytes, q.device) if stream_k else None
     check(LIB.pbsa_bsa_fwd(q.data_ptr(), k_pool.data_ptr(), v_pool.data_ptr(), n_slots,
                            _ptr(dense_slots), 0 if dense_slots is None else dense_slots.shape[1], nd,
                            _ptr(local_slots), 0 if local_slots is None else local_slots.shape[1], nl,
-                           _ptr(sel), k, nqb, b, d, units, scale, o.data_ptr(), _ptr(lse), _stream()))
+                           _ptr(sel), k, nqb, b, d, units, scale, o.data_ptr(), _ptr(lse),
+                           _ptr(ws), ws_bytes, _stream()))
     return (o, lse) if want_lse else o
+
+
+_WS: dict = {}
+
+
+def _workspace(nbytes: int, device) -> torch.Tensor:
+    """Zero-initialised K3 workspace, cached per device (the kernel leaves it zeroed)."""
+    key = str(device)
+    t = _WS.get(key)
+    if t is None or t.numel() < nbytes:
+        t = torch.zeros(max(nbytes, 1), dtype=torch.uint8, device=device)
+        _WS[key] = t
+    return t
 
 
 def debug_tile(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor):

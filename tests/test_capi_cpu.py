@@ -47,7 +47,7 @@ def test_argument_errors_need_no_gpu():
     assert b"sink chunk" in lib.pbsa_last_error()
     assert lib.pbsa_mem_create(C.byref(h), 1, 8, 1, 8, 60, 96) == _capi.PBSA_EUNSUPPORTED
     rc = lib.pbsa_bsa_fwd(None, None, None, 4, None, 0, 0, None, 0, 0, None, 0, 1, 65, 128, 1,
-                          0.0, None, None, None)
+                          0.0, None, None, None, 0, None)
     assert rc == _capi.PBSA_EINVAL and b"block size" in lib.pbsa_last_error()
     rc = lib.pbsa_score_select(None, None, 0, None, 4, 4, 0, 4, 5, 1, 1, 128, 0.0, None, None,
                                None, 0, None)

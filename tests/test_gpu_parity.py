@@ -107,7 +107,7 @@ def test_score_select_large_window(pb):
 
 
 # ------------------------------------------------------------------ (c) block-sparse attention
-def _bsa_case(pb, units, nqb, b, d, n_dense, n_local, k, seed, scale_q=1.0):
+def _bsa_case(pb, units, nqb, b, d, n_dense, n_local, k, seed, scale_q=1.0, stream_k=True):
     g = np.random.default_rng(seed)
     n_slots = n_dense + n_local + 3
     kp = np.zeros((units, n_slots, 64, d), np.float32)
@@ -123,7 +123,7 @@ def _bsa_case(pb, units, nqb, b, d, n_dense, n_local, k, seed, scale_q=1.0):
                     for _ in range(units)]).astype(np.int32) if k else None
     o = pb.attention_sparse(dev(q), dev(kp), dev(vp), dev(dense, torch.int32) if n_dense else None,
                             dev(local, torch.int32) if n_local else None,
-                            dev(sel, torch.int32) if k else None, b).float().cpu().numpy()
+                            dev(sel, torch.int32) if k else None, b, stream_k=stream_k).float().cpu().numpy()
     for u in range(units):
         vis = [np.concatenate([dense[u], local[u][sel[u][i]] if k else np.zeros(0, np.int32)])
                for i in range(nqb)]
@@ -133,8 +133,16 @@ def _bsa_case(pb, units, nqb, b, d, n_dense, n_local, k, seed, scale_q=1.0):
 
 
 @pytest.mark.parametrize("d,b", [(128, 60), (64, 64), (128, 64), (64, 60), (128, 17)])
-def test_bsa_fwd_parity(pb, d, b):
-    _bsa_case(pb, 2, 5, b, d, 6, 16, 4, seed=d + b)
+@pytest.mark.parametrize("stream_k", [True, False])
+def test_bsa_fwd_parity(pb, d, b, stream_k):
+    _bsa_case(pb, 2, 5, b, d, 6, 16, 4, seed=d + b, stream_k=stream_k)
+
+
+def test_bsa_fwd_stream_k_many_tiles(pb):
+    """More tiles than CTA slots: whole tiles, split tiles and the partial merge all exercised;
+    stream-K and whole-tile schedules must agree."""
+    _bsa_case(pb, 40, 17, 60, 128, 10, 24, 6, seed=21)
+    _bsa_case(pb, 40, 17, 60, 128, 10, 24, 6, seed=21, stream_k=False)
 
 
 def test_bsa_fwd_dense_only_and_full_local(pb):
