@@ -3,6 +3,7 @@
 #include <cudaTypedefs.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -131,6 +132,13 @@ void free_mem(pbsa_mem* m) {
                     m->dev.keys, m->qc, m->s_t, m->ws, m->sel, m->k3ws};
     for (void* p : ptrs)
         if (p) cudaFree(p);
+}
+
+// The stream-K schedule of K3 is correct but measured slower than whole tiles at the Wan-1.3B
+// shape; opt in with PBSA_STREAM_K=1.
+bool use_stream_k() {
+    static const bool on = getenv("PBSA_STREAM_K") && atoi(getenv("PBSA_STREAM_K")) != 0;
+    return on;
 }
 
 MemCounts next_counts(const pbsa_mem* m, const MemCounts& c, int* dropped) {
@@ -458,7 +466,8 @@ int pbsa_attend(pbsa_mem* m, const void* q, int k_top, float scale, int mode, vo
     // (c) block-sparse attention over P ++ current (dense) and the selected local blocks
     if (int rc = launch_bsa_fwd(static_cast<const bf16*>(q), m->k_pool, m->v_pool, m->S, m->dev.dense,
                                 m->C + bpc, n_p + bpc, m->dev.l_slot, m->Lcap, n_l, m->sel, k, bpc, b, d, U,
-                                scale, static_cast<bf16*>(o), lse, m->k3ws, m->k3ws_bytes, s))
+                                scale, static_cast<bf16*>(o), lse, use_stream_k() ? m->k3ws : nullptr,
+                                m->k3ws_bytes, s))
         return rc;
     prof_mark(m, 3, s);
     // (d) persistent-memory update after the k=0 pass

@@ -29,16 +29,17 @@ for u in range(U):
     for t in range(0, nqb, 2):
         un += nd + len(set(sc[u, t].tolist()) | set(sc[u, t + 1].tolist()))
 exe = 4.0 * 128 * 64 * d * un
-for _ in range(3):
-    pb.attention_sparse(q, kp, vp, dense, local, sel, b)
-torch.cuda.synchronize()
-e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
-reps = 20
-e0.record()
-for _ in range(reps):
-    pb.attention_sparse(q, kp, vp, dense, local, sel, b)
-e1.record()
-torch.cuda.synchronize()
-ms = e0.elapsed_time(e1) / reps
-print(f"ablate={os.environ.get('PBSA_ABLATE', '0')} ms={ms:.4f} alg_TFLOPs={alg / ms / 1e9:.1f} "
-      f"exec_TFLOPs={exe / ms / 1e9:.1f} exec/alg={exe / alg:.3f}")
+for sk in (True, False):
+    for _ in range(3):
+        pb.attention_sparse(q, kp, vp, dense, local, sel, b, stream_k=sk)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    reps = 20
+    e0.record()
+    for _ in range(reps):
+        pb.attention_sparse(q, kp, vp, dense, local, sel, b, stream_k=sk)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    print(f"ablate={os.environ.get('PBSA_ABLATE', '0')} stream_k={sk} ms={ms:.4f} alg_TFLOPs={alg / ms / 1e9:.1f} "
+          f"exec_TFLOPs={exe / ms / 1e9:.1f} exec/alg={exe / alg:.3f}")
