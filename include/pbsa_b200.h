@@ -122,6 +122,10 @@ int pbsa_mem_commit(pbsa_mem* m, const float* s_t, void* stream);
 enum { PBSA_MODE_DENOISE = 0, PBSA_MODE_CACHE_UPDATE = 1 };
 int pbsa_attend(pbsa_mem* m, const void* q, int k_top, float scale, int mode, void* o,
                 float* lse, void* stream);
+/* Invalid-input status since the last reset (synchronises `stream`): bit 0 = NaN coarse logits
+ * seen by K2, bit 1 = NaN scores seen by K4.  The reference rejects NaN scores
+ * (tensor.cpp:61-64); the device path keeps a consistent state (NaN ranks lowest) and reports. */
+int pbsa_mem_status(const pbsa_mem* m, int* flags, void* stream);
 /* last selection of pbsa_attend (device): [units][blocks_per_chunk][k] ascending, and last s_t */
 int pbsa_last_selection(const pbsa_mem* m, const int32_t** sel, int* k, const float** s_t,
                         int* n_keys);

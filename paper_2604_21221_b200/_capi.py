@@ -51,6 +51,7 @@ _SIGS = {
                                    C.POINTER(_i32)]),
     "pbsa_mem_profile": (_i32, [_vp, _i32, _i32]),
     "pbsa_mem_profile_read": (_i32, [_vp, C.POINTER(C.c_double), C.POINTER(_i32), C.POINTER(_i32)]),
+    "pbsa_mem_status": (_i32, [_vp, C.POINTER(_i32), _vp]),
     "pbsa_copy": (_i32, [_vp, _vp, C.c_size_t, _vp]),
     "pbsa_debug_tile": (_i32, [_vp, _vp, _vp, _i32, _vp, _vp, _vp]),
 }

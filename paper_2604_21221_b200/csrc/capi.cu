@@ -129,7 +129,7 @@ void free_mem(pbsa_mem* m) {
     free_events(m);
     void* ptrs[] = {m->k_pool, m->v_pool, m->krep, m->dev.p_slot, m->dev.p_id, m->dev.p_score,
                     m->dev.l_slot, m->dev.l_id, m->dev.stage, m->dev.free_slot, m->dev.dense,
-                    m->dev.keys, m->qc, m->s_t, m->ws, m->sel, m->k3ws};
+                    m->dev.keys, m->qc, m->s_t, m->ws, m->sel, m->k3ws, m->dev.status};
     for (void* p : ptrs)
         if (p) cudaFree(p);
 }
@@ -287,6 +287,7 @@ int pbsa_mem_create(pbsa_mem** out, int units, int capacity_c, int window_chunks
               alloc(reinterpret_cast<void**>(&m->dev.free_slot), U * S * 4) &&
               alloc(reinterpret_cast<void**>(&m->dev.dense), U * (C + bpc) * 4) &&
               alloc(reinterpret_cast<void**>(&m->dev.keys), U * S * 4) &&
+              alloc(reinterpret_cast<void**>(&m->dev.status), 16) &&
               alloc(reinterpret_cast<void**>(&m->qc), U * bpc * d * 4) &&
               alloc(reinterpret_cast<void**>(&m->s_t), U * S * 4) &&
               alloc(reinterpret_cast<void**>(&m->sel), U * bpc * L * 4);
@@ -452,13 +453,13 @@ int pbsa_attend(pbsa_mem* m, const void* q, int k_top, float scale, int mode, vo
         const int n_keys = n_p + n_l + bpc;
         if (int rc = launch_score_select(m->qc, m->krep, static_cast<int64_t>(m->S) * d, m->dev.keys, m->S,
                                          n_keys, n_p, n_l, k, bpc, U, d, scale, m->sel, m->s_t, m->ws,
-                                         m->ws_bytes, s))
+                                         m->ws_bytes, s, m->dev.status))
             return rc;
         m->last_n_keys = n_keys;
     } else if (k > 0) {
         if (int rc = launch_score_select(m->qc, m->krep, static_cast<int64_t>(m->S) * d, m->dev.l_slot, m->Lcap,
                                          n_l, 0, n_l, k, bpc, U, d, scale, m->sel, nullptr, m->ws,
-                                         m->ws_bytes, s))
+                                         m->ws_bytes, s, m->dev.status))
             return rc;
     }
     m->last_k = k;
@@ -476,6 +477,13 @@ int pbsa_attend(pbsa_mem* m, const void* q, int k_top, float scale, int mode, vo
     prof_mark(m, 4, s);
     if (m->prof_on && m->prof_attend < m->prof_max) ++m->prof_attend;
     return rc;
+}
+
+int pbsa_mem_status(const pbsa_mem* m, int* flags, void* stream) {
+    PBSA_REQUIRE(m != nullptr && flags != nullptr, "mem_status: null pointer");
+    PBSA_CUDA(cudaMemcpyAsync(flags, m->dev.status, sizeof(int), cudaMemcpyDeviceToHost, as_stream(stream)));
+    PBSA_CUDA(cudaStreamSynchronize(as_stream(stream)));
+    return PBSA_OK;
 }
 
 int pbsa_last_selection(const pbsa_mem* m, const int32_t** sel, int* k, const float** s_t, int* n_keys) {

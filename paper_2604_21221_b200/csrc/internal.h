@@ -29,7 +29,7 @@ size_t score_select_workspace(int units, int nqb, int n_keys);
 int launch_score_select(const float* qc, const float* krep, int64_t krep_unit_stride,
                         const int32_t* key_slots, int key_stride, int n_keys, int local_off,
                         int n_local, int k, int nqb, int units, int d, float scale, int32_t* sel,
-                        float* s_t, void* ws, size_t ws_bytes, cudaStream_t s);
+                        float* s_t, void* ws, size_t ws_bytes, cudaStream_t s, int* status = nullptr);
 // K3
 int launch_bsa_fwd(const bf16* q, const bf16* k_pool, const bf16* v_pool, int n_slots,
                    const int32_t* dense, int dense_stride, int n_dense, const int32_t* local,
@@ -49,6 +49,7 @@ struct MemDev {
     int32_t* free_slot;  // [U][S]
     int32_t* dense;    // [U][C+bpc]
     int32_t* keys;     // [U][S]
+    int* status;       // device status word: bit 0 NaN logits (K2), bit 1 NaN scores (K4)
 };
 struct MemCounts {
     int n_p, n_sinks, n_l, n_free;

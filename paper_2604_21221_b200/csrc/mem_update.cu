@@ -26,7 +26,10 @@ struct CommitParams {
     MemCounts cur, next;
 };
 
+__device__ __forceinline__ float nan_low(float x) { return x != x ? -INFINITY : x; }
+
 __global__ void mem_init_kernel(MemDev m, int C, int Lcap, int bpc, int S) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *m.status = 0;
     const int u = blockIdx.x;
     for (int i = threadIdx.x; i < bpc; i += blockDim.x) {
         m.stage[static_cast<int64_t>(u) * bpc + i] = i;
@@ -98,15 +101,19 @@ __global__ void __launch_bounds__(256) mem_commit_kernel(const CommitParams p) {
     for (int i = tid; i < n_cand; i += nt) {
         int keep = 1;
         if (i >= n_s && !(sink_chunk && i >= n_p)) {
-            const float si = c_score[i];
+            // (score desc, id asc) is a strict total order once NaN (invalid input, which the
+            // reference rejects, tensor.cpp:61-64) ranks below every number: exactly dyn_cap
+            // candidates survive whatever the scores are, so the slot accounting stays exact
+            const float si = nan_low(c_score[i]);
             const int64_t ii = c_id[i];
             int rank = 0;
             for (int j = n_s; j < n_cand; ++j) {
                 if (sink_chunk && j >= n_p) break;
-                const float sj = c_score[j];
+                const float sj = nan_low(c_score[j]);
                 rank += (sj > si) || (sj == si && c_id[j] < ii);
             }
             keep = rank < dyn_cap;
+            if (c_score[i] != c_score[i]) atomicOr(p.m.status, 2);
         }
         c_keep[i] = keep;
     }

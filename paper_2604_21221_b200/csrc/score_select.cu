@@ -155,7 +155,8 @@ __device__ void warp_topk(const uint32_t* pb, int n, int k, uint32_t* hist, int3
         const int tie_rank = tie_run + __popc(eb & lt);
         const bool take = gt || (eq && tie_rank < kk);
         const uint32_t tb = __ballot_sync(0xffffffffu, take);
-        if (take) out[run + __popc(tb & lt)] = j;
+        const int pos = run + __popc(tb & lt);
+        if (take && pos < k) out[pos] = j;
         run += __popc(tb);
         tie_run += __popc(eb);
     }
@@ -167,6 +168,7 @@ struct SelectParams {
     size_t per_warp;      // bytes of smem per warp (16-aligned)
     int32_t* sel;         // [U][nqb][k]
     float* arows;         // [U][nqb][n_keys] or null
+    int* status;          // nullable: bit 0 set when a logit row holds NaN (invalid input)
 };
 
 __global__ void __launch_bounds__(256) select_kernel(const SelectParams p) {
@@ -181,7 +183,12 @@ __global__ void __launch_bounds__(256) select_kernel(const SelectParams p) {
     uint32_t* pb = reinterpret_cast<uint32_t*>(base + static_cast<size_t>(n) * 12);
     uint32_t* hist = pb + p.n_local;
     const float* src = p.logits + row * n;
-    for (int j = lane; j < n; j += 32) z[j] = src[j];
+    bool bad = false;
+    for (int j = lane; j < n; j += 32) {
+        z[j] = src[j];
+        bad |= src[j] != src[j];
+    }
+    if (p.status != nullptr && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(p.status, 1);
     __syncwarp();
     if (p.k > 0 && p.n_local > 0) {
         warp_softmax(z + p.local_off, p.n_local, e, pb, nullptr);
@@ -211,7 +218,7 @@ size_t score_select_workspace(int units, int nqb, int n_keys) {
 int launch_score_select(const float* qc, const float* krep, int64_t kru, const int32_t* keys,
                         int key_stride, int n_keys, int local_off, int n_local, int k, int nqb,
                         int units, int d, float scale, int32_t* sel, float* s_t, void* ws,
-                        size_t ws_bytes, cudaStream_t s) {
+                        size_t ws_bytes, cudaStream_t s, int* status) {
     if (units == 0 || nqb == 0 || n_keys == 0) return 0;
     const bool do_select = k > 0 && n_local > 0;
     if (!do_select && s_t == nullptr) return 0;
@@ -238,7 +245,7 @@ int launch_score_select(const float* qc, const float* krep, int64_t kru, const i
         int rows = static_cast<int>(budget / per_warp);
         rows = rows < 1 ? 1 : (rows > 8 ? 8 : rows);
         SelectParams p{logits, n_keys, local_off, n_local, do_select ? k : 0, nqb, units, rows, per_warp,
-                       sel, arows};
+                       sel, arows, status};
         const size_t smem = per_warp * rows;
         static size_t configured = 0;
         if (smem > 48 * 1024 && smem > configured) {

@@ -273,6 +273,12 @@ class Memory:
         keys = ["kv_write", "compress_q", "score_select", "bsa_fwd", "mem_update"]
         return {"ms": dict(zip(keys, list(ms))), "attend_calls": na.value, "kv_writes": nw.value}
 
+    def status(self) -> int:
+        """Invalid-input flags since the last reset (bit 0 NaN logits, bit 1 NaN scores)."""
+        f = C.c_int()
+        check(LIB.pbsa_mem_status(self._h, C.byref(f), _stream()))
+        return f.value
+
     def last_selection(self):
         sel, k, st, nk = C.c_void_p(), C.c_int(), C.c_void_p(), C.c_int()
         check(LIB.pbsa_last_selection(self._h, C.byref(sel), C.byref(k), C.byref(st), C.byref(nk)))

@@ -1,0 +1,280 @@
+"""Alg. 1 rollout driver over the B200 PBSA path, with JSONL memory traces.
+
+Reference: SPEC.md:419-508 (module rollout) and PAPER.md:197-230 (Algorithm 1).  This is the
+CALLER of the hot path: it drives one pbsa.Memory per layer through
+M chunks x T denoise steps + the k=0 cache-update pass, exactly the call order that defines the
+per-chunk decode latency of BASELINE.json, and records the memory trace of SPEC.md:235 (one JSON
+record per (chunk, denoise index): persistent ids, window ids, evicted ids, scores, flags).
+
+The denoiser is SPEC's ToyDenoiser: seeded linear maps W_q, W_k, W_v,
+W_o per layer on blockified latents; x_hat_0 = W_o . PBSA output (+ residual).  It is plumbing
+(torch matmuls); the attention/memory path is the product (pbsa.Memory -> libpbsa_b200.so).
+"""
+from __future__ import annotations
+
+import argparse
+import dataclasses
+import json
+import math
+import os
+import time
+
+import torch
+
+from . import pbsa
+
+# ---------------------------------------------------------------- configuration
+
+
+@dataclasses.dataclass
+class RolloutConfig:
+    num_chunks: int = 4                      # M
+    timesteps: tuple = (1.0, 0.75, 0.5, 0.25)  # t_T .. t_1, strictly decreasing
+    topk_ratio: float = 0.25
+    capacity_frames: int = 6                 # C
+    window_frames: int = 12                  # L_local (frames; whole chunks)
+    chunk_frames: int = 3
+    height: int = 30
+    width: int = 52
+    block_shape: tuple = (1, 15, 4)          # (b_t, b_h, b_w)
+    layers: int = 2
+    heads: int = 12
+    head_dim: int = 128
+    seed: int = 7
+    trace_units: int = 1                     # heads recorded in the trace (unit 0..n-1)
+
+    def validate(self):
+        ts = list(self.timesteps)
+        if not ts or any(not (0.0 < t <= 1.0) for t in ts) or any(a <= b for a, b in zip(ts, ts[1:])):
+            raise ValueError("timesteps must be strictly decreasing values in (0,1]")
+        if self.num_chunks < 1:
+            raise ValueError("num_chunks must be >= 1")
+        bt, bh, bw = self.block_shape
+        for ax, n, bsz in (("t", self.chunk_frames, bt), ("h", self.height, bh), ("w", self.width, bw)):
+            if n % bsz:
+                raise ValueError(f"axis {ax} ({n}) not divisible by block extent ({bsz})")
+        if self.window_frames % self.chunk_frames or self.capacity_frames % bt:
+            raise ValueError("window must be whole chunks and capacity whole block rows")
+
+    @property
+    def b(self) -> int:
+        return self.block_shape[0] * self.block_shape[1] * self.block_shape[2]
+
+    @property
+    def blocks_per_frame(self) -> int:
+        return (self.height // self.block_shape[1]) * (self.width // self.block_shape[2])
+
+    @property
+    def blocks_per_chunk(self) -> int:
+        return (self.chunk_frames // self.block_shape[0]) * self.blocks_per_frame
+
+    @property
+    def capacity_blocks(self) -> int:
+        return (self.capacity_frames // self.block_shape[0]) * self.blocks_per_frame
+
+    @property
+    def window_chunks(self) -> int:
+        return self.window_frames // self.chunk_frames
+
+    @property
+    def d_model(self) -> int:
+        return self.heads * self.head_dim
+
+
+def sigma(t: float) -> float:
+    """Linear schedule, sigma(0) = 0."""
+    return float(t)
+
+
+def renoise(x0_hat: torch.Tensor, eps: torch.Tensor, t: float) -> torch.Tensor:
+    """Psi(x0_hat, eps, t) = (1 - sigma(t)) x0_hat + sigma(t) eps."""
+    if x0_hat.shape != eps.shape:
+        raise ValueError("renoise: shape mismatch")
+    s = sigma(t)
+    return (1.0 - s) * x0_hat + s * eps
+
+
+def blockify_tokens(x: torch.Tensor, shape) -> torch.Tensor:
+    """(t, h, w, d) -> block-major (n_b*b, d) (blockify.cpp:38-65)."""
+    t, h, w, d = x.shape
+    bt, bh, bw = shape
+    x = x.reshape(t // bt, bt, h // bh, bh, w // bw, bw, d).permute(0, 2, 4, 1, 3, 5, 6)
+    return x.reshape(-1, d)
+
+
+def unblockify_tokens(xb: torch.Tensor, dims, shape) -> torch.Tensor:
+    t, h, w, d = dims
+    bt, bh, bw = shape
+    x = xb.reshape(t // bt, h // bh, w // bw, bt, bh, bw, d).permute(0, 3, 1, 4, 2, 5, 6)
+    return x.reshape(t, h, w, d)
+
+
+class ToyDenoiser:
+    """Seeded linear maps per layer; deterministic per seed."""
+
+    def __init__(self, cfg: RolloutConfig, device="cuda"):
+        g = torch.Generator(device="cpu").manual_seed(cfg.seed)
+        dm = cfg.d_model
+        std = 1.0 / math.sqrt(dm)
+        self.w = [[(torch.randn(dm, dm, generator=g) * std).to(device, torch.bfloat16) for _ in range(4)]
+                  for _ in range(cfg.layers)]
+        self.cfg = cfg
+
+    def qkv(self, layer: int, x: torch.Tensor, t: float):
+        """x: [n_tok, d_model] bf16 (block-major tokens) -> q, k, v as [heads, n_tok, head_dim]."""
+        cfg = self.cfg
+        wq, wk, wv, _ = self.w[layer]
+        # RMS-normalised layer input (keeps a deep toy stack finite) + timestep conditioning
+        xf = x.float()
+        xt = (xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + 1e-6) * (1.0 + 0.1 * t)).to(x.dtype)
+        out = []
+        for w in (wq, wk, wv):
+            y = (xt @ w).view(x.shape[0], cfg.heads, cfg.head_dim).transpose(0, 1).contiguous()
+            out.append(y)
+        return out
+
+    def project_out(self, layer: int, o: torch.Tensor, x: torch.Tensor) -> torch.Tensor:
+        """o: [heads, n_tok, head_dim] -> residual update of x."""
+        wo = self.w[layer][3]
+        y = o.transpose(0, 1).reshape(x.shape[0], self.cfg.d_model) @ wo
+        return x + y * (1.0 / self.cfg.layers)
+
+
+# ---------------------------------------------------------------- Alg. 1
+
+
+def run_inference(cfg: RolloutConfig, denoiser: ToyDenoiser | None = None, trace_path: str | None = None,
+                  device="cuda", record_scores: bool = True):
+    """Returns (frames [list of (t,h,w,d) bf16 chunks], trace [list of dicts], timing dict)."""
+    cfg.validate()
+    den = denoiser or ToyDenoiser(cfg, device)
+    bpc, b, U = cfg.blocks_per_chunk, cfg.b, cfg.heads
+    k_top = None
+    mems = [pbsa.Memory(U, cfg.capacity_blocks, cfg.window_chunks, bpc, b, cfg.head_dim)
+            for _ in range(cfg.layers)]
+    g = torch.Generator(device=device).manual_seed(cfg.seed + 1)
+    dims = (cfg.chunk_frames, cfg.height, cfg.width, cfg.d_model)
+    frames, trace = [], []
+    calls = 0
+    stream = torch.cuda.current_stream()
+    ev = []
+    for i in range(cfg.num_chunks):
+        x = torch.randn(dims, device=device, generator=g).to(torch.bfloat16)  # x ~ N(0, I)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for jj, t in enumerate(cfg.timesteps):
+            j = len(cfg.timesteps) - jj  # j = T .. 1
+            xb = blockify_tokens(x, cfg.block_shape)
+            h = xb
+            for layer, mem in enumerate(mems):
+                q, k, v = den.qkv(layer, h, t)
+                n_l = mem.info().n_l
+                k_top = pbsa.topk_count(n_l, cfg.topk_ratio) if n_l else 0
+                mem.write_chunk(k, v)
+                o = mem.attend(q, k_top, pbsa.MODE_DENOISE)
+                h = den.project_out(layer, o, h)
+                calls += 1
+            x0_hat = unblockify_tokens(h, dims, cfg.block_shape)
+            rec = {"chunk": i, "j": j, "t": t, "cache_updated": j == 1, "grad_enabled": False}
+            if j == 1:
+                frames.append(x0_hat)
+                # k = 0 pass on the clean chunk: scores, push/evict, Top-C (Alg. 1 lines 9-10)
+                hb = blockify_tokens(x0_hat, cfg.block_shape)
+                before = [_ids(m, cfg.trace_units) for m in mems[:1]]
+                for layer, mem in enumerate(mems):
+                    q, k, v = den.qkv(layer, hb, 0.0)
+                    n_l = mem.info().n_l
+                    k_top = pbsa.topk_count(n_l, cfg.topk_ratio) if n_l else 0
+                    mem.write_chunk(k, v)
+                    o = mem.attend(q, k_top, pbsa.MODE_CACHE_UPDATE)
+                    if layer == 0 and record_scores:
+                        _, s_t = mem.last_selection()
+                        rec["scores"] = [[float(v_) for v_ in s_t[u].tolist()] for u in range(cfg.trace_units)]
+                    hb = den.project_out(layer, o, hb)
+                p_ids, l_ids = _ids(mems[0], cfg.trace_units)
+                prev_l = before[0][1]
+                rec["evicted"] = [sorted(set(prev_l[u]) - set(l_ids[u])) for u in range(cfg.trace_units)]
+                rec["persistent"] = p_ids
+                rec["window"] = l_ids
+            else:
+                eps = torch.randn(dims, device=device, generator=g).to(torch.bfloat16)
+                x = renoise(x0_hat, eps, cfg.timesteps[jj + 1]).to(torch.bfloat16)
+            trace.append(rec)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record(stream)
+        ev.append((e0, e1))
+    torch.cuda.synchronize()
+    chunk_ms = [a.elapsed_time(b_) for a, b_ in ev]
+    status = max(m.status() for m in mems)
+    for m in mems:
+        m.close()
+    if trace_path:
+        with open(trace_path, "w") as f:
+            for rec in trace:
+                f.write(json.dumps(rec) + "\n")
+    return frames, trace, {"chunk_ms": chunk_ms, "pbsa_calls": calls, "invalid_input_flags": status}
+
+
+def _ids(mem: pbsa.Memory, n_units: int):
+    p, l_ = mem.assemble()
+    return [p[u].tolist() for u in range(n_units)], [l_[u].tolist() for u in range(n_units)]
+
+
+def check_trace(cfg: RolloutConfig, trace) -> None:
+    """SPEC.md:484-488 / acceptance 6: cache updates exactly once per chunk at j=1, |P| <= C,
+    |window| <= L_local, evicted ids strictly increasing, P and L disjoint."""
+    updates = [r for r in trace if r["cache_updated"]]
+    if len(updates) != cfg.num_chunks or any(r["j"] != 1 for r in updates):
+        raise AssertionError("cache updates must happen exactly once per chunk, at j = 1")
+    if len(trace) != cfg.num_chunks * len(cfg.timesteps):
+        raise AssertionError("one trace record per (chunk, denoise step)")
+    last = -1
+    for r in updates:
+        for u, (p, l_) in enumerate(zip(r["persistent"], r["window"])):
+            if len(p) > cfg.capacity_blocks or len(l_) > cfg.window_chunks * cfg.blocks_per_chunk:
+                raise AssertionError("capacity exceeded")
+            if set(p) & set(l_):
+                raise AssertionError("P and L overlap")
+        ev = r["evicted"][0]
+        if ev:
+            if min(ev) <= last:
+                raise AssertionError("eviction ids must strictly increase")
+            last = max(ev)
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description="Sparse Forcing Alg. 1 rollout on the B200 PBSA path")
+    ap.add_argument("--frames", type=int, default=12, help="latent frames to generate (multiple of chunk)")
+    ap.add_argument("--steps", type=int, default=4, help="denoise steps T")
+    ap.add_argument("--topk", type=float, default=0.25)
+    ap.add_argument("--capacity-frames", type=int, default=6)
+    ap.add_argument("--window-frames", type=int, default=12)
+    ap.add_argument("--layers", type=int, default=30)
+    ap.add_argument("--heads", type=int, default=12)
+    ap.add_argument("--seed", type=int, default=7)
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args(argv)
+    if a.frames < 3 or a.frames % 3:
+        raise SystemExit(2)
+    ts = tuple(1.0 - i / a.steps for i in range(a.steps))
+    cfg = RolloutConfig(num_chunks=a.frames // 3, timesteps=ts, topk_ratio=a.topk,
+                        capacity_frames=a.capacity_frames, window_frames=a.window_frames,
+                        layers=a.layers, heads=a.heads, seed=a.seed)
+    trace_path = None
+    if a.out:
+        os.makedirs(a.out, exist_ok=True)
+        trace_path = os.path.join(a.out, "trace.jsonl")
+    t0 = time.time()
+    frames, trace, timing = run_inference(cfg, trace_path=trace_path)
+    check_trace(cfg, trace)
+    steady = timing["chunk_ms"][cfg.window_chunks + 2:] or timing["chunk_ms"]
+    print(json.dumps({"chunks": cfg.num_chunks, "layers": cfg.layers, "heads": cfg.heads,
+                      "pbsa_calls": timing["pbsa_calls"], "chunk_ms": timing["chunk_ms"],
+                      "invalid_input_flags": timing["invalid_input_flags"],
+                      "steady_chunk_ms_median": sorted(steady)[len(steady) // 2],
+                      "wall_s": time.time() - t0}))
+    return 0
+
+
+if __name__ == "__main__":
+    raise SystemExit(main())
