@@ -55,7 +55,8 @@ struct BsaParams {
     float* lse;
     float scale_log2;
     int max_list, bm_words;
-    int ablate;  // perf experiments only (PBSA_ABLATE): 1 = softmax writes P=0 without computing
+    long long* trace;  // perf experiments only: per-event clock64 stamps of CTA 0 (null = off)
+    int ablate;  // perf experiments only (PBSA_ABLATE): 1 no softmax math, 2 no K/V loads, 3 no MMAs
     // schedule
     int tiles_per_unit, n_tiles, grid;
     int64_t vlen, vtotal;  // virtual length of one tile (upper bound of its list) and of all tiles
@@ -92,6 +93,10 @@ struct Layout {
         return 1024 + kOffList + 2 * static_cast<size_t>(max_list) * 4 + 2 * static_cast<size_t>(bm_words) * 4;
     }
 };
+
+__device__ __forceinline__ void stamp(const BsaParams& p, int ev, int j) {
+    if (p.trace != nullptr && blockIdx.x == 0 && j < 256) p.trace[ev * 256 + j] = clock64();
+}
 
 // CTA holding virtual position x (stream-K ranges B_c = floor(c * W / G))
 __device__ __forceinline__ int cta_of(int64_t x, int64_t W, int G) {
@@ -205,6 +210,10 @@ __global__ void __launch_bounds__(kThreads, 2)
                         const int j = jg + idx;
                         const int s = j % NSV;
                         mbar_wait(v_empty + s, ((j / NSV) & 1) ^ 1);
+                        if (p.ablate == 2) {  // experiment: no K/V traffic
+                            mbar_arrive(v_full + s);
+                            return;
+                        }
                         mbar_arrive_expect_tx(v_full + s, L::kKVBytes);
                         const int row0 = (fm.u * p.n_slots + (list[fm.e0 + idx] & 0xFFFFFF)) * 64;
                         for (int h = 0; h < L::kHalves; ++h)
@@ -214,10 +223,14 @@ __global__ void __launch_bounds__(kThreads, 2)
                         const int j = jg + idx;
                         const int s = j % NSK;
                         mbar_wait(k_empty + s, ((j / NSK) & 1) ^ 1);
-                        mbar_arrive_expect_tx(k_full + s, L::kKVBytes);
-                        const int row0 = (fm.u * p.n_slots + (list[fm.e0 + idx] & 0xFFFFFF)) * 64;
-                        for (int h = 0; h < L::kHalves; ++h)
-                            tma_load_2d(k_smem + s * L::kKVBytes + h * 8192, &tm_k, k_full + s, h * 64, row0);
+                        if (p.ablate == 2) {
+                            mbar_arrive(k_full + s);
+                        } else {
+                            mbar_arrive_expect_tx(k_full + s, L::kKVBytes);
+                            const int row0 = (fm.u * p.n_slots + (list[fm.e0 + idx] & 0xFFFFFF)) * 64;
+                            for (int h = 0; h < L::kHalves; ++h)
+                                tma_load_2d(k_smem + s * L::kKVBytes + h * 8192, &tm_k, k_full + s, h * 64, row0);
+                        }
                         if (idx >= 1) load_v(idx - 1);
                     }
                     load_v(nf - 1);
@@ -228,33 +241,42 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
     } else if (warp == 1) {
         // ============================================================== tcgen05 issuer
-        if (lane == 0) {
+        // The whole warp runs the loop so every descriptor is warp-uniform (uniform registers,
+        // no per-instruction R2UR); one lane issues each tcgen05 instruction.
+        {
             constexpr uint32_t idesc_s = idesc_bf16_f32(128, 64, 0, 0);
             constexpr uint32_t idesc_o = idesc_bf16_f32(128, D, 0, 1);
-            const uint32_t q_base = smem_u32(q_smem);
-            const uint32_t k_base = smem_u32(k_smem);
-            const uint32_t v_base = smem_u32(v_smem);
+            const bool do_mma = p.ablate != 3;
+            const uint64_t qdesc = smem_desc_sw128(smem_u32(q_smem), 16, 1024);
+            const uint64_t kdesc = smem_desc_sw128(smem_u32(k_smem), 16, 1024);
+            const uint64_t vdesc = smem_desc_sw128(smem_u32(v_smem), 8192, 1024);
             int jg = 0, q_uses = 0;
             auto issue_s = [&](int j) {
                 const int s = j % NSK;
                 mbar_wait(k_full + s, (j / NSK) & 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem + L::kSColBase + (j & 1) * 64;
+                const uint64_t kd = kdesc + ((s * L::kKVBytes) >> 4);
+                if (elect_one()) {
+                    if (do_mma) {
 #pragma unroll
-                for (int kk = 0; kk < D / 16; ++kk) {
-                    const uint32_t off = (kk & 3) * 32;
-                    const uint64_t a = smem_desc_sw128(q_base + (kk >> 2) * 16384 + off, 16, 1024);
-                    const uint64_t b = smem_desc_sw128(k_base + s * L::kKVBytes + (kk >> 2) * 8192 + off, 16, 1024);
-                    mma_ss(d_tmem, a, b, idesc_s, kk > 0 ? 1u : 0u);
+                        for (int kk = 0; kk < D / 16; ++kk) {
+                            const uint32_t off_q = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
+                            const uint32_t off_k = ((kk >> 2) * 8192 + (kk & 3) * 32) >> 4;
+                            mma_ss(d_tmem, qdesc + off_q, kd + off_k, idesc_s, kk > 0 ? 1u : 0u);
+                        }
+                    }
+                    mma_commit(k_empty + s);
+                    mma_commit(s_full + (j & 1));
                 }
-                mma_commit(k_empty + s);
-                mma_commit(s_full + (j & 1));
+                __syncwarp();
             };
             for (int f = 0; f < n_frag; ++f) {
                 const int lb = f & 1;
                 mbar_wait(list_full + lb, (f >> 1) & 1);
                 const int nf = meta[lb].e1 - meta[lb].e0;
-                mbar_arrive(list_empty + lb);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(list_empty + lb);
                 if (f > 0) mbar_wait(o_free, (f - 1) & 1);  // previous epilogue has read O
                 if (nf == 0) continue;
                 mbar_wait(q_full, q_uses & 1);
@@ -262,21 +284,31 @@ __global__ void __launch_bounds__(kThreads, 2)
                 issue_s(jg);
                 for (int idx = 0; idx < nf; ++idx) {
                     const int j = jg + idx;
+                    stamp(p, 0, j);  // MMA: before issuing S_{j+1}
                     if (idx + 1 < nf) issue_s(j + 1);
                     const int sv = j % NSV;
+                    stamp(p, 1, j);  // MMA: S_{j+1} issued, waiting for P_j
                     mbar_wait(p_full + (j & 1), (j >> 1) & 1);
+                    stamp(p, 2, j);  // MMA: P_j seen
                     mbar_wait(v_full + sv, (j / NSV) & 1);
                     tc_fence_after();
                     const uint32_t a_tmem = tmem + L::kSColBase + (j & 1) * 64;
+                    const uint64_t vd = vdesc + ((sv * L::kKVBytes) >> 4);
+                    if (elect_one()) {
+                        if (do_mma) {
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) {
-                        const uint64_t b = smem_desc_sw128(v_base + sv * L::kKVBytes + kk * 2048, 8192, 1024);
-                        mma_ts(tmem, a_tmem + kk * 8, b, idesc_o, (idx > 0 || kk > 0) ? 1u : 0u);
+                            for (int kk = 0; kk < 4; ++kk)
+                                mma_ts(tmem, a_tmem + kk * 8, vd + ((kk * 2048) >> 4), idesc_o,
+                                       (idx > 0 || kk > 0) ? 1u : 0u);
+                        }
+                        mma_commit(v_empty + sv);
+                        mma_commit(o_done + (j & 1));
                     }
-                    mma_commit(v_empty + sv);
-                    mma_commit(o_done + (j & 1));
+                    __syncwarp();
+                    stamp(p, 3, j);  // MMA: PV_j issued
                 }
-                mma_commit(q_empty);  // every S MMA reading this Q has been issued
+                if (elect_one()) mma_commit(q_empty);  // every S MMA reading this Q has been issued
+                __syncwarp();
                 ++q_uses;
                 jg += nf;
             }
@@ -399,7 +431,9 @@ __global__ void __launch_bounds__(kThreads, 2)
             for (int idx = 0; idx < nf; ++idx) {
                 const int j = jg + idx;
                 const int buf = j & 1;
+                if (threadIdx.x == 64) stamp(p, 4, j);  // softmax warp 2 lane 0: waiting for S_j
                 mbar_wait(s_full + buf, (j >> 1) & 1);
+                if (threadIdx.x == 64) stamp(p, 5, j);  // S_j seen
                 tc_fence_after();
                 pv_done(j - 2);  // already complete: S_j was committed after PV_{j-2}
                 const uint32_t t_s = t_o + L::kSColBase + buf * 64;
@@ -481,6 +515,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 tmem_st32(t_s, pk);
                 tmem_wait_st();
                 tc_fence_before();
+                if (threadIdx.x == 64) stamp(p, 6, j);  // about to arrive P_j
                 mbar_arrive(p_full + buf);
             }
             pv_done(jg + nf - 2);
@@ -670,6 +705,14 @@ size_t bsa_fwd_workspace(int units, int nqb, int d) {
     return slots * 128 * d * 4 + slots * 256 * 4 + tiles * 4 + 256;
 }
 
+static long long* g_trace = nullptr;
+
+}  // namespace pbsa
+
+extern "C" void pbsa_debug_trace_buffer(void* p) { pbsa::g_trace = static_cast<long long*>(p); }
+
+namespace pbsa {
+
 int launch_bsa_fwd(const bf16* q, const bf16* k_pool, const bf16* v_pool, int n_slots,
                    const int32_t* dense, int dense_stride, int n_dense, const int32_t* local,
                    int local_stride, int n_local, const int32_t* sel, int k, int nqb, int b, int d,
@@ -693,6 +736,7 @@ int launch_bsa_fwd(const bf16* q, const bf16* k_pool, const bf16* v_pool, int n_
     {
         static const int ablate = getenv("PBSA_ABLATE") ? atoi(getenv("PBSA_ABLATE")) : 0;
         p.ablate = ablate;
+        p.trace = g_trace;
     }
     p.bm_words = (n_local + 31) / 32 + 1;
     p.max_list = n_dense + (p.k > 0 ? (2 * p.k < n_local ? 2 * p.k : n_local) : 0);
