@@ -158,12 +158,12 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(s_full + s, 1);
-            mbar_init(p_full + s, 128);
+            mbar_init(p_full + s, 4);  // one elected arrival per softmax warp
             mbar_init(o_done + s, 1);
             mbar_init(list_full + s, 1);
             mbar_init(list_empty + s, 2);
         }
-        mbar_init(o_free, 128);
+        mbar_init(o_free, 4);
         fence_barrier_init();
         tma_prefetch(&tm_q);
         tma_prefetch(&tm_k);
@@ -189,7 +189,8 @@ __global__ void __launch_bounds__(kThreads, 2)
 
     if (warp == 0) {
         // ============================================================== TMA producer
-        if (lane == 0) {
+        // whole warp in the loop (uniform operands), one elected lane issues each TMA
+        {
             int jg = 0, q_uses = 0;
             for (int f = 0; f < n_frag; ++f) {
                 const int lb = f & 1;
@@ -200,43 +201,53 @@ __global__ void __launch_bounds__(kThreads, 2)
                 if (nf > 0) {
                     if (q_uses > 0) mbar_wait(q_empty, (q_uses - 1) & 1);
                     const uint32_t qbytes = (fm.has2 ? 2u : 1u) * L::kHalves * static_cast<uint32_t>(p.b) * 128u;
-                    mbar_arrive_expect_tx(q_full, qbytes);
-                    for (int r = 0; r < (fm.has2 ? 2 : 1); ++r)
-                        for (int h = 0; h < L::kHalves; ++h)
-                            tma_load_3d(q_smem + h * 16384 + r * 8192, &tm_q, q_full, h * 64, 0,
-                                        fm.u * p.nqb + fm.qb0 + r);
+                    if (elect_one()) {
+                        mbar_arrive_expect_tx(q_full, qbytes);
+                        for (int r = 0; r < (fm.has2 ? 2 : 1); ++r)
+                            for (int h = 0; h < L::kHalves; ++h)
+                                tma_load_3d(q_smem + h * 16384 + r * 8192, &tm_q, q_full, h * 64, 0,
+                                            fm.u * p.nqb + fm.qb0 + r);
+                    }
+                    __syncwarp();
                     ++q_uses;
                     auto load_v = [&](int idx) {
                         const int j = jg + idx;
                         const int s = j % NSV;
                         mbar_wait(v_empty + s, ((j / NSV) & 1) ^ 1);
-                        if (p.ablate == 2) {  // experiment: no K/V traffic
-                            mbar_arrive(v_full + s);
-                            return;
-                        }
-                        mbar_arrive_expect_tx(v_full + s, L::kKVBytes);
                         const int row0 = (fm.u * p.n_slots + (list[fm.e0 + idx] & 0xFFFFFF)) * 64;
-                        for (int h = 0; h < L::kHalves; ++h)
-                            tma_load_2d(v_smem + s * L::kKVBytes + h * 8192, &tm_v, v_full + s, h * 64, row0);
+                        if (elect_one()) {
+                            if (p.ablate == 2) {  // experiment: no K/V traffic
+                                mbar_arrive(v_full + s);
+                            } else {
+                                mbar_arrive_expect_tx(v_full + s, L::kKVBytes);
+                                for (int h = 0; h < L::kHalves; ++h)
+                                    tma_load_2d(v_smem + s * L::kKVBytes + h * 8192, &tm_v, v_full + s, h * 64, row0);
+                            }
+                        }
+                        __syncwarp();
                     };
                     for (int idx = 0; idx < nf; ++idx) {
                         const int j = jg + idx;
                         const int s = j % NSK;
                         mbar_wait(k_empty + s, ((j / NSK) & 1) ^ 1);
-                        if (p.ablate == 2) {
-                            mbar_arrive(k_full + s);
-                        } else {
-                            mbar_arrive_expect_tx(k_full + s, L::kKVBytes);
-                            const int row0 = (fm.u * p.n_slots + (list[fm.e0 + idx] & 0xFFFFFF)) * 64;
-                            for (int h = 0; h < L::kHalves; ++h)
-                                tma_load_2d(k_smem + s * L::kKVBytes + h * 8192, &tm_k, k_full + s, h * 64, row0);
+                        const int row0 = (fm.u * p.n_slots + (list[fm.e0 + idx] & 0xFFFFFF)) * 64;
+                        if (elect_one()) {
+                            if (p.ablate == 2) {
+                                mbar_arrive(k_full + s);
+                            } else {
+                                mbar_arrive_expect_tx(k_full + s, L::kKVBytes);
+                                for (int h = 0; h < L::kHalves; ++h)
+                                    tma_load_2d(k_smem + s * L::kKVBytes + h * 8192, &tm_k, k_full + s, h * 64, row0);
+                            }
                         }
+                        __syncwarp();
                         if (idx >= 1) load_v(idx - 1);
                     }
                     load_v(nf - 1);
                     jg += nf;
                 }
-                mbar_arrive(list_empty + lb);
+                if (lane == 0) mbar_arrive(list_empty + lb);
+                __syncwarp();
             }
         }
     } else if (warp == 1) {
@@ -516,7 +527,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                 tmem_wait_st();
                 tc_fence_before();
                 if (threadIdx.x == 64) stamp(p, 6, j);  // about to arrive P_j
-                mbar_arrive(p_full + buf);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(p_full + buf);
             }
             pv_done(jg + nf - 2);
             pv_done(jg + nf - 1);
@@ -551,7 +563,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                 if (valid && p.lse != nullptr)
                     p.lse[orow_idx] = l > 0.0f ? (m + __log2f(l)) * 0.69314718055994531f : -INFINITY;
                 tc_fence_before();
-                mbar_arrive(o_free);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(o_free);
             } else {
                 // fragment of a split tile: unnormalised fp32 partial + (m, l)
                 float* po = p.part_o + (static_cast<int64_t>(fm.slot) * 128 + r) * D;
@@ -575,7 +588,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                 pml[r] = (nf > 0 && l > 0.0f) ? m : -INFINITY;
                 pml[128 + r] = nf > 0 ? l : 0.0f;
                 tc_fence_before();
-                mbar_arrive(o_free);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(o_free);
                 __threadfence();
                 named_bar_sync(1, 128);
                 if (t == 0) misc[1] = (atomicAdd(p.counters + tile, 1) == fm.nf - 1) ? 1u : 0u;
