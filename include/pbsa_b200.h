@@ -126,6 +126,11 @@ int pbsa_attend(pbsa_mem* m, const void* q, int k_top, float scale, int mode, vo
  * seen by K2, bit 1 = NaN scores seen by K4.  The reference rejects NaN scores
  * (tensor.cpp:61-64); the device path keeps a consistent state (NaN ranks lowest) and reports. */
 int pbsa_mem_status(const pbsa_mem* m, int* flags, void* stream);
+/* Fused form of pbsa_mem_write_chunk + pbsa_attend for a layer that has the current chunk's
+ * Q, K and V ([units][blocks_per_chunk*b][d] bf16): one ingest pass writes K/V into the stage
+ * slots and compresses K and Q (K1), then K2 -> K3 (-> K4) as pbsa_attend. */
+int pbsa_attend_qkv(pbsa_mem* m, const void* q, const void* k_chunk, const void* v_chunk, int k_top,
+                    float scale, int mode, void* o, float* lse, void* stream);
 /* last selection of pbsa_attend (device): [units][blocks_per_chunk][k] ascending, and last s_t */
 int pbsa_last_selection(const pbsa_mem* m, const int32_t** sel, int* k, const float** s_t,
                         int* n_keys);

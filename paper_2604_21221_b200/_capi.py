@@ -47,6 +47,7 @@ _SIGS = {
     "pbsa_mem_write_chunk": (_i32, [_vp, _vp, _vp, _vp]),
     "pbsa_mem_commit": (_i32, [_vp, _vp, _vp]),
     "pbsa_attend": (_i32, [_vp, _vp, _i32, _f32, _i32, _vp, _vp, _vp]),
+    "pbsa_attend_qkv": (_i32, [_vp, _vp, _vp, _vp, _i32, _f32, _i32, _vp, _vp, _vp]),
     "pbsa_last_selection": (_i32, [_vp, C.POINTER(_vp), C.POINTER(_i32), C.POINTER(_vp),
                                    C.POINTER(_i32)]),
     "pbsa_mem_profile": (_i32, [_vp, _i32, _i32]),

@@ -90,7 +90,7 @@ struct Layout {
     static constexpr uint32_t kOffList = kOffMisc + 16;
     static constexpr uint32_t kSColBase = D;  // S0 at D, S1 at D + 64
     static size_t bytes(int max_list, int bm_words) {
-        return 1024 + kOffList + 2 * static_cast<size_t>(max_list) * 4 + 2 * static_cast<size_t>(bm_words) * 4;
+        return 1024 + kOffList + static_cast<size_t>(max_list) * 4 + 2 * static_cast<size_t>(bm_words) * 4;
     }
 };
 
@@ -137,8 +137,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     uint64_t* list_empty = list_full + 2;
     FragMeta* meta = reinterpret_cast<FragMeta*>(smem + L::kOffMeta);
     uint32_t* misc = reinterpret_cast<uint32_t*>(smem + L::kOffMisc);  // [0] tmem base, [1] merge flag
-    int32_t* lists = reinterpret_cast<int32_t*>(smem + L::kOffList);  // [2][max_list]
-    uint32_t* bm = reinterpret_cast<uint32_t*>(lists + 2 * p.max_list);  // [2][bm_words]
+    int32_t* lists = reinterpret_cast<int32_t*>(smem + L::kOffList);  // [max_list]
+    uint32_t* bm = reinterpret_cast<uint32_t*>(lists + p.max_list);  // [2][bm_words]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int cta = blockIdx.x;
@@ -193,8 +193,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         {
             int jg = 0, q_uses = 0;
             for (int f = 0; f < n_frag; ++f) {
-                const int lb = f & 1;
-                mbar_wait(list_full + lb, (f >> 1) & 1);
+                const int lb = 0;  // single list buffer: it is rebuilt only after the previous epilogue
+                mbar_wait(list_full + lb, f & 1);
                 const FragMeta fm = meta[lb];
                 const int32_t* list = lists + lb * p.max_list;
                 const int nf = fm.e1 - fm.e0;
@@ -283,8 +283,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                 __syncwarp();
             };
             for (int f = 0; f < n_frag; ++f) {
-                const int lb = f & 1;
-                mbar_wait(list_full + lb, (f >> 1) & 1);
+                const int lb = 0;  // single list buffer: it is rebuilt only after the previous epilogue
+                mbar_wait(list_full + lb, f & 1);
                 const int nf = meta[lb].e1 - meta[lb].e0;
                 __syncwarp();
                 if (lane == 0) mbar_arrive(list_empty + lb);
@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int my_first_tile = p.part_o ? static_cast<int>(my_begin / p.vlen) : cta;
 
         for (int f = 0; f < n_frag; ++f) {
-            const int lb = f & 1;
+            const int lb = 0;  // single list buffer: it is rebuilt only after the previous epilogue
             int32_t* list = lists + lb * p.max_list;
             // ---------------------------------------------------------- fragment schedule
             const int tile = p.part_o ? my_first_tile + f : cta + f * p.grid;
@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 nfr = cta_of(t0 + p.vlen - 1, p.vtotal, p.grid) - first_cta + 1;
             }
             // ---------------------------------------------------------- visible list of the tile
-            mbar_wait(list_empty + lb, ((f >> 1) & 1) ^ 1);
+            mbar_wait(list_empty + lb, (f & 1) ^ 1);
             for (int w = t; w < 2 * p.bm_words; w += 128) bm[w] = 0u;
             named_bar_sync(1, 128);
             if (p.k > 0 && p.n_local > 0) {
@@ -691,11 +691,8 @@ int launch_impl(const bf16* q, const bf16* kp, const bf16* vp, BsaParams p, cuda
     const size_t smem = L::bytes(p.max_list, p.bm_words);
     if (smem > 227 * 1024)
         return set_error(PBSA_EUNSUPPORTED, "bsa_fwd: visible list too long for shared memory");
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(bsa_fwd_kernel<D, NSK, NSV, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        configured = true;
-    }
+    if (int rc = ensure_smem(reinterpret_cast<const void*>(bsa_fwd_kernel<D, NSK, NSV, B>), smem, "bsa_fwd"))
+        return rc;
     const int slots = 2 * num_sms();
     if (p.part_o != nullptr) {
         // at most ~4 CTAs share a tile (the merge handles up to 8 fragments)

@@ -7,6 +7,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "internal.h"
@@ -22,6 +23,23 @@ const char* last_error() { return g_err.c_str(); }
 int set_error(int code, const std::string& msg) {
     g_err = msg;
     return code;
+}
+
+int ensure_smem(const void* kernel, size_t bytes, const char* what) {
+    if (bytes <= 48 * 1024) return PBSA_OK;
+    static std::mutex mu;
+    static std::unordered_map<const void*, size_t> done;
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& cur = done[kernel];
+    if (bytes <= cur) return PBSA_OK;
+    const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return set_error(PBSA_EUNSUPPORTED, std::string(what) + ": " + std::to_string(bytes) +
+                                                " bytes of shared memory refused (" + cudaGetErrorString(e) + ")");
+    }
+    cur = bytes;
+    return PBSA_OK;
 }
 
 int check_launch(const char* what) {
@@ -371,8 +389,8 @@ int pbsa_mem_write_chunk(pbsa_mem* m, const void* k_chunk, const void* v_chunk, 
     const bool prof = m->prof_on && m->prof_write < m->prof_max;
     if (prof) cudaEventRecord(m->ev_write[static_cast<size_t>(m->prof_write) * 2], s);
     const int rc = launch_write_chunk(static_cast<const bf16*>(k_chunk), static_cast<const bf16*>(v_chunk),
-                                      m->dev.stage, m->bpc, m->b, m->d, m->units, m->S, m->k_pool, m->v_pool,
-                                      m->krep, s);
+                                      nullptr, m->dev.stage, m->bpc, m->b, m->d, m->units, m->S, m->k_pool,
+                                      m->v_pool, m->krep, nullptr, s);
     if (prof) {
         cudaEventRecord(m->ev_write[static_cast<size_t>(m->prof_write) * 2 + 1], s);
         ++m->prof_write;
@@ -429,8 +447,12 @@ int pbsa_mem_commit(pbsa_mem* m, const float* s_t, void* stream) {
     return rc;
 }
 
-int pbsa_attend(pbsa_mem* m, const void* q, int k_top, float scale, int mode, void* o, float* lse,
-                void* stream) {
+}  // extern "C"
+
+namespace {
+
+int attend_impl(pbsa_mem* m, const void* q, int k_top, float scale, int mode, void* o, float* lse, void* stream,
+                bool q_compressed) {
     PBSA_REQUIRE(m != nullptr && q != nullptr && o != nullptr, "attend: null pointer");
     PBSA_REQUIRE(mode == PBSA_MODE_DENOISE || mode == PBSA_MODE_CACHE_UPDATE, "attend: unknown mode");
     PBSA_REQUIRE(k_top >= 0, "attend: k_top must be >= 0");
@@ -441,11 +463,13 @@ int pbsa_attend(pbsa_mem* m, const void* q, int k_top, float scale, int mode, vo
     const int n_p = m->counts.n_p, n_l = m->counts.n_l;
     const int k = n_l == 0 ? 0 : (k_top < n_l ? k_top : n_l);
     prof_mark(m, 0, s);
-    // (a) query-block representatives
-    if (int rc = launch_compress(static_cast<const bf16*>(q), static_cast<int64_t>(bpc) * b * d,
-                                 static_cast<int64_t>(b) * d, nullptr, bpc, U, b, d, m->qc,
-                                 static_cast<int64_t>(bpc) * d, s))
-        return rc;
+    // (a) query-block representatives (already produced by the fused ingest in pbsa_attend_qkv)
+    if (!q_compressed) {
+        if (int rc = launch_compress(static_cast<const bf16*>(q), static_cast<int64_t>(bpc) * b * d,
+                                     static_cast<int64_t>(b) * d, nullptr, bpc, U, b, d, m->qc,
+                                     static_cast<int64_t>(bpc) * d, s))
+            return rc;
+    }
     prof_mark(m, 1, s);
     // (b) coarse scoring + Top-K (+ s_t over P ++ L ++ current at the k=0 pass)
     const bool update = mode == PBSA_MODE_CACHE_UPDATE;
@@ -477,6 +501,34 @@ int pbsa_attend(pbsa_mem* m, const void* q, int k_top, float scale, int mode, vo
     prof_mark(m, 4, s);
     if (m->prof_on && m->prof_attend < m->prof_max) ++m->prof_attend;
     return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pbsa_attend(pbsa_mem* m, const void* q, int k_top, float scale, int mode, void* o, float* lse,
+                void* stream) {
+    return attend_impl(m, q, k_top, scale, mode, o, lse, stream, false);
+}
+
+int pbsa_attend_qkv(pbsa_mem* m, const void* q, const void* k_chunk, const void* v_chunk, int k_top,
+                    float scale, int mode, void* o, float* lse, void* stream) {
+    PBSA_REQUIRE(m != nullptr && q != nullptr && k_chunk != nullptr && v_chunk != nullptr,
+                 "attend_qkv: null pointer");
+    PBSA_REQUIRE(aligned16(q) && aligned16(k_chunk) && aligned16(v_chunk), "attend_qkv: tensors must be 16-byte aligned");
+    cudaStream_t s = as_stream(stream);
+    const bool prof = m->prof_on && m->prof_write < m->prof_max;
+    if (prof) cudaEventRecord(m->ev_write[static_cast<size_t>(m->prof_write) * 2], s);
+    if (int rc = launch_write_chunk(static_cast<const bf16*>(k_chunk), static_cast<const bf16*>(v_chunk),
+                                    static_cast<const bf16*>(q), m->dev.stage, m->bpc, m->b, m->d, m->units, m->S,
+                                    m->k_pool, m->v_pool, m->krep, m->qc, s))
+        return rc;
+    if (prof) {
+        cudaEventRecord(m->ev_write[static_cast<size_t>(m->prof_write) * 2 + 1], s);
+        ++m->prof_write;
+    }
+    return attend_impl(m, q, k_top, scale, mode, o, lse, stream, true);
 }
 
 int pbsa_mem_status(const pbsa_mem* m, int* flags, void* stream) {

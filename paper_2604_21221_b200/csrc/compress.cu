@@ -79,15 +79,17 @@ __global__ void __launch_bounds__(256) compress_kernel(const bf16* __restrict__ 
 }
 
 // Writes block i of the current chunk (rows [i*b, i*b+b) of kc / vc) into pool slot stage[u][i]
-// rows [0, b) and its K representative into krep[u][slot].  Pool rows >= b are never written
-// (zeroed at creation), which is what the attention kernel's padding logic relies on.
-template <int D>
+// rows [0, b) and its K representative into krep[u][slot]; with WITH_Q also compresses the same
+// block of Q into qrep[u][i] (the fused ingest of one PBSA call: one pass over Q, K and V).  Pool
+// rows >= b are never written (zeroed at creation), which the attention kernel relies on.
+template <int D, bool WITH_Q>
 __global__ void __launch_bounds__(256) write_chunk_kernel(const bf16* __restrict__ kc,
                                                           const bf16* __restrict__ vc,
+                                                          const bf16* __restrict__ qcur,
                                                           const int32_t* __restrict__ stage, int bpc,
                                                           int b, int units, int n_slots,
                                                           bf16* __restrict__ kp, bf16* __restrict__ vp,
-                                                          float* __restrict__ krep) {
+                                                          float* __restrict__ krep, float* __restrict__ qrep) {
     constexpr int C = D / 32;
     using V = typename Vec<C>::T;
     const int64_t w = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
@@ -99,18 +101,20 @@ __global__ void __launch_bounds__(256) write_chunk_kernel(const bf16* __restrict
     const int64_t dst_off = (static_cast<int64_t>(u) * n_slots + slot) * 64 * D;
     const V* ks = reinterpret_cast<const V*>(kc + src_off) + lane;
     const V* vs = reinterpret_cast<const V*>(vc + src_off) + lane;
+    const V* qs = WITH_Q ? reinterpret_cast<const V*>(qcur + src_off) + lane : nullptr;
     V* kd = reinterpret_cast<V*>(kp + dst_off) + lane;
     V* vd = reinterpret_cast<V*>(vp + dst_off) + lane;
-    double acc[C];
+    double acc[C], qacc[C];
 #pragma unroll
-    for (int c = 0; c < C; ++c) acc[c] = 0.0;
+    for (int c = 0; c < C; ++c) acc[c] = qacc[c] = 0.0;
     int t = 0;
     for (; t + 4 <= b; t += 4) {
-        V kv[4], vv[4];
+        V kv[4], vv[4], qv[4];
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
             kv[r] = __ldg(ks + (t + r) * (D / C));
             vv[r] = __ldg(vs + (t + r) * (D / C));
+            if (WITH_Q) qv[r] = __ldg(qs + (t + r) * (D / C));
         }
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
@@ -120,6 +124,11 @@ __global__ void __launch_bounds__(256) write_chunk_kernel(const bf16* __restrict
             unpack<C>(kv[r], f);
 #pragma unroll
             for (int c = 0; c < C; ++c) acc[c] += static_cast<double>(f[c]);
+            if (WITH_Q) {
+                unpack<C>(qv[r], f);
+#pragma unroll
+                for (int c = 0; c < C; ++c) qacc[c] += static_cast<double>(f[c]);
+            }
         }
     }
     for (; t < b; ++t) {
@@ -130,11 +139,21 @@ __global__ void __launch_bounds__(256) write_chunk_kernel(const bf16* __restrict
         unpack<C>(kv, f);
 #pragma unroll
         for (int c = 0; c < C; ++c) acc[c] += static_cast<double>(f[c]);
+        if (WITH_Q) {
+            unpack<C>(__ldg(qs + t * (D / C)), f);
+#pragma unroll
+            for (int c = 0; c < C; ++c) qacc[c] += static_cast<double>(f[c]);
+        }
     }
-    float* dst = krep + (static_cast<int64_t>(u) * n_slots + slot) * D + lane * C;
     const double db = static_cast<double>(b);
+    float* dst = krep + (static_cast<int64_t>(u) * n_slots + slot) * D + lane * C;
 #pragma unroll
     for (int c = 0; c < C; ++c) dst[c] = __double2float_rn(__ddiv_rn(acc[c], db));
+    if (WITH_Q) {
+        float* qd = qrep + (static_cast<int64_t>(u) * bpc + i) * D + lane * C;
+#pragma unroll
+        for (int c = 0; c < C; ++c) qd[c] = __double2float_rn(__ddiv_rn(qacc[c], db));
+    }
 }
 
 }  // namespace
@@ -151,15 +170,19 @@ int launch_compress(const bf16* x, int64_t xu, int64_t xb, const int32_t* map, i
     return check_launch("compress_kernel");
 }
 
-int launch_write_chunk(const bf16* kc, const bf16* vc, const int32_t* stage, int bpc, int b, int d,
-                       int units, int n_slots, bf16* kp, bf16* vp, float* krep, cudaStream_t s) {
+int launch_write_chunk(const bf16* kc, const bf16* vc, const bf16* q, const int32_t* stage, int bpc, int b,
+                       int d, int units, int n_slots, bf16* kp, bf16* vp, float* krep, float* qrep,
+                       cudaStream_t s) {
     const int64_t warps = static_cast<int64_t>(bpc) * units;
     if (warps == 0) return 0;
     const int grid = static_cast<int>((warps + 7) / 8);
-    if (d == 128)
-        write_chunk_kernel<128><<<grid, 256, 0, s>>>(kc, vc, stage, bpc, b, units, n_slots, kp, vp, krep);
-    else
-        write_chunk_kernel<64><<<grid, 256, 0, s>>>(kc, vc, stage, bpc, b, units, n_slots, kp, vp, krep);
+#define PBSA_WC(DD, WQ) write_chunk_kernel<DD, WQ><<<grid, 256, 0, s>>>(kc, vc, q, stage, bpc, b, units, n_slots, kp, vp, krep, qrep)
+    if (d == 128) {
+        if (q) PBSA_WC(128, true); else PBSA_WC(128, false);
+    } else {
+        if (q) PBSA_WC(64, true); else PBSA_WC(64, false);
+    }
+#undef PBSA_WC
     return check_launch("write_chunk_kernel");
 }
 

@@ -14,6 +14,8 @@ using bf16 = __nv_bfloat16;
 
 int set_error(int code, const std::string& msg);
 int check_launch(const char* what);
+// Raise a kernel's dynamic shared-memory limit to `bytes` (cached per kernel); error if refused.
+int ensure_smem(const void* kernel, size_t bytes, const char* what);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
@@ -21,8 +23,9 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 int launch_compress(const bf16* x, int64_t x_unit_stride, int64_t x_block_stride, const int32_t* map,
                     int n_blocks, int units, int b, int d, float* reps, int64_t reps_unit_stride,
                     cudaStream_t s);
-int launch_write_chunk(const bf16* kc, const bf16* vc, const int32_t* stage, int bpc, int b, int d,
-                       int units, int n_slots, bf16* k_pool, bf16* v_pool, float* krep,
+// q / qrep nullable: with q, the same pass also compresses the current chunk's query blocks
+int launch_write_chunk(const bf16* kc, const bf16* vc, const bf16* q, const int32_t* stage, int bpc, int b,
+                       int d, int units, int n_slots, bf16* k_pool, bf16* v_pool, float* krep, float* qrep,
                        cudaStream_t s);
 // K2
 size_t score_select_workspace(int units, int nqb, int n_keys);

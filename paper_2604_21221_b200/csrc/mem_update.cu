@@ -200,11 +200,7 @@ int launch_mem_commit(const MemDev& m, const float* s_t, int units, int C, int L
     const size_t smem = static_cast<size_t>(max_cand) * (8 + 4 + 4 + 4) + static_cast<size_t>(Lcap) * 12 +
                         static_cast<size_t>(bpc) * 4 + static_cast<size_t>(S) * 4 + static_cast<size_t>(C) * 16 + 64;
     if (smem > 227 * 1024) return set_error(PBSA_EUNSUPPORTED, "mem_commit: memory geometry too large for one CTA");
-    static size_t configured = 48 * 1024;
-    if (smem > configured) {
-        cudaFuncSetAttribute(mem_commit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        configured = 227 * 1024;
-    }
+    if (int rc = ensure_smem(reinterpret_cast<const void*>(mem_commit_kernel), smem, "mem_commit")) return rc;
     mem_commit_kernel<<<units, 256, smem, s>>>(p);
     return check_launch("mem_commit_kernel");
 }

@@ -10,58 +10,19 @@
 // selected indices and s_t are bit-exact with oracle/pbsa_oracle.cpp.  The only transcendental
 // is the fp64 exp; see DESIGN.md "bit-exactness" for the residual-risk argument.
 //
-// Three kernels:
-//   coarse_logits_kernel  thread per key block, R query blocks per CTA (amortises krep reads)
-//   select_kernel         warp per query-block row: softmax (fp64 exp, sequential ascending
-//                         denominator on lane 0 exactly like the oracle), 4-pass 8-bit radix
-//                         select on the fp32 probability bits, ballot compaction of the winners
-//   aggregate_kernel      thread per key block, ascending-row fp64 column sums (k=0 pass only)
+// Two kernels:
+//   score_select_kernel  CTA = unit x up to 8 query-block rows.  Phase 1: logits, thread per key
+//                        block (fp64 query reps in smem, each key element converted once).
+//                        Phase 2: warp per row: softmax (fp64 exp, sequential ascending denominator
+//                        on lane 0 exactly like the oracle), 4-pass 8-bit radix select on the fp32
+//                        probability bits, ballot compaction of the winners
+//   aggregate_kernel     thread per key block, ascending-row fp64 column sums (k=0 pass only)
 #include <cfloat>
 
 #include "internal.h"
 
 namespace pbsa {
 namespace {
-
-constexpr int kLogitRows = 8;
-
-template <int D, int R>
-__global__ void __launch_bounds__(128) coarse_logits_kernel(
-    const float* __restrict__ qc, const float* __restrict__ krep, int64_t kru,
-    const int32_t* __restrict__ keys, int key_stride, int n_keys, int nqb, float scale,
-    float* __restrict__ logits) {
-    __shared__ float qs[R][D];
-    const int u = blockIdx.y;
-    const int i0 = blockIdx.x * R;
-    const int nr = min(R, nqb - i0);
-    for (int e = threadIdx.x; e < R * D; e += blockDim.x) {
-        const int r = e / D, c = e % D;
-        qs[r][c] = r < nr ? qc[(static_cast<int64_t>(u) * nqb + i0 + r) * D + c] : 0.0f;
-    }
-    __syncthreads();
-    const int j = blockIdx.z * blockDim.x + threadIdx.x;
-    if (j >= n_keys) return;
-    const int slot = __ldg(keys + static_cast<int64_t>(u) * key_stride + j);
-    const float4* kr = reinterpret_cast<const float4*>(krep + u * kru + static_cast<int64_t>(slot) * D);
-    double acc[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) acc[r] = 0.0;
-#pragma unroll 4
-    for (int c4 = 0; c4 < D / 4; ++c4) {
-        const float4 kv = __ldg(kr + c4);
-#pragma unroll
-        for (int r = 0; r < R; ++r) {  // ascending c per row: x, y, z, w
-            acc[r] = __fma_rn(static_cast<double>(qs[r][4 * c4 + 0]), static_cast<double>(kv.x), acc[r]);
-            acc[r] = __fma_rn(static_cast<double>(qs[r][4 * c4 + 1]), static_cast<double>(kv.y), acc[r]);
-            acc[r] = __fma_rn(static_cast<double>(qs[r][4 * c4 + 2]), static_cast<double>(kv.z), acc[r]);
-            acc[r] = __fma_rn(static_cast<double>(qs[r][4 * c4 + 3]), static_cast<double>(kv.w), acc[r]);
-        }
-    }
-    // fp32 x fp32 products are exact in fp64, so fma == mul-then-add of the oracle.
-    for (int r = 0; r < nr; ++r)
-        logits[(static_cast<int64_t>(u) * nqb + i0 + r) * n_keys + j] =
-            __fmul_rn(__double2float_rn(acc[r]), scale);
-}
 
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
@@ -162,32 +123,75 @@ __device__ void warp_topk(const uint32_t* pb, int n, int k, uint32_t* hist, int3
     }
 }
 
-struct SelectParams {
-    const float* logits;  // [U][nqb][n_keys]
-    int n_keys, local_off, n_local, k, nqb, units, rows_per_cta;
-    size_t per_warp;      // bytes of smem per warp (16-aligned)
+struct ScoreParams {
+    const float* qc;      // [U][nqb][D]
+    const float* krep;    // [U][...][D] (slot-indexed)
+    int64_t kru;
+    const int32_t* keys;  // [U][key_stride]
+    int key_stride, n_keys, local_off, n_local, k, nqb, units, rows;
+    float scale;
+    size_t per_warp;      // bytes of smem per row (16-aligned)
     int32_t* sel;         // [U][nqb][k]
     float* arows;         // [U][nqb][n_keys] or null
     int* status;          // nullable: bit 0 set when a logit row holds NaN (invalid input)
 };
 
-__global__ void __launch_bounds__(256) select_kernel(const SelectParams p) {
+constexpr int kMaxRows = 8;
+
+// One CTA = one unit x up to 8 query-block rows.  Phase 1 (all 256 threads): coarse logits of the
+// rows against every key block, thread per key, ascending-k fp64 dot products -- the query reps are
+// converted to fp64 once into shared memory and each key element once, so the DFMA chains are not
+// starved by float->double conversions.  Phase 2 (warp per row): softmax, Top-K, optional A_t row.
+template <int D>
+__global__ void __launch_bounds__(256) score_select_kernel(const ScoreParams p) {
     extern __shared__ __align__(16) uint8_t smem[];
-    const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
-    const int64_t row = static_cast<int64_t>(blockIdx.x) * p.rows_per_cta + warp;
-    if (warp >= p.rows_per_cta || row >= static_cast<int64_t>(p.units) * p.nqb) return;
+    const int tid = threadIdx.x, warp = tid / 32, lane = tid & 31;
+    const int u = blockIdx.y, i0 = blockIdx.x * p.rows;
+    const int nr = min(p.rows, p.nqb - i0);
     const int n = p.n_keys;
-    uint8_t* base = smem + p.per_warp * warp;
+    double* qd = reinterpret_cast<double*>(smem);                 // [kMaxRows][D]
+    uint8_t* rows_base = smem + static_cast<size_t>(kMaxRows) * D * 8;
+    for (int e = tid; e < kMaxRows * D; e += blockDim.x) {
+        const int r = e / D, c = e % D;
+        qd[e] = r < nr ? static_cast<double>(p.qc[(static_cast<int64_t>(u) * p.nqb + i0 + r) * D + c]) : 0.0;
+    }
+    __syncthreads();
+    for (int j = tid; j < n; j += blockDim.x) {
+        const int slot = __ldg(p.keys + static_cast<int64_t>(u) * p.key_stride + j);
+        const float4* kr = reinterpret_cast<const float4*>(p.krep + u * p.kru + static_cast<int64_t>(slot) * D);
+        double acc[kMaxRows];
+#pragma unroll
+        for (int r = 0; r < kMaxRows; ++r) acc[r] = 0.0;
+#pragma unroll 2
+        for (int c4 = 0; c4 < D / 4; ++c4) {
+            const float4 kv = __ldg(kr + c4);
+            const double k0 = kv.x, k1 = kv.y, k2 = kv.z, k3 = kv.w;
+#pragma unroll
+            for (int r = 0; r < kMaxRows; ++r) {  // ascending c per row; fp32 x fp32 is exact in fp64
+                const double* q = qd + r * D + 4 * c4;
+                acc[r] = __fma_rn(q[0], k0, acc[r]);
+                acc[r] = __fma_rn(q[1], k1, acc[r]);
+                acc[r] = __fma_rn(q[2], k2, acc[r]);
+                acc[r] = __fma_rn(q[3], k3, acc[r]);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < kMaxRows; ++r)
+            if (r < nr) {
+                float* z = reinterpret_cast<float*>(rows_base + p.per_warp * r + static_cast<size_t>(n) * 8);
+                z[j] = __fmul_rn(__double2float_rn(acc[r]), p.scale);
+            }
+    }
+    __syncthreads();
+    if (warp >= nr) return;
+    const int64_t row = static_cast<int64_t>(u) * p.nqb + i0 + warp;
+    uint8_t* base = rows_base + p.per_warp * warp;
     double* e = reinterpret_cast<double*>(base);
     float* z = reinterpret_cast<float*>(base + static_cast<size_t>(n) * 8);
     uint32_t* pb = reinterpret_cast<uint32_t*>(base + static_cast<size_t>(n) * 12);
     uint32_t* hist = pb + p.n_local;
-    const float* src = p.logits + row * n;
     bool bad = false;
-    for (int j = lane; j < n; j += 32) {
-        z[j] = src[j];
-        bad |= src[j] != src[j];
-    }
+    for (int j = lane; j < n; j += 32) bad |= z[j] != z[j];
     if (p.status != nullptr && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(p.status, 1);
     __syncwarp();
     if (p.k > 0 && p.n_local > 0) {
@@ -211,8 +215,7 @@ __global__ void aggregate_kernel(const float* __restrict__ arows, int n_keys, in
 }  // namespace
 
 size_t score_select_workspace(int units, int nqb, int n_keys) {
-    const size_t one = static_cast<size_t>(units) * nqb * n_keys * sizeof(float);
-    return 2 * one + 256;
+    return static_cast<size_t>(units) * nqb * n_keys * sizeof(float) + 256;  // A_t rows (k=0 pass)
 }
 
 int launch_score_select(const float* qc, const float* krep, int64_t kru, const int32_t* keys,
@@ -224,38 +227,30 @@ int launch_score_select(const float* qc, const float* krep, int64_t kru, const i
     if (!do_select && s_t == nullptr) return 0;
     if (ws_bytes < score_select_workspace(units, nqb, n_keys))
         return set_error(PBSA_EINVAL, "score_select: workspace too small");
-    float* logits = static_cast<float*>(ws);
-    float* arows = s_t ? logits + static_cast<size_t>(units) * nqb * n_keys : nullptr;
-    {
-        dim3 grid((nqb + kLogitRows - 1) / kLogitRows, units, (n_keys + 127) / 128);
-        if (d == 128)
-            coarse_logits_kernel<128, kLogitRows><<<grid, 128, 0, s>>>(qc, krep, kru, keys, key_stride,
-                                                                       n_keys, nqb, scale, logits);
-        else
-            coarse_logits_kernel<64, kLogitRows><<<grid, 128, 0, s>>>(qc, krep, kru, keys, key_stride,
-                                                                      n_keys, nqb, scale, logits);
-        if (int rc = check_launch("coarse_logits_kernel")) return rc;
-    }
+    float* arows = s_t ? static_cast<float*>(ws) : nullptr;
     {
         const size_t per_warp =
             (static_cast<size_t>(n_keys) * 12 + static_cast<size_t>(n_local) * 4 + 1024 + 15) & ~size_t(15);
-        const size_t budget = 200 * 1024;
+        const size_t qbytes = static_cast<size_t>(kMaxRows) * d * 8;
+        const size_t budget = 200 * 1024 - qbytes;
         if (per_warp > budget)
             return set_error(PBSA_EUNSUPPORTED, "score_select: too many key blocks for one row in smem");
         int rows = static_cast<int>(budget / per_warp);
-        rows = rows < 1 ? 1 : (rows > 8 ? 8 : rows);
-        SelectParams p{logits, n_keys, local_off, n_local, do_select ? k : 0, nqb, units, rows, per_warp,
-                       sel, arows, status};
-        const size_t smem = per_warp * rows;
-        static size_t configured = 0;
-        if (smem > 48 * 1024 && smem > configured) {
-            cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-            configured = 227 * 1024;
+        rows = rows < 1 ? 1 : (rows > kMaxRows ? kMaxRows : rows);
+        ScoreParams p{qc, krep, kru, keys, key_stride, n_keys, local_off, n_local, do_select ? k : 0, nqb, units,
+                      rows, scale, per_warp, sel, arows, status};
+        const size_t smem = qbytes + per_warp * rows;
+        dim3 grid((nqb + rows - 1) / rows, units);
+        if (d == 128) {
+            if (int rc = ensure_smem(reinterpret_cast<const void*>(score_select_kernel<128>), smem, "score_select"))
+                return rc;
+            score_select_kernel<128><<<grid, 256, smem, s>>>(p);
+        } else {
+            if (int rc = ensure_smem(reinterpret_cast<const void*>(score_select_kernel<64>), smem, "score_select"))
+                return rc;
+            score_select_kernel<64><<<grid, 256, smem, s>>>(p);
         }
-        const int64_t total = static_cast<int64_t>(units) * nqb;
-        const int grid = static_cast<int>((total + rows - 1) / rows);
-        select_kernel<<<grid, rows * 32, smem, s>>>(p);
-        if (int rc = check_launch("select_kernel")) return rc;
+        if (int rc = check_launch("score_select_kernel")) return rc;
     }
     if (s_t) {
         dim3 grid((n_keys + 127) / 128, units);

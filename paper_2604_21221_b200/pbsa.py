@@ -258,6 +258,22 @@ class Memory:
                               int(mode), o.data_ptr(), _ptr(lse), _stream()))
         return (o, lse) if want_lse else o
 
+    def attend_qkv(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, k_top: int,
+                   mode: int = MODE_DENOISE, scale: float | None = None, out: torch.Tensor | None = None,
+                   want_lse: bool = False):
+        """write_chunk(k, v) + attend(q) fused: one ingest pass over Q, K and V (pbsa_attend_qkv)."""
+        shape = (self.units, self.blocks_per_chunk * self.b, self.d)
+        for name, t in (("q", q), ("k", k), ("v", v)):
+            _need(t, torch.bfloat16, name)
+            if t.shape != shape:
+                raise PbsaError(f"attend_qkv: {name} must be {shape}")
+        o = torch.empty_like(q) if out is None else out
+        lse = torch.empty(q.shape[:2], device=q.device, dtype=torch.float32) if want_lse else None
+        check(LIB.pbsa_attend_qkv(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), int(k_top),
+                                  0.0 if scale is None else float(scale), int(mode), o.data_ptr(),
+                                  _ptr(lse), _stream()))
+        return (o, lse) if want_lse else o
+
     def commit(self, s_t: torch.Tensor) -> None:
         _need(s_t, torch.float32, "s_t")
         check(LIB.pbsa_mem_commit(self._h, s_t.data_ptr(), _stream()))

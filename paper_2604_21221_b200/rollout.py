@@ -170,8 +170,7 @@ def run_inference(cfg: RolloutConfig, denoiser: ToyDenoiser | None = None, trace
                 q, k, v = den.qkv(layer, h, t)
                 n_l = mem.info().n_l
                 k_top = pbsa.topk_count(n_l, cfg.topk_ratio) if n_l else 0
-                mem.write_chunk(k, v)
-                o = mem.attend(q, k_top, pbsa.MODE_DENOISE)
+                o = mem.attend_qkv(q, k, v, k_top, pbsa.MODE_DENOISE)
                 h = den.project_out(layer, o, h)
                 calls += 1
             x0_hat = unblockify_tokens(h, dims, cfg.block_shape)
@@ -185,8 +184,7 @@ def run_inference(cfg: RolloutConfig, denoiser: ToyDenoiser | None = None, trace
                     q, k, v = den.qkv(layer, hb, 0.0)
                     n_l = mem.info().n_l
                     k_top = pbsa.topk_count(n_l, cfg.topk_ratio) if n_l else 0
-                    mem.write_chunk(k, v)
-                    o = mem.attend(q, k_top, pbsa.MODE_CACHE_UPDATE)
+                    o = mem.attend_qkv(q, k, v, k_top, pbsa.MODE_CACHE_UPDATE)
                     if layer == 0 and record_scores:
                         _, s_t = mem.last_selection()
                         rec["scores"] = [[float(v_) for v_ in s_t[u].tolist()] for u in range(cfg.trace_units)]

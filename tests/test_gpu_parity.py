@@ -175,8 +175,12 @@ def run_rollout(pb, units, d, b, bpc, C, W, n_chunks, k_top, seed, denoise_steps
             q = normal_bf16(base, (units, bpc * b, d))
             kc = normal_bf16(base + 7, (units, bpc * b, d))
             vc = normal_bf16(base + 13, (units, bpc * b, d))
-            mem.write_chunk(dev(kc), dev(vc))
-            o = mem.attend(dev(q), k_top, pb.MODE_CACHE_UPDATE if update else pb.MODE_DENOISE)
+            mode = pb.MODE_CACHE_UPDATE if update else pb.MODE_DENOISE
+            if (c + step) % 2:  # both entry points: fused ingest and write_chunk + attend
+                o = mem.attend_qkv(dev(q), dev(kc), dev(vc), k_top, mode)
+            else:
+                mem.write_chunk(dev(kc), dev(vc))
+                o = mem.attend(dev(q), k_top, mode)
             sel_gpu, st_gpu = mem.last_selection()
             o = o.float().cpu().numpy()
             sel_gpu = None if sel_gpu is None else sel_gpu.cpu().numpy()
