@@ -42,7 +42,22 @@ __device__ void warp_softmax(const float* z, int n, double* e, uint32_t* out_bit
     __syncwarp();
     double denom = 0.0;
     if (lane == 0) {  // ascending-j fp64 accumulation, exactly as tensor.cpp:96-102
-        for (int j = 0; j < n; ++j) denom = __dadd_rn(denom, e[j]);
+        int j = 0;
+        for (; j + 8 <= n; j += 8) {  // 16-byte loads issued ahead of the dependent adds
+            const double2 a0 = *reinterpret_cast<const double2*>(e + j);
+            const double2 a1 = *reinterpret_cast<const double2*>(e + j + 2);
+            const double2 a2 = *reinterpret_cast<const double2*>(e + j + 4);
+            const double2 a3 = *reinterpret_cast<const double2*>(e + j + 6);
+            denom = __dadd_rn(denom, a0.x);
+            denom = __dadd_rn(denom, a0.y);
+            denom = __dadd_rn(denom, a1.x);
+            denom = __dadd_rn(denom, a1.y);
+            denom = __dadd_rn(denom, a2.x);
+            denom = __dadd_rn(denom, a2.y);
+            denom = __dadd_rn(denom, a3.x);
+            denom = __dadd_rn(denom, a3.y);
+        }
+        for (; j < n; ++j) denom = __dadd_rn(denom, e[j]);
     }
     denom = __shfl_sync(0xffffffffu, denom, 0);
     for (int j = lane; j < n; j += 32) {
@@ -65,9 +80,13 @@ __device__ void warp_topk(const uint32_t* pb, int n, int k, uint32_t* hist, int3
 #pragma unroll
         for (int t = 0; t < 8; ++t) hist[lane * 8 + t] = 0;
         __syncwarp();
-        for (int j = lane; j < n; j += 32) {
-            const uint32_t v = pb[j];
-            if ((v & pmask) == prefix) atomicAdd(&hist[(v >> shift) & 255u], 1u);
+        for (int base = 0; base < n; base += 32) {  // warp-aggregated: one atomic per distinct bin
+            const int j = base + lane;
+            const uint32_t v = j < n ? pb[j] : 0u;
+            const bool in = j < n && (v & pmask) == prefix;
+            const uint32_t bin = in ? ((v >> shift) & 255u) : 256u;
+            const uint32_t peers = __match_any_sync(0xffffffffu, bin);
+            if (in && lane == __ffs(peers) - 1) atomicAdd(&hist[bin], static_cast<uint32_t>(__popc(peers)));
         }
         __syncwarp();
         // lane l owns digits [255-8l-7, 255-8l] (lane 0 the largest)
@@ -201,6 +220,69 @@ __global__ void __launch_bounds__(256) score_select_kernel(const ScoreParams p) 
     if (p.arows != nullptr) warp_softmax(z, n, e, nullptr, p.arows + row * n);
 }
 
+// Long key lists (a row's scratch does not fit 8 rows per CTA): logits for 8 rows per CTA into a
+// global scratch (so each key representative is read once per 8 rows), then one warp per row.
+template <int D>
+__global__ void __launch_bounds__(256) logits_kernel(const ScoreParams p, float* __restrict__ logits) {
+    __shared__ double qd[kMaxRows * D];
+    const int u = blockIdx.y, i0 = blockIdx.x * kMaxRows;
+    const int nr = min(kMaxRows, p.nqb - i0);
+    for (int e = threadIdx.x; e < kMaxRows * D; e += blockDim.x) {
+        const int r = e / D, c = e % D;
+        qd[e] = r < nr ? static_cast<double>(p.qc[(static_cast<int64_t>(u) * p.nqb + i0 + r) * D + c]) : 0.0;
+    }
+    __syncthreads();
+    const int j = blockIdx.z * blockDim.x + threadIdx.x;
+    if (j >= p.n_keys) return;
+    const int slot = __ldg(p.keys + static_cast<int64_t>(u) * p.key_stride + j);
+    const float4* kr = reinterpret_cast<const float4*>(p.krep + u * p.kru + static_cast<int64_t>(slot) * D);
+    double acc[kMaxRows];
+#pragma unroll
+    for (int r = 0; r < kMaxRows; ++r) acc[r] = 0.0;
+#pragma unroll 2
+    for (int c4 = 0; c4 < D / 4; ++c4) {
+        const float4 kv = __ldg(kr + c4);
+        const double k0 = kv.x, k1 = kv.y, k2 = kv.z, k3 = kv.w;
+#pragma unroll
+        for (int r = 0; r < kMaxRows; ++r) {
+            const double* q = qd + r * D + 4 * c4;
+            acc[r] = __fma_rn(q[0], k0, acc[r]);
+            acc[r] = __fma_rn(q[1], k1, acc[r]);
+            acc[r] = __fma_rn(q[2], k2, acc[r]);
+            acc[r] = __fma_rn(q[3], k3, acc[r]);
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < kMaxRows; ++r)
+        if (r < nr)
+            logits[(static_cast<int64_t>(u) * p.nqb + i0 + r) * p.n_keys + j] = __fmul_rn(__double2float_rn(acc[r]), p.scale);
+}
+
+__global__ void __launch_bounds__(256) select_rows_kernel(const ScoreParams p, const float* __restrict__ logits) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
+    const int64_t row = static_cast<int64_t>(blockIdx.x) * p.rows + warp;
+    if (warp >= p.rows || row >= static_cast<int64_t>(p.units) * p.nqb) return;
+    const int n = p.n_keys;
+    uint8_t* base = smem + p.per_warp * warp;
+    double* e = reinterpret_cast<double*>(base);
+    float* z = reinterpret_cast<float*>(base + static_cast<size_t>(n) * 8);
+    uint32_t* pb = reinterpret_cast<uint32_t*>(base + static_cast<size_t>(n) * 12);
+    uint32_t* hist = pb + p.n_local;
+    bool bad = false;
+    for (int j = lane; j < n; j += 32) {
+        z[j] = logits[row * n + j];
+        bad |= z[j] != z[j];
+    }
+    if (p.status != nullptr && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(p.status, 1);
+    __syncwarp();
+    if (p.k > 0 && p.n_local > 0) {
+        warp_softmax(z + p.local_off, p.n_local, e, pb, nullptr);
+        warp_topk(pb, p.n_local, p.k, hist, p.sel + row * p.k);
+    }
+    if (p.arows != nullptr) warp_softmax(z, n, e, nullptr, p.arows + row * n);
+}
+
 __global__ void aggregate_kernel(const float* __restrict__ arows, int n_keys, int nqb, int units,
                                  float* __restrict__ s_t) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -215,7 +297,8 @@ __global__ void aggregate_kernel(const float* __restrict__ arows, int n_keys, in
 }  // namespace
 
 size_t score_select_workspace(int units, int nqb, int n_keys) {
-    return static_cast<size_t>(units) * nqb * n_keys * sizeof(float) + 256;  // A_t rows (k=0 pass)
+    // A_t rows (k=0 pass) + logits scratch of the long-window path
+    return 2 * static_cast<size_t>(units) * nqb * n_keys * sizeof(float) + 256;
 }
 
 int launch_score_select(const float* qc, const float* krep, int64_t kru, const int32_t* keys,
@@ -233,12 +316,26 @@ int launch_score_select(const float* qc, const float* krep, int64_t kru, const i
             (static_cast<size_t>(n_keys) * 12 + static_cast<size_t>(n_local) * 4 + 1024 + 15) & ~size_t(15);
         const size_t qbytes = static_cast<size_t>(kMaxRows) * d * 8;
         const size_t budget = 200 * 1024 - qbytes;
-        if (per_warp > budget)
+        if (per_warp > 200 * 1024)
             return set_error(PBSA_EUNSUPPORTED, "score_select: too many key blocks for one row in smem");
         int rows = static_cast<int>(budget / per_warp);
         rows = rows < 1 ? 1 : (rows > kMaxRows ? kMaxRows : rows);
         ScoreParams p{qc, krep, kru, keys, key_stride, n_keys, local_off, n_local, do_select ? k : 0, nqb, units,
                       rows, scale, per_warp, sel, arows, status};
+        if (rows < kMaxRows) {
+            // long key lists: logits of 8 rows per CTA into scratch, then warp-per-row selection
+            float* logits = static_cast<float*>(ws) + static_cast<size_t>(units) * nqb * n_keys;
+            dim3 g1((nqb + kMaxRows - 1) / kMaxRows, units, (n_keys + 255) / 256);
+            if (d == 128) logits_kernel<128><<<g1, 256, 0, s>>>(p, logits);
+            else logits_kernel<64><<<g1, 256, 0, s>>>(p, logits);
+            if (int rc = check_launch("logits_kernel")) return rc;
+            const size_t smem2 = per_warp * rows;
+            if (int rc = ensure_smem(reinterpret_cast<const void*>(select_rows_kernel), smem2, "score_select"))
+                return rc;
+            const int64_t total = static_cast<int64_t>(units) * nqb;
+            select_rows_kernel<<<static_cast<int>((total + rows - 1) / rows), rows * 32, smem2, s>>>(p, logits);
+            if (int rc = check_launch("select_rows_kernel")) return rc;
+        } else {
         const size_t smem = qbytes + per_warp * rows;
         dim3 grid((nqb + rows - 1) / rows, units);
         if (d == 128) {
@@ -251,6 +348,7 @@ int launch_score_select(const float* qc, const float* krep, int64_t kru, const i
             score_select_kernel<64><<<grid, 256, smem, s>>>(p);
         }
         if (int rc = check_launch("score_select_kernel")) return rc;
+        }
     }
     if (s_t) {
         dim3 grid((n_keys + 127) / 128, units);
