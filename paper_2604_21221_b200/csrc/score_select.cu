@@ -220,11 +220,21 @@ __global__ void __launch_bounds__(256) score_select_kernel(const ScoreParams p) 
     if (p.arows != nullptr) warp_softmax(z, n, e, nullptr, p.arows + row * n);
 }
 
-// Long key lists (a row's scratch does not fit 8 rows per CTA): logits for 8 rows per CTA into a
-// global scratch (so each key representative is read once per 8 rows), then one warp per row.
+// ---------------------------------------------------------------------------------------------
+// Long key lists (a row's scratch does not fit 8 rows per CTA; config 5: 6006-block windows).
+// Three kernels, each at high occupancy instead of one latency-bound warp per row:
+//   logits_t_kernel  8 query rows x 4 keys per thread (4x fewer shared-memory q reads per DFMA than
+//                    one key per thread), logits stored key-major: zt[j][R], R = u*nqb + i, so that
+//   row_denom_kernel thread per row R: fp32 max and the ascending-j fp64 denominator (the only
+//                    sequential part), with the next 8 logits loaded ahead of the add chain
+//   row_prob_kernel  fully parallel fp32 probabilities, row-major through a 32x32 smem transpose
+//   topk_rows_kernel warp per row: radix select over the row's probability bits.
+// The operation sequence per row is the same as warp_softmax / warp_topk above (and the oracle).
+constexpr int kKeysPerThread = 4;
+
 template <int D>
-__global__ void __launch_bounds__(256) logits_kernel(const ScoreParams p, float* __restrict__ logits) {
-    __shared__ double qd[kMaxRows * D];
+__global__ void __launch_bounds__(256, 2) logits_t_kernel(const ScoreParams p, float* __restrict__ zt) {
+    __shared__ __align__(16) double qd[kMaxRows * D];
     const int u = blockIdx.y, i0 = blockIdx.x * kMaxRows;
     const int nr = min(kMaxRows, p.nqb - i0);
     for (int e = threadIdx.x; e < kMaxRows * D; e += blockDim.x) {
@@ -232,55 +242,162 @@ __global__ void __launch_bounds__(256) logits_kernel(const ScoreParams p, float*
         qd[e] = r < nr ? static_cast<double>(p.qc[(static_cast<int64_t>(u) * p.nqb + i0 + r) * D + c]) : 0.0;
     }
     __syncthreads();
-    const int j = blockIdx.z * blockDim.x + threadIdx.x;
-    if (j >= p.n_keys) return;
-    const int slot = __ldg(p.keys + static_cast<int64_t>(u) * p.key_stride + j);
-    const float4* kr = reinterpret_cast<const float4*>(p.krep + u * p.kru + static_cast<int64_t>(slot) * D);
-    double acc[kMaxRows];
+    const int jb = blockIdx.z * blockDim.x * kKeysPerThread + threadIdx.x;
+    const float4* kr[kKeysPerThread];
 #pragma unroll
-    for (int r = 0; r < kMaxRows; ++r) acc[r] = 0.0;
-#pragma unroll 2
+    for (int q = 0; q < kKeysPerThread; ++q) {
+        const int j = jb + q * blockDim.x;
+        const int slot = j < p.n_keys ? __ldg(p.keys + static_cast<int64_t>(u) * p.key_stride + j) : 0;
+        kr[q] = reinterpret_cast<const float4*>(p.krep + u * p.kru + static_cast<int64_t>(slot) * D);
+    }
+    double acc[kKeysPerThread][kMaxRows];
+#pragma unroll
+    for (int q = 0; q < kKeysPerThread; ++q)
+#pragma unroll
+        for (int r = 0; r < kMaxRows; ++r) acc[q][r] = 0.0;
+    float4 kn[kKeysPerThread];  // next column quad, loaded one iteration ahead
+#pragma unroll
+    for (int q = 0; q < kKeysPerThread; ++q) kn[q] = __ldg(kr[q]);
+#pragma unroll 1
     for (int c4 = 0; c4 < D / 4; ++c4) {
-        const float4 kv = __ldg(kr + c4);
-        const double k0 = kv.x, k1 = kv.y, k2 = kv.z, k3 = kv.w;
+        double kd[kKeysPerThread][4];
+#pragma unroll
+        for (int q = 0; q < kKeysPerThread; ++q) {
+            const float4 kv = kn[q];
+            if (c4 + 1 < D / 4) kn[q] = __ldg(kr[q] + c4 + 1);
+            kd[q][0] = kv.x;
+            kd[q][1] = kv.y;
+            kd[q][2] = kv.z;
+            kd[q][3] = kv.w;
+        }
 #pragma unroll
         for (int r = 0; r < kMaxRows; ++r) {
-            const double* q = qd + r * D + 4 * c4;
-            acc[r] = __fma_rn(q[0], k0, acc[r]);
-            acc[r] = __fma_rn(q[1], k1, acc[r]);
-            acc[r] = __fma_rn(q[2], k2, acc[r]);
-            acc[r] = __fma_rn(q[3], k3, acc[r]);
+            const double2 qa = *reinterpret_cast<const double2*>(qd + r * D + 4 * c4);
+            const double2 qb = *reinterpret_cast<const double2*>(qd + r * D + 4 * c4 + 2);
+#pragma unroll
+            for (int q = 0; q < kKeysPerThread; ++q) {  // ascending c per (row, key)
+                acc[q][r] = __fma_rn(qa.x, kd[q][0], acc[q][r]);
+                acc[q][r] = __fma_rn(qa.y, kd[q][1], acc[q][r]);
+                acc[q][r] = __fma_rn(qb.x, kd[q][2], acc[q][r]);
+                acc[q][r] = __fma_rn(qb.y, kd[q][3], acc[q][r]);
+            }
         }
     }
+    const int64_t rt = static_cast<int64_t>(p.units) * p.nqb;
+    const int64_t r0 = static_cast<int64_t>(u) * p.nqb + i0;
 #pragma unroll
-    for (int r = 0; r < kMaxRows; ++r)
-        if (r < nr)
-            logits[(static_cast<int64_t>(u) * p.nqb + i0 + r) * p.n_keys + j] = __fmul_rn(__double2float_rn(acc[r]), p.scale);
+    for (int q = 0; q < kKeysPerThread; ++q) {
+        const int j = jb + q * blockDim.x;
+        if (j >= p.n_keys) continue;
+#pragma unroll
+        for (int r = 0; r < kMaxRows; ++r)
+            if (r < nr) zt[j * rt + r0 + r] = __fmul_rn(__double2float_rn(acc[q][r]), p.scale);
+    }
 }
 
-__global__ void __launch_bounds__(256) select_rows_kernel(const ScoreParams p, const float* __restrict__ logits) {
-    extern __shared__ __align__(16) uint8_t smem[];
-    const int warp = threadIdx.x / 32, lane = threadIdx.x & 31;
-    const int64_t row = static_cast<int64_t>(blockIdx.x) * p.rows + warp;
-    if (warp >= p.rows || row >= static_cast<int64_t>(p.units) * p.nqb) return;
-    const int n = p.n_keys;
-    uint8_t* base = smem + p.per_warp * warp;
-    double* e = reinterpret_cast<double*>(base);
-    float* z = reinterpret_cast<float*>(base + static_cast<size_t>(n) * 8);
-    uint32_t* pb = reinterpret_cast<uint32_t*>(base + static_cast<size_t>(n) * 12);
-    uint32_t* hist = pb + p.n_local;
+// Thread per row R over keys [off, off + n) of zt: fp32 row max and the ascending-j fp64 softmax
+// denominator (tensor.cpp:87-102); the exponentials of the next 8 keys are loaded ahead of the
+// dependent add chain.  NaN logits set status bit 0 (the oracle rejects them).
+__global__ void __launch_bounds__(128) row_denom_kernel(const float* __restrict__ zt, int64_t rt, int off, int n,
+                                                        float* __restrict__ mrow, double* __restrict__ drow,
+                                                        int* status) {
+    const int lane = threadIdx.x & 31;
+    const int64_t R = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool live = R < rt;
+    const float* z = zt + static_cast<int64_t>(off) * rt + (live ? R : 0);
+    float m = -FLT_MAX;
     bool bad = false;
-    for (int j = lane; j < n; j += 32) {
-        z[j] = logits[row * n + j];
-        bad |= z[j] != z[j];
+    if (live) {
+        float mq[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) mq[q] = -FLT_MAX;
+        int j = 0;
+        for (; j + 8 <= n; j += 8) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const float a = __ldg(z + (j + q) * rt);
+                bad |= a != a;
+                mq[q] = fmaxf(mq[q], a);
+            }
+        }
+        for (; j < n; ++j) {
+            const float a = __ldg(z + j * rt);
+            bad |= a != a;
+            m = fmaxf(m, a);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) m = fmaxf(m, mq[q]);  // max is exact: order-free
     }
-    if (p.status != nullptr && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(p.status, 1);
-    __syncwarp();
-    if (p.k > 0 && p.n_local > 0) {
-        warp_softmax(z + p.local_off, p.n_local, e, pb, nullptr);
-        warp_topk(pb, p.n_local, p.k, hist, p.sel + row * p.k);
+    if (status != nullptr && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, 1);
+    if (!live) return;
+    const double dm = static_cast<double>(m);
+    double denom = 0.0;
+    int j = 0;
+    if (n >= 8) {
+        float zn[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) zn[q] = __ldg(z + q * rt);
+        for (; j + 8 <= n; j += 8) {
+            float zc[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) zc[q] = zn[q];
+            if (j + 16 <= n) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) zn[q] = __ldg(z + (j + 8 + q) * rt);
+            }
+            double e[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) e[q] = exp(static_cast<double>(zc[q]) - dm);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) denom = __dadd_rn(denom, e[q]);  // ascending j
+        }
     }
-    if (p.arows != nullptr) warp_softmax(z, n, e, nullptr, p.arows + row * n);
+    for (; j < n; ++j) denom = __dadd_rn(denom, exp(static_cast<double>(__ldg(z + j * rt)) - dm));
+    mrow[R] = m;
+    drow[R] = denom;
+}
+
+// p[R][j] = float(exp(double(z[j][R]) - double(m_R)) / denom_R), fully parallel: a CTA converts a
+// 32-key x 32-row tile of the key-major logits into row-major probabilities through shared memory.
+__global__ void __launch_bounds__(256) row_prob_kernel(const float* __restrict__ zt, int64_t rt, int off, int n,
+                                                       const float* __restrict__ mrow,
+                                                       const double* __restrict__ drow, float* __restrict__ out) {
+    __shared__ float tile[32][33];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int j0 = blockIdx.x * 32;
+    const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 32;
+    const int64_t R = r0 + lane;
+    if (R < rt) {
+        const double dm = static_cast<double>(mrow[R]);
+        const double den = drow[R];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int jl = warp * 4 + q;
+            if (j0 + jl < n) {
+                const double e = exp(static_cast<double>(__ldg(zt + static_cast<int64_t>(off + j0 + jl) * rt + R)) - dm);
+                tile[lane][jl] = __double2float_rn(__ddiv_rn(e, den));
+            }
+        }
+    }
+    __syncthreads();
+    if (j0 + lane < n) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int rl = warp * 4 + q;
+            if (r0 + rl < rt) out[(r0 + rl) * n + j0 + lane] = tile[rl][lane];
+        }
+    }
+}
+
+// Warp per row: radix select straight from the row-major probabilities (L2-resident while the warp
+// works on them; staging rows in shared memory measured slower -- it caps residency at 8 warps/SM).
+__global__ void __launch_bounds__(256) topk_rows_kernel(const float* __restrict__ prob, int n, int k, int64_t rows,
+                                                        int32_t* __restrict__ sel) {
+    __shared__ uint32_t hist[8][256];
+    const int warp = threadIdx.x >> 5;
+    const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + warp;
+    if (row >= rows) return;
+    warp_topk(reinterpret_cast<const uint32_t*>(prob) + row * n, n, k, hist[warp], sel + row * k);
 }
 
 __global__ void aggregate_kernel(const float* __restrict__ arows, int n_keys, int nqb, int units,
@@ -297,8 +414,9 @@ __global__ void aggregate_kernel(const float* __restrict__ arows, int n_keys, in
 }  // namespace
 
 size_t score_select_workspace(int units, int nqb, int n_keys) {
-    // A_t rows (k=0 pass) + logits scratch of the long-window path
-    return 2 * static_cast<size_t>(units) * nqb * n_keys * sizeof(float) + 256;
+    // A_t rows (k=0 pass) + key-major logits and local-window probabilities of the long-window path
+    // + per-row max / denominator
+    return 3 * static_cast<size_t>(units) * nqb * n_keys * sizeof(float) + static_cast<size_t>(units) * nqb * 16 + 512;
 }
 
 int launch_score_select(const float* qc, const float* krep, int64_t kru, const int32_t* keys,
@@ -323,18 +441,32 @@ int launch_score_select(const float* qc, const float* krep, int64_t kru, const i
         ScoreParams p{qc, krep, kru, keys, key_stride, n_keys, local_off, n_local, do_select ? k : 0, nqb, units,
                       rows, scale, per_warp, sel, arows, status};
         if (rows < kMaxRows) {
-            // long key lists: logits of 8 rows per CTA into scratch, then warp-per-row selection
-            float* logits = static_cast<float*>(ws) + static_cast<size_t>(units) * nqb * n_keys;
-            dim3 g1((nqb + kMaxRows - 1) / kMaxRows, units, (n_keys + 255) / 256);
-            if (d == 128) logits_kernel<128><<<g1, 256, 0, s>>>(p, logits);
-            else logits_kernel<64><<<g1, 256, 0, s>>>(p, logits);
-            if (int rc = check_launch("logits_kernel")) return rc;
-            const size_t smem2 = per_warp * rows;
-            if (int rc = ensure_smem(reinterpret_cast<const void*>(select_rows_kernel), smem2, "score_select"))
-                return rc;
-            const int64_t total = static_cast<int64_t>(units) * nqb;
-            select_rows_kernel<<<static_cast<int>((total + rows - 1) / rows), rows * 32, smem2, s>>>(p, logits);
-            if (int rc = check_launch("select_rows_kernel")) return rc;
+            // long key lists: key-major logits -> thread-per-row softmax statistics -> warp-per-row select
+            const int64_t rt = static_cast<int64_t>(units) * nqb;
+            float* zt = static_cast<float*>(ws) + static_cast<size_t>(rt) * n_keys;
+            float* prob = zt + static_cast<size_t>(rt) * n_keys;
+            dim3 g1((nqb + kMaxRows - 1) / kMaxRows, units, (n_keys + 256 * kKeysPerThread - 1) / (256 * kKeysPerThread));
+            if (d == 128) logits_t_kernel<128><<<g1, 256, 0, s>>>(p, zt);
+            else logits_t_kernel<64><<<g1, 256, 0, s>>>(p, zt);
+            if (int rc = check_launch("logits_t_kernel")) return rc;
+            float* mrow = prob + static_cast<size_t>(rt) * n_keys;
+            double* drow = reinterpret_cast<double*>(mrow + ((rt + 1) & ~int64_t(1)));
+            const int gr = static_cast<int>((rt + 127) / 128);
+            auto softmax_rows = [&](int off, int n, float* out, int* st) -> int {
+                row_denom_kernel<<<gr, 128, 0, s>>>(zt, rt, off, n, mrow, drow, st);
+                if (int rc = check_launch("row_denom_kernel")) return rc;
+                dim3 g2((n + 31) / 32, static_cast<unsigned>((rt + 31) / 32));
+                row_prob_kernel<<<g2, 256, 0, s>>>(zt, rt, off, n, mrow, drow, out);
+                return check_launch("row_prob_kernel");
+            };
+            if (do_select) {
+                if (int rc = softmax_rows(local_off, n_local, prob, status)) return rc;
+                topk_rows_kernel<<<static_cast<int>((rt + 7) / 8), 256, 0, s>>>(prob, n_local, k, rt, sel);
+                if (int rc = check_launch("topk_rows_kernel")) return rc;
+            }
+            if (arows != nullptr) {
+                if (int rc = softmax_rows(0, n_keys, arows, do_select ? nullptr : status)) return rc;
+            }
         } else {
         const size_t smem = qbytes + per_warp * rows;
         dim3 grid((nqb + rows - 1) / rows, units);

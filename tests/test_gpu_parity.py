@@ -106,6 +106,13 @@ def test_score_select_large_window(pb):
     _score_case(pb, 1, 4, 156, 6006, 78, 128, 1502, seed=12)
 
 
+def test_score_select_long_path_rows_across_units(pb):
+    """Long-window kernels (key-major logits, thread-per-row statistics): 39 rows of 3 units share
+    warps; tied probabilities from duplicated representatives."""
+    _score_case(pb, 3, 13, 40, 2100, 20, 64, 300, seed=13)
+    _score_case(pb, 2, 5, 10, 2500, 10, 128, 77, seed=14, ties=True)
+
+
 # ------------------------------------------------------------------ (c) block-sparse attention
 def _bsa_case(pb, units, nqb, b, d, n_dense, n_local, k, seed, scale_q=1.0, stream_k=True):
     g = np.random.default_rng(seed)
