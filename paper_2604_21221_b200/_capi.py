@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libpbsa_b200.so")
+# PBSA_LIB_PATH: perf experiments only (e.g. the -DPBSA_K3_TRACE build of `make trace-lib`)
+LIB_PATH = os.environ.get("PBSA_LIB_PATH") or os.path.join(HERE, "_lib", "libpbsa_b200.so")
 
 PBSA_OK, PBSA_EINVAL, PBSA_ECUDA, PBSA_EUNSUPPORTED = 0, 1, 2, 3
 MODE_DENOISE, MODE_CACHE_UPDATE = 0, 1

@@ -10,14 +10,16 @@
 // blocks -- dense blocks first, then the union of the two Top-K selections (built from two
 // bitmaps) -- with a 2-bit mask per entry saying which half sees it.
 //
-// Schedule (persistent, stream-K): the grid is 2 CTAs per SM.  The global iteration space
-// (tile x virtual visible-block index, every tile counted with the same upper-bound length V) is
-// cut into equal contiguous ranges, one per CTA, so a CTA processes whole tiles and at most two
-// tile FRAGMENTS (its first and last).  A fragment writes fp32 partials (unnormalised O, running
-// max m, sum l) to a workspace; the last CTA to finish a split tile (per-tile arrival counter)
-// merges all fragments of that tile in fragment order (deterministic) and writes O.  Without a
-// workspace every CTA takes whole tiles round-robin.  This removes the 1.58-wave quantisation of
-// one-tile-per-CTA launches at the Wan-1.3B shape (468 tiles on 296 CTA slots).
+// Schedule (persistent, 2 CTAs per SM).  Without a workspace every CTA takes whole tiles
+// round-robin (tile = cta + f * grid).  With one (hybrid stream-K): full waves of whole tiles
+// first -- concurrently active tiles then belong to few heads, whose KV blocks stay L2-resident
+// -- and only the tail tiles (n_tiles mod grid) are split: their iteration space (tile x virtual
+// visible-block index, every tile counted with the upper-bound length V) is cut into equal
+// contiguous ranges, one per tail CTA, so a CTA processes at most two tile FRAGMENTS of the
+// tail.  A fragment writes fp32 partials (unnormalised O, running max m, sum l) to a workspace;
+// the last CTA to finish a split tile (per-tile arrival counter) merges all fragments of that
+// tile in fragment order (deterministic) and writes O.  This removes the 1.58-wave quantisation
+// of one-tile-per-CTA launches at the Wan-1.3B shape (468 tiles on 296 CTA slots).
 //
 // Warp roles (192 threads):
 //   warp 0  TMA producer: Q (3-D map over [unit*nqb][b][d], one box per query block and d-half),
@@ -42,6 +44,9 @@ namespace {
 constexpr int kThreads = 192;
 constexpr uint32_t kTmemCols = 256;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
+// column pairs whose exp2 runs as a polynomial on the FMA pipe instead of MUFU (bit c2 = pair c2)
+constexpr uint32_t kPolyMask = 0x11111111u;
+constexpr int kPolyDefault = 3;
 
 struct BsaParams {
     int units, nqb, b, n_slots;
@@ -57,9 +62,11 @@ struct BsaParams {
     int max_list, bm_words;
     long long* trace;  // perf experiments only: per-event clock64 stamps of CTA 0 (null = off)
     int ablate;  // perf experiments only (PBSA_ABLATE): 1 no softmax math, 2 no K/V loads, 3 no MMAs
-    // schedule
+    // schedule: `whole_waves` rounds of one whole tile per CTA (tile = cta + w * grid), then the
+    // remaining tiles [tail_base, n_tiles) split stream-K over the first tail_grid CTAs
     int tiles_per_unit, n_tiles, grid;
-    int64_t vlen, vtotal;  // virtual length of one tile (upper bound of its list) and of all tiles
+    int whole_waves, tail_base, tail_grid;
+    int64_t vlen, vtotal;  // virtual length of one tile (upper bound of its list) and of the tail
     float* part_o;         // [2*grid][128][D] fp32 (null -> whole tiles only)
     float* part_ml;        // [2*grid][2][128]
     int* counters;         // [n_tiles], zero between launches
@@ -94,8 +101,13 @@ struct Layout {
     }
 };
 
+// handshake timeline (tools/k3_timeline.py): compiled in only with -DPBSA_K3_TRACE
 __device__ __forceinline__ void stamp(const BsaParams& p, int ev, int j) {
+#ifdef PBSA_K3_TRACE
     if (p.trace != nullptr && blockIdx.x == 0 && j < 256) p.trace[ev * 256 + j] = clock64();
+#else
+    (void)p; (void)ev; (void)j;
+#endif
 }
 
 // CTA holding virtual position x (stream-K ranges B_c = floor(c * W / G))
@@ -107,12 +119,13 @@ __device__ __forceinline__ int64_t range_begin(int c, int64_t W, int G) { return
 // number of fragments this CTA processes
 __device__ __forceinline__ int num_fragments(const BsaParams& p, int c) {
     if (p.part_o == nullptr) return c < p.n_tiles ? (p.n_tiles - 1 - c) / p.grid + 1 : 0;
-    const int64_t a = range_begin(c, p.vtotal, p.grid), b = range_begin(c + 1, p.vtotal, p.grid);
-    if (b <= a) return 0;
-    return static_cast<int>((b - 1) / p.vlen - a / p.vlen) + 1;
+    if (c >= p.tail_grid || p.vtotal == 0) return p.whole_waves;
+    const int64_t a = range_begin(c, p.vtotal, p.tail_grid), b = range_begin(c + 1, p.vtotal, p.tail_grid);
+    if (b <= a) return p.whole_waves;
+    return p.whole_waves + static_cast<int>((b - 1) / p.vlen - a / p.vlen) + 1;
 }
 
-template <int D, int NSK, int NSV, int B>
+template <int D, int NSK, int NSV, int B, uint32_t POLY>
 __global__ void __launch_bounds__(kThreads, 2)
     bsa_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                    const __grid_constant__ CUtensorMap tm_v, const BsaParams p) {
@@ -352,26 +365,28 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int bcols = B > 0 ? B : p.b;
         const float2 scl2 = make_float2(p.scale_log2, p.scale_log2);
         int jg = 0;
-        const int64_t my_begin = p.part_o ? range_begin(cta, p.vtotal, p.grid) : 0;
-        const int64_t my_end = p.part_o ? range_begin(cta + 1, p.vtotal, p.grid) : 0;
-        const int my_first_tile = p.part_o ? static_cast<int>(my_begin / p.vlen) : cta;
+        const bool in_tail = p.part_o != nullptr && cta < p.tail_grid;
+        const int64_t my_begin = in_tail ? range_begin(cta, p.vtotal, p.tail_grid) : 0;
+        const int64_t my_end = in_tail ? range_begin(cta + 1, p.vtotal, p.tail_grid) : 0;
+        const int my_first_tile = p.tail_base + static_cast<int>(my_begin / p.vlen);  // first tail tile
 
         for (int f = 0; f < n_frag; ++f) {
             const int lb = 0;  // single list buffer: it is rebuilt only after the previous epilogue
             int32_t* list = lists + lb * p.max_list;
             // ---------------------------------------------------------- fragment schedule
-            const int tile = p.part_o ? my_first_tile + f : cta + f * p.grid;
+            const bool tail_frag = p.part_o != nullptr && f >= p.whole_waves;
+            const int tile = tail_frag ? my_first_tile + (f - p.whole_waves) : cta + f * p.grid;
             const int u = tile / p.tiles_per_unit;
             const int qb0 = 2 * (tile % p.tiles_per_unit);
             const bool has2 = qb0 + 1 < p.nqb;
             int64_t va = 0, vb = p.vlen;
             int nfr = 1, first_cta = cta;
-            if (p.part_o) {
-                const int64_t t0 = static_cast<int64_t>(tile) * p.vlen;
+            if (tail_frag) {
+                const int64_t t0 = static_cast<int64_t>(tile - p.tail_base) * p.vlen;
                 va = (my_begin > t0 ? my_begin : t0) - t0;
                 vb = (my_end < t0 + p.vlen ? my_end : t0 + p.vlen) - t0;
-                first_cta = cta_of(t0, p.vtotal, p.grid);
-                nfr = cta_of(t0 + p.vlen - 1, p.vtotal, p.grid) - first_cta + 1;
+                first_cta = cta_of(t0, p.vtotal, p.tail_grid);
+                nfr = cta_of(t0 + p.vlen - 1, p.vtotal, p.tail_grid) - first_cta + 1;
             }
             // ---------------------------------------------------------- visible list of the tile
             mbar_wait(list_empty + lb, (f & 1) ^ 1);
@@ -449,6 +464,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 pv_done(j - 2);  // already complete: S_j was committed after PV_{j-2}
                 const uint32_t t_s = t_o + L::kSColBase + buf * 64;
                 uint32_t pk[32];
+                float sv[64];  // S_j, then exp2 values
                 // rows of one warp all lie in one half -> visibility is warp-uniform
                 const bool vis = ((list[fm.e0 + idx] >> (24 + half)) & 1) && p.ablate != 1;
                 if (vis) {
@@ -456,7 +472,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                     tmem_ld32(t_s, *reinterpret_cast<uint32_t(*)[32]>(sr));
                     tmem_ld32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
                     tmem_wait_ld();
-                    float sv[64];
+                    if (threadIdx.x == 64) stamp(p, 7, j);  // S_j in registers
 #pragma unroll
                     for (int c = 0; c < 64; ++c) {
                         sv[c] = __uint_as_float(sr[c]);
@@ -475,6 +491,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                     }
                     float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * p.scale_log2;
                     if (!valid) mx = -INFINITY;
+                    if (threadIdx.x == 64) stamp(p, 8, j);  // row max done
                     float factor = 1.0f;
                     bool resc = false;
                     if (mx > m) {
@@ -502,33 +519,47 @@ __global__ void __launch_bounds__(kThreads, 2)
                     }
                     const float bias = valid ? -m : -INFINITY;  // padding rows -> p = 0
                     const float2 bias2 = make_float2(bias, bias);
-                    float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                                     make_float2(0.f, 0.f)};
 #pragma unroll
                     for (int c2 = 0; c2 < 32; ++c2) {
                         const float2 x = __ffma2_rn(make_float2(sv[2 * c2], sv[2 * c2 + 1]), scl2, bias2);
                         float2 e;
-                        e.x = (2 * c2 < BB) ? exp2_approx(x.x) : 0.0f;
-                        e.y = (2 * c2 + 1 < BB) ? exp2_approx(x.y) : 0.0f;
+                        if ((POLY >> c2) & 1u) {  // this column pair on the FMA pipe
+                            e = exp2_poly2(x);
+                            if (2 * c2 >= BB) e.x = 0.0f;
+                            if (2 * c2 + 1 >= BB) e.y = 0.0f;
+                        } else {
+                            e.x = (2 * c2 < BB) ? exp2_approx(x.x) : 0.0f;
+                            e.y = (2 * c2 + 1 < BB) ? exp2_approx(x.y) : 0.0f;
+                        }
                         if (B == 0) {
                             if (2 * c2 >= bcols) e.x = 0.0f;
                             if (2 * c2 + 1 >= bcols) e.y = 0.0f;
                         }
-                        acc[c2 & 3] = __fadd2_rn(acc[c2 & 3], e);
+                        sv[2 * c2] = e.x;  // kept for the row sum, taken after P_j is handed over
+                        sv[2 * c2 + 1] = e.y;
                         pk[c2] = pack_bf16x2(e.x, e.y);
                     }
-                    const float2 s01 = __fadd2_rn(__fadd2_rn(acc[0], acc[1]), __fadd2_rn(acc[2], acc[3]));
-                    l += s01.x + s01.y;
+                    if (threadIdx.x == 64) stamp(p, 9, j);  // exps done
                 } else {
 #pragma unroll
                     for (int c = 0; c < 32; ++c) pk[c] = 0u;
                 }
                 tmem_st32(t_s, pk);
                 tmem_wait_st();
+                if (threadIdx.x == 64) stamp(p, 10, j);  // P_j stored
                 tc_fence_before();
                 if (threadIdx.x == 64) stamp(p, 6, j);  // about to arrive P_j
                 __syncwarp();
                 if (lane == 0) mbar_arrive(p_full + buf);
+                if (vis) {  // row sum off the S -> P -> PV critical path
+                    float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                                     make_float2(0.f, 0.f)};
+#pragma unroll
+                    for (int c2 = 0; c2 < 32; ++c2)
+                        acc[c2 & 3] = __fadd2_rn(acc[c2 & 3], make_float2(sv[2 * c2], sv[2 * c2 + 1]));
+                    const float2 s01 = __fadd2_rn(__fadd2_rn(acc[0], acc[1]), __fadd2_rn(acc[2], acc[3]));
+                    l += s01.x + s01.y;
+                }
             }
             pv_done(jg + nf - 2);
             pv_done(jg + nf - 1);
@@ -603,7 +634,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                     const int nfr2 = fm.nf < 8 ? fm.nf : 8;
                     for (int q2 = 0; q2 < nfr2; ++q2) {
                         const int c2 = fm.first_cta + q2;
-                        const int first2 = static_cast<int>(range_begin(c2, p.vtotal, p.grid) / p.vlen);
+                        const int first2 =
+                            p.tail_base + static_cast<int>(range_begin(c2, p.vtotal, p.tail_grid) / p.vlen);
                         sl[q2] = 2 * c2 + (tile == first2 ? 0 : 1);
                         mf[q2] = __ldcg(p.part_ml + static_cast<int64_t>(sl[q2]) * 256 + r);
                         lf[q2] = __ldcg(p.part_ml + static_cast<int64_t>(sl[q2]) * 256 + 128 + r);
@@ -666,7 +698,7 @@ int num_sms() {
     return n;
 }
 
-template <int D, int NSK, int NSV, int B>
+template <int D, int NSK, int NSV, int B, uint32_t POLY>
 int launch_impl(const bf16* q, const bf16* kp, const bf16* vp, BsaParams p, cudaStream_t s) {
     using L = Layout<D, NSK, NSV>;
     alignas(64) CUtensorMap tq, tk, tv;
@@ -691,20 +723,29 @@ int launch_impl(const bf16* q, const bf16* kp, const bf16* vp, BsaParams p, cuda
     const size_t smem = L::bytes(p.max_list, p.bm_words);
     if (smem > 227 * 1024)
         return set_error(PBSA_EUNSUPPORTED, "bsa_fwd: visible list too long for shared memory");
-    if (int rc = ensure_smem(reinterpret_cast<const void*>(bsa_fwd_kernel<D, NSK, NSV, B>), smem, "bsa_fwd"))
+    if (int rc = ensure_smem(reinterpret_cast<const void*>(bsa_fwd_kernel<D, NSK, NSV, B, POLY>), smem, "bsa_fwd"))
         return rc;
     const int slots = 2 * num_sms();
+    p.grid = p.n_tiles < slots ? p.n_tiles : slots;
+    p.whole_waves = 0;
+    p.tail_base = 0;
+    p.tail_grid = 0;
+    p.vtotal = 0;
     if (p.part_o != nullptr) {
-        // at most ~4 CTAs share a tile (the merge handles up to 8 fragments)
+        p.grid = slots;
+        p.whole_waves = p.n_tiles / slots;
+        p.tail_base = p.whole_waves * slots;
+        const int64_t tail = p.n_tiles - p.tail_base;
+        p.vtotal = tail * p.vlen;
+        // at most ~4 CTAs share a tail tile (the merge handles up to 8 fragments)
         int64_t g = slots;
         if (g > p.vtotal) g = p.vtotal;
-        if (g > 4 * static_cast<int64_t>(p.n_tiles)) g = 4 * static_cast<int64_t>(p.n_tiles);
-        p.grid = static_cast<int>(g);
-    } else {
-        p.grid = p.n_tiles < slots ? p.n_tiles : slots;
+        if (g > 4 * tail) g = 4 * tail;
+        p.tail_grid = static_cast<int>(g);
+        if (p.whole_waves == 0) p.grid = p.tail_grid;
     }
     if (p.grid <= 0) return 0;
-    bsa_fwd_kernel<D, NSK, NSV, B><<<p.grid, kThreads, smem, s>>>(tq, tk, tv, p);
+    bsa_fwd_kernel<D, NSK, NSV, B, POLY><<<p.grid, kThreads, smem, s>>>(tq, tk, tv, p);
     return check_launch("bsa_fwd_kernel");
 }
 
@@ -754,7 +795,6 @@ int launch_bsa_fwd(const bf16* q, const bf16* k_pool, const bf16* v_pool, int n_
     p.tiles_per_unit = (nqb + 1) / 2;
     p.n_tiles = units * p.tiles_per_unit;
     p.vlen = p.max_list > 0 ? p.max_list : 1;
-    p.vtotal = static_cast<int64_t>(p.n_tiles) * p.vlen;
     if (units == 0 || nqb == 0) return 0;
     if (ws != nullptr) {
         if (ws_bytes < bsa_fwd_workspace(units, nqb, d))
@@ -765,13 +805,23 @@ int launch_bsa_fwd(const bf16* q, const bf16* k_pool, const bf16* v_pool, int n_
         p.counters = reinterpret_cast<int*>(p.part_ml + slots * 256);
     }
     if (d == 128) {
-        if (b == 60) return launch_impl<128, 2, 2, 60>(q, k_pool, v_pool, p, s);
-        if (b == 64) return launch_impl<128, 2, 2, 64>(q, k_pool, v_pool, p, s);
-        return launch_impl<128, 2, 2, 0>(q, k_pool, v_pool, p, s);
+        if (b == 60) {
+            // perf experiments only: PBSA_POLY selects the share of exp2 pairs on the FMA pipe
+            static const int poly = getenv("PBSA_POLY") ? atoi(getenv("PBSA_POLY")) : kPolyDefault;
+            switch (poly) {
+                case 0: return launch_impl<128, 2, 2, 60, 0u>(q, k_pool, v_pool, p, s);
+                case 1: return launch_impl<128, 2, 2, 60, 0x24924924u>(q, k_pool, v_pool, p, s);  // 1/3
+                case 2: return launch_impl<128, 2, 2, 60, 0x55555555u>(q, k_pool, v_pool, p, s);  // 1/2
+                case 4: return launch_impl<128, 2, 2, 60, 0x4A4A4A4Au>(q, k_pool, v_pool, p, s);  // 3/8
+                default: return launch_impl<128, 2, 2, 60, 0x11111111u>(q, k_pool, v_pool, p, s);  // 1/4
+            }
+        }
+        if (b == 64) return launch_impl<128, 2, 2, 64, kPolyMask>(q, k_pool, v_pool, p, s);
+        return launch_impl<128, 2, 2, 0, kPolyMask>(q, k_pool, v_pool, p, s);
     }
-    if (b == 60) return launch_impl<64, 3, 3, 60>(q, k_pool, v_pool, p, s);
-    if (b == 64) return launch_impl<64, 3, 3, 64>(q, k_pool, v_pool, p, s);
-    return launch_impl<64, 3, 3, 0>(q, k_pool, v_pool, p, s);
+    if (b == 60) return launch_impl<64, 3, 3, 60, 0u>(q, k_pool, v_pool, p, s);
+    if (b == 64) return launch_impl<64, 3, 3, 64, 0u>(q, k_pool, v_pool, p, s);
+    return launch_impl<64, 3, 3, 0, 0u>(q, k_pool, v_pool, p, s);
 }
 
 }  // namespace pbsa

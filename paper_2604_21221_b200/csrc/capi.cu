@@ -152,10 +152,10 @@ void free_mem(pbsa_mem* m) {
         if (p) cudaFree(p);
 }
 
-// The stream-K schedule of K3 is correct but measured slower than whole tiles at the Wan-1.3B
-// shape; opt in with PBSA_STREAM_K=1.
+// K3 runs the hybrid schedule (whole-tile waves + stream-K tail) by default;
+// PBSA_STREAM_K=0 selects whole tiles only (perf experiments).
 bool use_stream_k() {
-    static const bool on = getenv("PBSA_STREAM_K") && atoi(getenv("PBSA_STREAM_K")) != 0;
+    static const bool on = !(getenv("PBSA_STREAM_K") && atoi(getenv("PBSA_STREAM_K")) == 0);
     return on;
 }
 

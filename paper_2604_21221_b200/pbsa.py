@@ -109,7 +109,7 @@ def attention_sparse(q: torch.Tensor, k_pool: torch.Tensor, v_pool: torch.Tensor
                      dense_slots: torch.Tensor | None, local_slots: torch.Tensor | None,
                      sel: torch.Tensor | None, b: int, scale: float | None = None,
                      n_dense: int | None = None, n_local: int | None = None,
-                     want_lse: bool = False, stream_k: bool = False):
+                     want_lse: bool = False, stream_k: bool = True):
     """Block-sparse attention forward.
 
     q [units, nqb*b, d] bf16 (query tokens block-major); k_pool / v_pool [units, n_slots, 64, d]

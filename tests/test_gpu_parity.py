@@ -152,6 +152,11 @@ def test_bsa_fwd_stream_k_many_tiles(pb):
     _bsa_case(pb, 40, 17, 60, 128, 10, 24, 6, seed=21, stream_k=False)
 
 
+def test_bsa_fwd_hybrid_two_waves_and_tail(pb):
+    """Two full waves of whole tiles (2 x 296 CTA slots on a B200) then a stream-K tail."""
+    _bsa_case(pb, 70, 17, 60, 128, 5, 12, 3, seed=22)
+
+
 def test_bsa_fwd_dense_only_and_full_local(pb):
     _bsa_case(pb, 2, 4, 60, 128, 9, 0, 0, seed=1)     # first chunk: no local window
     _bsa_case(pb, 1, 3, 60, 128, 0, 10, 10, seed=2)   # k = N_l (full visibility), no P
