@@ -26,7 +26,7 @@
 //           K and V slots (2-D maps over the slot pools, one 64x64 box per d-half)
 //   warp 1  tcgen05 issuer: S_j = Q K_j^T (SS, M128 N64), O += P_j V_j (TS: P from TMEM as packed
 //           bf16, V as an MN-major operand), commits to mbarriers
-//   warps 2-5  list builder + softmax: thread = query row = TMEM lane; online softmax with lazy
+//   warps 2-5  softmax: thread = query row = TMEM lane; online softmax with lazy
 //           rescale (only when the running max grows by > 8 in log2 units), P written back over
 //           S in TMEM; epilogue O / l straight from TMEM to HBM (or to the partial workspace).
 // TMEM: O [0, d), S0 [d, d+64), S1 [d+64, d+128) -> 256 columns, two CTAs per SM.
@@ -97,7 +97,7 @@ struct Layout {
     static constexpr uint32_t kOffList = kOffMisc + 16;
     static constexpr uint32_t kSColBase = D;  // S0 at D, S1 at D + 64
     static size_t bytes(int max_list, int bm_words) {
-        return 1024 + kOffList + static_cast<size_t>(max_list) * 4 + 2 * static_cast<size_t>(bm_words) * 4;
+        return 1024 + kOffList + 2 * static_cast<size_t>(max_list) * 4 + 2 * static_cast<size_t>(bm_words) * 4;
     }
 };
 
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     FragMeta* meta = reinterpret_cast<FragMeta*>(smem + L::kOffMeta);
     uint32_t* misc = reinterpret_cast<uint32_t*>(smem + L::kOffMisc);  // [0] tmem base, [1] merge flag
     int32_t* lists = reinterpret_cast<int32_t*>(smem + L::kOffList);  // [max_list]
-    uint32_t* bm = reinterpret_cast<uint32_t*>(lists + p.max_list);  // [2][bm_words]
+    uint32_t* bm = reinterpret_cast<uint32_t*>(lists + 2 * p.max_list);  // [2][bm_words] (producer only)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int cta = blockIdx.x;
@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             mbar_init(p_full + s, 4);  // one elected arrival per softmax warp
             mbar_init(o_done + s, 1);
             mbar_init(list_full + s, 1);
-            mbar_init(list_empty + s, 2);
+            mbar_init(list_empty + s, 5);  // MMA warp + 4 softmax warps
         }
         mbar_init(o_free, 4);
         fence_barrier_init();
@@ -204,12 +204,90 @@ __global__ void __launch_bounds__(kThreads, 2)
         // ============================================================== TMA producer
         // whole warp in the loop (uniform operands), one elected lane issues each TMA
         {
+            // The producer also builds each fragment's visible list (double-buffered): list f+1 is
+            // built while the MMA / softmax warps still work on the last blocks of fragment f.
+            const bool in_tail = p.part_o != nullptr && cta < p.tail_grid;
+            const int64_t my_begin = in_tail ? range_begin(cta, p.vtotal, p.tail_grid) : 0;
+            const int64_t my_end = in_tail ? range_begin(cta + 1, p.vtotal, p.tail_grid) : 0;
+            const int my_first_tile = p.tail_base + static_cast<int>(my_begin / p.vlen);  // first tail tile
             int jg = 0, q_uses = 0;
             for (int f = 0; f < n_frag; ++f) {
-                const int lb = 0;  // single list buffer: it is rebuilt only after the previous epilogue
-                mbar_wait(list_full + lb, f & 1);
-                const FragMeta fm = meta[lb];
-                const int32_t* list = lists + lb * p.max_list;
+                const int lb = f & 1;
+                mbar_wait(list_empty + lb, ((f >> 1) & 1) ^ 1);
+                int32_t* list = lists + lb * p.max_list;
+                // ---------------------------------------------------------- fragment schedule
+                const bool tail_frag = p.part_o != nullptr && f >= p.whole_waves;
+                const int tile = tail_frag ? my_first_tile + (f - p.whole_waves) : cta + f * p.grid;
+                const int u = tile / p.tiles_per_unit;
+                const int qb0 = 2 * (tile % p.tiles_per_unit);
+                const bool has2 = qb0 + 1 < p.nqb;
+                int64_t va = 0, vb = p.vlen;
+                int nfr = 1, first_cta = cta;
+                if (tail_frag) {
+                    const int64_t t0 = static_cast<int64_t>(tile - p.tail_base) * p.vlen;
+                    va = (my_begin > t0 ? my_begin : t0) - t0;
+                    vb = (my_end < t0 + p.vlen ? my_end : t0 + p.vlen) - t0;
+                    first_cta = cta_of(t0, p.vtotal, p.tail_grid);
+                    nfr = cta_of(t0 + p.vlen - 1, p.vtotal, p.tail_grid) - first_cta + 1;
+                }
+                // ---------------------------------------------------------- visible list of the tile
+                // dense blocks first (both halves), then the union of the two Top-K selections in
+                // ascending local order with a 2-bit visibility mask in bits 24-25
+                for (int w = lane; w < 2 * p.bm_words; w += 32) bm[w] = 0u;
+                __syncwarp();
+                if (p.k > 0 && p.n_local > 0) {
+                    const int sel_rows = has2 ? 2 : 1;
+                    for (int e = lane; e < sel_rows * p.k; e += 32) {
+                        const int rw = e / p.k, c = e % p.k;
+                        const int idx = __ldg(p.sel + (static_cast<int64_t>(u) * p.nqb + qb0 + rw) * p.k + c);
+                        atomicOr(&bm[rw * p.bm_words + (idx >> 5)], 1u << (idx & 31));
+                    }
+                }
+                for (int e = lane; e < p.n_dense; e += 32)
+                    list[e] = __ldg(p.dense + static_cast<int64_t>(u) * p.dense_stride + e) | (3 << 24);
+                __syncwarp();
+                int run = p.n_dense;
+                {
+                    const int32_t* loc = p.local + static_cast<int64_t>(u) * p.local_stride;
+                    for (int w0 = 0; w0 < p.bm_words; w0 += 32) {
+                        const int w = w0 + lane;
+                        const uint32_t a = w < p.bm_words ? bm[w] : 0u;
+                        const uint32_t c = w < p.bm_words ? bm[p.bm_words + w] : 0u;
+                        uint32_t un = a | c;
+                        const int cnt = __popc(un);
+                        int incl = cnt;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                            if (lane >= o) incl += y;
+                        }
+                        int pos = run + incl - cnt;
+                        while (un) {
+                            const int bit = __ffs(un) - 1;
+                            un &= un - 1;
+                            const int idx = w * 32 + bit;
+                            const int mask = static_cast<int>((a >> bit) & 1u) | (static_cast<int>((c >> bit) & 1u) << 1);
+                            list[pos++] = __ldg(loc + idx) | (mask << 24);
+                        }
+                        run += __shfl_sync(0xffffffffu, incl, 31);
+                    }
+                }
+                FragMeta fm;
+                fm.tile = tile;
+                fm.u = u;
+                fm.qb0 = qb0;
+                fm.has2 = has2;
+                fm.n = run;
+                fm.e0 = static_cast<int>((va * run) / p.vlen);
+                fm.e1 = static_cast<int>((vb * run) / p.vlen);
+                fm.whole = (nfr == 1);
+                fm.nf = nfr;
+                fm.slot = 2 * cta + (tile == my_first_tile ? 0 : 1);
+                fm.first_cta = first_cta;
+                fm.pad = 0;
+                if (lane == 0) meta[lb] = fm;
+                __syncwarp();
+                if (lane == 0) mbar_arrive(list_full + lb);
                 const int nf = fm.e1 - fm.e0;
                 if (nf > 0) {
                     if (q_uses > 0) mbar_wait(q_empty, (q_uses - 1) & 1);
@@ -259,8 +337,6 @@ __global__ void __launch_bounds__(kThreads, 2)
                     load_v(nf - 1);
                     jg += nf;
                 }
-                if (lane == 0) mbar_arrive(list_empty + lb);
-                __syncwarp();
             }
         }
     } else if (warp == 1) {
@@ -296,8 +372,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                 __syncwarp();
             };
             for (int f = 0; f < n_frag; ++f) {
-                const int lb = 0;  // single list buffer: it is rebuilt only after the previous epilogue
-                mbar_wait(list_full + lb, f & 1);
+                const int lb = f & 1;
+                mbar_wait(list_full + lb, (f >> 1) & 1);
                 const int nf = meta[lb].e1 - meta[lb].e0;
                 __syncwarp();
                 if (lane == 0) mbar_arrive(list_empty + lb);
@@ -338,7 +414,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
         }
     } else {
-        // ============================================================== list builder + softmax
+        // ============================================================== softmax
         const int t = threadIdx.x - 64;
         const int quarter = warp & 3;
         const int r = quarter * 32 + lane;
@@ -365,90 +441,13 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int bcols = B > 0 ? B : p.b;
         const float2 scl2 = make_float2(p.scale_log2, p.scale_log2);
         int jg = 0;
-        const bool in_tail = p.part_o != nullptr && cta < p.tail_grid;
-        const int64_t my_begin = in_tail ? range_begin(cta, p.vtotal, p.tail_grid) : 0;
-        const int64_t my_end = in_tail ? range_begin(cta + 1, p.vtotal, p.tail_grid) : 0;
-        const int my_first_tile = p.tail_base + static_cast<int>(my_begin / p.vlen);  // first tail tile
-
         for (int f = 0; f < n_frag; ++f) {
-            const int lb = 0;  // single list buffer: it is rebuilt only after the previous epilogue
-            int32_t* list = lists + lb * p.max_list;
-            // ---------------------------------------------------------- fragment schedule
-            const bool tail_frag = p.part_o != nullptr && f >= p.whole_waves;
-            const int tile = tail_frag ? my_first_tile + (f - p.whole_waves) : cta + f * p.grid;
-            const int u = tile / p.tiles_per_unit;
-            const int qb0 = 2 * (tile % p.tiles_per_unit);
-            const bool has2 = qb0 + 1 < p.nqb;
-            int64_t va = 0, vb = p.vlen;
-            int nfr = 1, first_cta = cta;
-            if (tail_frag) {
-                const int64_t t0 = static_cast<int64_t>(tile - p.tail_base) * p.vlen;
-                va = (my_begin > t0 ? my_begin : t0) - t0;
-                vb = (my_end < t0 + p.vlen ? my_end : t0 + p.vlen) - t0;
-                first_cta = cta_of(t0, p.vtotal, p.tail_grid);
-                nfr = cta_of(t0 + p.vlen - 1, p.vtotal, p.tail_grid) - first_cta + 1;
-            }
-            // ---------------------------------------------------------- visible list of the tile
-            mbar_wait(list_empty + lb, (f & 1) ^ 1);
-            for (int w = t; w < 2 * p.bm_words; w += 128) bm[w] = 0u;
-            named_bar_sync(1, 128);
-            if (p.k > 0 && p.n_local > 0) {
-                const int sel_rows = has2 ? 2 : 1;
-                for (int e = t; e < sel_rows * p.k; e += 128) {
-                    const int rw = e / p.k, c = e % p.k;
-                    const int idx = __ldg(p.sel + (static_cast<int64_t>(u) * p.nqb + qb0 + rw) * p.k + c);
-                    atomicOr(&bm[rw * p.bm_words + (idx >> 5)], 1u << (idx & 31));
-                }
-            }
-            for (int e = t; e < p.n_dense; e += 128)
-                list[e] = __ldg(p.dense + static_cast<int64_t>(u) * p.dense_stride + e) | (3 << 24);
-            named_bar_sync(1, 128);
-            if (warp == 2) {
-                int run = p.n_dense;
-                const int32_t* loc = p.local + static_cast<int64_t>(u) * p.local_stride;
-                for (int w0 = 0; w0 < p.bm_words; w0 += 32) {
-                    const int w = w0 + lane;
-                    const uint32_t a = w < p.bm_words ? bm[w] : 0u;
-                    const uint32_t c = w < p.bm_words ? bm[p.bm_words + w] : 0u;
-                    uint32_t un = a | c;
-                    const int cnt = __popc(un);
-                    int incl = cnt;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-                        if (lane >= o) incl += y;
-                    }
-                    int pos = run + incl - cnt;
-                    while (un) {
-                        const int bit = __ffs(un) - 1;
-                        un &= un - 1;
-                        const int idx = w * 32 + bit;
-                        const int mask = static_cast<int>((a >> bit) & 1u) | (static_cast<int>((c >> bit) & 1u) << 1);
-                        list[pos++] = __ldg(loc + idx) | (mask << 24);
-                    }
-                    run += __shfl_sync(0xffffffffu, incl, 31);
-                }
-                if (lane == 0) {
-                    FragMeta fm;
-                    fm.tile = tile;
-                    fm.u = u;
-                    fm.qb0 = qb0;
-                    fm.has2 = has2;
-                    fm.n = run;
-                    fm.e0 = static_cast<int>((va * run) / p.vlen);
-                    fm.e1 = static_cast<int>((vb * run) / p.vlen);
-                    fm.whole = (nfr == 1);
-                    fm.nf = nfr;
-                    fm.slot = 2 * cta + (tile == my_first_tile ? 0 : 1);
-                    fm.first_cta = first_cta;
-                    fm.pad = 0;
-                    meta[lb] = fm;
-                }
-            }
-            named_bar_sync(1, 128);
-            if (t == 0) mbar_arrive(list_full + lb);
+            const int lb = f & 1;
+            const int32_t* list = lists + lb * p.max_list;
+            mbar_wait(list_full + lb, (f >> 1) & 1);
             const FragMeta fm = meta[lb];
             const int nf = fm.e1 - fm.e0;
+            const int tile = fm.tile, u = fm.u, qb0 = fm.qb0;
             const int qb = qb0 + half;
             const bool valid = rr < p.b && qb < p.nqb;
 
@@ -561,6 +560,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                     l += s01.x + s01.y;
                 }
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(list_empty + lb);  // this warp is done with the list
             pv_done(jg + nf - 2);
             pv_done(jg + nf - 1);
             tc_fence_after();

@@ -93,6 +93,14 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, ui
         : "memory");
 }
 
+// L2 prefetch of one 2-D TMA box (no shared memory, no barrier)
+__device__ __forceinline__ void tma_prefetch_l2_2d(const CUtensorMap* tm, int c0, int c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                     reinterpret_cast<uint64_t>(tm)),
+                 "r"(c0), "r"(c1)
+                 : "memory");
+}
+
 // ---------------------------------------------------------------- tcgen05: TMEM management
 template <uint32_t kCols>
 __device__ __forceinline__ void tmem_alloc(uint32_t* holder_smem) {  // whole warp
