@@ -45,8 +45,8 @@ constexpr int kThreads = 192;
 constexpr uint32_t kTmemCols = 256;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units
 // column pairs whose exp2 runs as a polynomial on the FMA pipe instead of MUFU (bit c2 = pair c2)
-constexpr uint32_t kPolyMask = 0x11111111u;
-constexpr int kPolyDefault = 3;
+constexpr uint32_t kPolyMask = 0u;  // MUFU-only: the softmax is issue/latency-bound, not MUFU-bound
+constexpr int kPolyDefault = 0;
 
 struct BsaParams {
     int units, nqb, b, n_slots;
@@ -453,6 +453,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 
             // ---------------------------------------------------------- online softmax
             float m = -INFINITY, l = 0.0f;
+            const uint32_t list_s = smem_u32(list + fm.e0);
             for (int idx = 0; idx < nf; ++idx) {
                 const int j = jg + idx;
                 const int buf = j & 1;
@@ -462,11 +463,11 @@ __global__ void __launch_bounds__(kThreads, 2)
                 tc_fence_after();
                 pv_done(j - 2);  // already complete: S_j was committed after PV_{j-2}
                 const uint32_t t_s = t_o + L::kSColBase + buf * 64;
-                uint32_t pk[32];
                 float sv[64];  // S_j, then exp2 values
                 // rows of one warp all lie in one half -> visibility is warp-uniform
-                const bool vis = ((list[fm.e0 + idx] >> (24 + half)) & 1) && p.ablate != 1;
+                const bool vis = ((ld_shared_u32(list_s + idx * 4) >> (24 + half)) & 1) && p.ablate != 1;
                 if (vis) {
+                    uint32_t pk[32];
                     uint32_t sr[64];
                     tmem_ld32(t_s, *reinterpret_cast<uint32_t(*)[32]>(sr));
                     tmem_ld32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
@@ -491,18 +492,14 @@ __global__ void __launch_bounds__(kThreads, 2)
                     float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * p.scale_log2;
                     if (!valid) mx = -INFINITY;
                     if (threadIdx.x == 64) stamp(p, 8, j);  // row max done
-                    float factor = 1.0f;
-                    bool resc = false;
-                    if (mx > m) {
-                        if (m == -INFINITY) {
-                            m = mx;  // first visible block for this row: its O row is still zero
-                        } else if (mx > m + kRescaleThreshold) {
-                            factor = exp2_approx(m - mx);
-                            m = mx;
-                            resc = true;
-                        }
-                    }
+                    // lazy rescale, branch-free: the running max moves only when the block max
+                    // exceeds it by > kRescaleThreshold (or on the row's first visible block, whose
+                    // O row is still zero -- no rescale then)
+                    const bool grow = mx > m + kRescaleThreshold;
+                    const bool resc = grow && m != -INFINITY;
+                    const float m_new = grow ? mx : m;
                     if (__any_sync(0xffffffffu, resc)) {
+                        const float factor = resc ? exp2_approx(m - m_new) : 1.0f;
                         pv_done(j - 1);
                         tc_fence_after();
 #pragma unroll 1
@@ -516,6 +513,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                         }
                         l *= factor;
                     }
+                    m = m_new;
                     const float bias = valid ? -m : -INFINITY;  // padding rows -> p = 0
                     const float2 bias2 = make_float2(bias, bias);
 #pragma unroll
@@ -539,11 +537,13 @@ __global__ void __launch_bounds__(kThreads, 2)
                         pk[c2] = pack_bf16x2(e.x, e.y);
                     }
                     if (threadIdx.x == 64) stamp(p, 9, j);  // exps done
+                    tmem_st32(t_s, pk);
                 } else {
+                    uint32_t zero[32];
 #pragma unroll
-                    for (int c = 0; c < 32; ++c) pk[c] = 0u;
+                    for (int c = 0; c < 32; ++c) zero[c] = 0u;
+                    tmem_st32(t_s, zero);
                 }
-                tmem_st32(t_s, pk);
                 tmem_wait_st();
                 if (threadIdx.x == 64) stamp(p, 10, j);  // P_j stored
                 tc_fence_before();
