@@ -421,21 +421,12 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int half = r >> 6, rr = r & 63;
         const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
         const uint32_t t_o = tmem + lane_base;
-        int o_waited0 = 0, o_waited1 = 0;
-        auto pv_done = [&](int x) {  // wait until PV_x has completed
-            if (x < 0) return;
-            const int need = (x >> 1) + 1;
-            if (x & 1) {
-                while (o_waited1 < need) {
-                    mbar_wait(o_done + 1, o_waited1 & 1);
-                    ++o_waited1;
-                }
-            } else {
-                while (o_waited0 < need) {
-                    mbar_wait(o_done + 0, o_waited0 & 1);
-                    ++o_waited0;
-                }
-            }
+        // Wait until PV_x has completed.  o_done[x & 1] completes once per PV of that parity; PV_x
+        // is the LATEST PV of its parity that can have been issued when this is called (PV_{x+2}
+        // needs P_{x+2}, which this warp has not produced), so the barrier is at most one phase
+        // past PV_x's and a plain parity wait is exact -- no per-block bookkeeping.
+        auto pv_done = [&](int x) {
+            if (x >= 0) mbar_wait(o_done + (x & 1), (x >> 1) & 1);
         };
         constexpr int BB = B > 0 ? B : 64;
         const int bcols = B > 0 ? B : p.b;
@@ -461,7 +452,6 @@ __global__ void __launch_bounds__(kThreads, 2)
                 mbar_wait(s_full + buf, (j >> 1) & 1);
                 if (threadIdx.x == 64) stamp(p, 5, j);  // S_j seen
                 tc_fence_after();
-                pv_done(j - 2);  // already complete: S_j was committed after PV_{j-2}
                 const uint32_t t_s = t_o + L::kSColBase + buf * 64;
                 float sv[64];  // S_j, then exp2 values
                 // rows of one warp all lie in one half -> visibility is warp-uniform
@@ -554,7 +544,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                     float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                                      make_float2(0.f, 0.f)};
 #pragma unroll
-                    for (int c2 = 0; c2 < 32; ++c2)
+                    for (int c2 = 0; c2 < (BB + 1) / 2; ++c2)
                         acc[c2 & 3] = __fadd2_rn(acc[c2 & 3], make_float2(sv[2 * c2], sv[2 * c2 + 1]));
                     const float2 s01 = __fadd2_rn(__fadd2_rn(acc[0], acc[1]), __fadd2_rn(acc[2], acc[3]));
                     l += s01.x + s01.y;
