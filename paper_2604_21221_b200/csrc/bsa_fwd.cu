@@ -43,7 +43,8 @@ namespace {
 
 constexpr int kThreads = 192;
 constexpr uint32_t kTmemCols = 256;
-constexpr float kRescaleThreshold = 8.0f;  // log2 units
+// a block whose row sum (against the running max) exceeds this takes the exact rescale path
+constexpr float kOverflowSum = 65536.0f;
 // column pairs whose exp2 runs as a polynomial on the FMA pipe instead of MUFU (bit c2 = pair c2)
 constexpr uint32_t kPolyMask = 0u;  // MUFU-only: the softmax is issue/latency-bound, not MUFU-bound
 constexpr int kPolyDefault = 0;
@@ -453,43 +454,78 @@ __global__ void __launch_bounds__(kThreads, 2)
                 if (threadIdx.x == 64) stamp(p, 5, j);  // S_j seen
                 tc_fence_after();
                 const uint32_t t_s = t_o + L::kSColBase + buf * 64;
-                float sv[64];  // S_j, then exp2 values
                 // rows of one warp all lie in one half -> visibility is warp-uniform
                 const bool vis = ((ld_shared_u32(list_s + idx * 4) >> (24 + half)) & 1) && p.ablate != 1;
                 if (vis) {
                     uint32_t pk[32];
-                    uint32_t sr[64];
-                    tmem_ld32(t_s, *reinterpret_cast<uint32_t(*)[32]>(sr));
-                    tmem_ld32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(sr + 32));
+                    float sv[64];
+                    tmem_ld32(t_s, *reinterpret_cast<uint32_t(*)[32]>(sv));
+                    tmem_ld32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
                     tmem_wait_ld();
                     if (threadIdx.x == 64) stamp(p, 7, j);  // S_j in registers
+                    if (B == 0) {
 #pragma unroll
-                    for (int c = 0; c < 64; ++c) {
-                        sv[c] = __uint_as_float(sr[c]);
-                        if (B == 0 && c >= bcols) sv[c] = -INFINITY;  // generic block size
+                        for (int c = 0; c < 64; ++c)
+                            if (c >= bcols) sv[c] = -INFINITY;  // generic block size
                     }
-                    float mx4[4];
+                    auto row_max = [&]() {
+                        float mx4[4];
 #pragma unroll
-                    for (int q4 = 0; q4 < 4; ++q4) {
-                        float a = -INFINITY;
+                        for (int q4 = 0; q4 < 4; ++q4) {
+                            float a = -INFINITY;
 #pragma unroll
-                        for (int c = q4 * 16; c < q4 * 16 + 16; c += 2) {
-                            if (c + 1 < BB) a = fmax3(a, sv[c], sv[c + 1]);
-                            else if (c < BB) a = fmaxf(a, sv[c]);
+                            for (int c = q4 * 16; c < q4 * 16 + 16; c += 2) {
+                                if (c + 1 < BB) a = fmax3(a, sv[c], sv[c + 1]);
+                                else if (c < BB) a = fmaxf(a, sv[c]);
+                            }
+                            mx4[q4] = a;
                         }
-                        mx4[q4] = a;
+                        return fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * p.scale_log2;
+                    };
+                    // P_j = 2^(s * scale * log2e - m) packed to bf16 pairs; returns the block row sum
+                    auto exps = [&]() {
+                        const float bias = valid ? -m : -INFINITY;  // padding rows -> p = 0
+                        const float2 bias2 = make_float2(bias, bias);
+                        float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                                         make_float2(0.f, 0.f)};
+#pragma unroll
+                        for (int c2 = 0; c2 < 32; ++c2) {
+                            const float2 x = __ffma2_rn(make_float2(sv[2 * c2], sv[2 * c2 + 1]), scl2, bias2);
+                            float2 e;
+                            if ((POLY >> c2) & 1u) {  // this column pair on the FMA pipe
+                                e = exp2_poly2(x);
+                                if (2 * c2 >= BB) e.x = 0.0f;
+                                if (2 * c2 + 1 >= BB) e.y = 0.0f;
+                            } else {
+                                e.x = (2 * c2 < BB) ? exp2_approx(x.x) : 0.0f;
+                                e.y = (2 * c2 + 1 < BB) ? exp2_approx(x.y) : 0.0f;
+                            }
+                            if (B == 0) {
+                                if (2 * c2 >= bcols) e.x = 0.0f;
+                                if (2 * c2 + 1 >= bcols) e.y = 0.0f;
+                            }
+                            if (2 * c2 < BB) acc[c2 & 3] = __fadd2_rn(acc[c2 & 3], e);
+                            pk[c2] = pack_bf16x2(e.x, e.y);
+                        }
+                        const float2 s01 = __fadd2_rn(__fadd2_rn(acc[0], acc[1]), __fadd2_rn(acc[2], acc[3]));
+                        return s01.x + s01.y;
+                    };
+                    // Running max without a per-block max: the row's first visible block sets m
+                    // exactly (its O row is still zero); later blocks are exponentiated against the
+                    // running m directly, and only a block whose row sum exceeds kOverflowSum (some
+                    // score grew by ~10 in log2 units, or overflowed to inf) takes the exact path:
+                    // true block max, O and l rescaled, P recomputed.  Values below that bound are
+                    // exact-range fp32 / bf16, so the result is the usual online softmax.
+                    if (__any_sync(0xffffffffu, valid && m == -INFINITY)) {
+                        const float mx = row_max();
+                        if (valid && m == -INFINITY) m = mx;
                     }
-                    float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * p.scale_log2;
-                    if (!valid) mx = -INFINITY;
-                    if (threadIdx.x == 64) stamp(p, 8, j);  // row max done
-                    // lazy rescale, branch-free: the running max moves only when the block max
-                    // exceeds it by > kRescaleThreshold (or on the row's first visible block, whose
-                    // O row is still zero -- no rescale then)
-                    const bool grow = mx > m + kRescaleThreshold;
-                    const bool resc = grow && m != -INFINITY;
-                    const float m_new = grow ? mx : m;
-                    if (__any_sync(0xffffffffu, resc)) {
-                        const float factor = resc ? exp2_approx(m - m_new) : 1.0f;
+                    float lsum = exps();
+                    if (threadIdx.x == 64) stamp(p, 8, j);  // exps done
+                    const bool over = valid && lsum > kOverflowSum;
+                    if (__any_sync(0xffffffffu, over)) {
+                        const float m_new = over ? row_max() : m;
+                        const float factor = over ? exp2_approx(m - m_new) : 1.0f;
                         pv_done(j - 1);
                         tc_fence_after();
 #pragma unroll 1
@@ -502,31 +538,11 @@ __global__ void __launch_bounds__(kThreads, 2)
                             tmem_st32(t_o + c0, ov);
                         }
                         l *= factor;
+                        m = m_new;
+                        lsum = exps();
                     }
-                    m = m_new;
-                    const float bias = valid ? -m : -INFINITY;  // padding rows -> p = 0
-                    const float2 bias2 = make_float2(bias, bias);
-#pragma unroll
-                    for (int c2 = 0; c2 < 32; ++c2) {
-                        const float2 x = __ffma2_rn(make_float2(sv[2 * c2], sv[2 * c2 + 1]), scl2, bias2);
-                        float2 e;
-                        if ((POLY >> c2) & 1u) {  // this column pair on the FMA pipe
-                            e = exp2_poly2(x);
-                            if (2 * c2 >= BB) e.x = 0.0f;
-                            if (2 * c2 + 1 >= BB) e.y = 0.0f;
-                        } else {
-                            e.x = (2 * c2 < BB) ? exp2_approx(x.x) : 0.0f;
-                            e.y = (2 * c2 + 1 < BB) ? exp2_approx(x.y) : 0.0f;
-                        }
-                        if (B == 0) {
-                            if (2 * c2 >= bcols) e.x = 0.0f;
-                            if (2 * c2 + 1 >= bcols) e.y = 0.0f;
-                        }
-                        sv[2 * c2] = e.x;  // kept for the row sum, taken after P_j is handed over
-                        sv[2 * c2 + 1] = e.y;
-                        pk[c2] = pack_bf16x2(e.x, e.y);
-                    }
-                    if (threadIdx.x == 64) stamp(p, 9, j);  // exps done
+                    l += lsum;
+                    if (threadIdx.x == 64) stamp(p, 9, j);  // P_j ready
                     tmem_st32(t_s, pk);
                 } else {
                     uint32_t zero[32];
@@ -540,15 +556,6 @@ __global__ void __launch_bounds__(kThreads, 2)
                 if (threadIdx.x == 64) stamp(p, 6, j);  // about to arrive P_j
                 __syncwarp();
                 if (lane == 0) mbar_arrive(p_full + buf);
-                if (vis) {  // row sum off the S -> P -> PV critical path
-                    float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                                     make_float2(0.f, 0.f)};
-#pragma unroll
-                    for (int c2 = 0; c2 < (BB + 1) / 2; ++c2)
-                        acc[c2 & 3] = __fadd2_rn(acc[c2 & 3], make_float2(sv[2 * c2], sv[2 * c2 + 1]));
-                    const float2 s01 = __fadd2_rn(__fadd2_rn(acc[0], acc[1]), __fadd2_rn(acc[2], acc[3]));
-                    l += s01.x + s01.y;
-                }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(list_empty + lb);  // this warp is done with the list

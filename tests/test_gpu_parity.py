@@ -114,7 +114,7 @@ def test_score_select_long_path_rows_across_units(pb):
 
 
 # ------------------------------------------------------------------ (c) block-sparse attention
-def _bsa_case(pb, units, nqb, b, d, n_dense, n_local, k, seed, scale_q=1.0, stream_k=True):
+def _bsa_case(pb, units, nqb, b, d, n_dense, n_local, k, seed, scale_q=1.0, stream_k=True, k_ramp=False):
     g = np.random.default_rng(seed)
     n_slots = n_dense + n_local + 3
     kp = np.zeros((units, n_slots, 64, d), np.float32)
@@ -124,6 +124,10 @@ def _bsa_case(pb, units, nqb, b, d, n_dense, n_local, k, seed, scale_q=1.0, stre
     q = normal_bf16(seed + 3, (units, nqb * b, d)) * np.float32(scale_q)
     q = bf16_round(q)
     perm = np.stack([g.permutation(n_slots) for _ in range(units)]).astype(np.int32)
+    if k_ramp:  # scores grow along the visiting order (x 2 every two dense blocks, exact in bf16)
+        for u in range(units):
+            for i in range(n_dense):
+                kp[u, perm[u, i]] *= np.float32(2.0 ** (i // 2))
     dense = np.ascontiguousarray(perm[:, :n_dense])
     local = np.ascontiguousarray(perm[:, n_dense:n_dense + n_local])
     sel = np.stack([np.stack([np.sort(g.choice(n_local, k, replace=False)) for _ in range(nqb)])
@@ -150,6 +154,14 @@ def test_bsa_fwd_stream_k_many_tiles(pb):
     stream-K and whole-tile schedules must agree."""
     _bsa_case(pb, 40, 17, 60, 128, 10, 24, 6, seed=21)
     _bsa_case(pb, 40, 17, 60, 128, 10, 24, 6, seed=21, stream_k=False)
+
+
+def test_bsa_fwd_growing_scores_rescale_path(pb):
+    """Block maxima grow by up to 2^5 along the list: later blocks overflow the running-max fast
+    path (row sums beyond the bound, or inf) and must take the exact rescale path."""
+    _bsa_case(pb, 2, 6, 60, 128, 12, 24, 6, seed=31, k_ramp=True)
+    _bsa_case(pb, 2, 6, 60, 128, 12, 24, 6, seed=32, k_ramp=True, scale_q=0.25)
+    _bsa_case(pb, 1, 4, 64, 64, 10, 8, 3, seed=33, k_ramp=True)
 
 
 def test_bsa_fwd_hybrid_two_waves_and_tail(pb):
