@@ -9,8 +9,11 @@ row-wise Top-K k = 78 blocks (25 %), bf16 Q/K/V.  One STEP = one chunk of Alg. 1
 T = 4 denoise PBSA calls + 1 k=0 cache-update call (K1 Q compression, KV write + K compression,
 K2 scoring/Top-K (+ s_t), K3 block-sparse attention, K4 memory update).
 
-Multi-GPU: one process per GPU; every rank owns an independent batch element (12 heads) -- heads
-and batch shard with no data-path collective ("scaling": "weak"); timing is the max over ranks.
+Multi-GPU: one process per GPU, global batch = N (per-GPU work fixed: "scaling": "weak").  The
+batch x 12 head units are HEAD-partitioned round robin (unit u = e*12 + h on rank u % N), so every
+rank holds heads of several batch elements; after each PBSA call one NCCL all-to-all moves each
+head's output to its batch element's rank (the output gather of SURVEY.md section 8(e)), issued
+asynchronously so it overlaps the next call.  Timing is the max over ranks.
 
 Output: ONE JSON line on rank 0 (see README / DESIGN.md section 6 for every key).
 """
@@ -63,7 +66,9 @@ def config_block(k_top, n_gpus):
             "block_tokens": g["b"], "block_shape": [1, 15, 4], "tokens_per_frame": 1560,
             "chunk_frames": 3, "query_tokens_per_chunk": g["bpc"] * g["b"],
             "kv_cache_frames": {"persistent": 6, "local": 12, "current": 3}, "top_k_blocks": k_top,
-            "parallelism": f"batch/head-partitioned x{n_gpus}, no data-path collective",
+            "parallelism": (f"head-partitioned x{n_gpus} (unit e*12+h on rank (e*12+h) % {n_gpus}); one NCCL "
+                            "all-to-all of O per call to the batch element's rank" if n_gpus > 1
+                            else "single GPU, 12 head units"),
             "l2": "inputs larger than L2: KV slot pool 215 MB per GPU (> 126 MB L2), fresh Q/K/V per call"}
 
 
@@ -189,6 +194,13 @@ def run_ours(args, rank, world, local_rank):
     nq = bpc * b
     peaks = load_peaks()
 
+    from paper_2604_21221_b200.parallel import HeadLayout
+    # PBSA_BENCH_FORCE_LAYOUT=1 runs the N>1 exchange code path at N=1 (single-GPU check of the
+    # head-partitioned step; the all-to-all degenerates to a local copy)
+    force = os.environ.get("PBSA_BENCH_FORCE_LAYOUT") == "1"
+    lay = HeadLayout(world, U, world, rank) if (world > 1 or force) else None
+    if lay is not None:
+        assert lay.n_local == U  # global batch = world: 12 head units per rank
     mem = pb.Memory(U, C, W, bpc, b, d)
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
 
@@ -199,11 +211,31 @@ def run_ours(args, rank, world, local_rank):
     n_sets = 2 * (T + 1)  # two chunks' worth of fresh Q/K/V, rotated
     sets = [inputs() for _ in range(n_sets)]
     out = torch.empty(U, nq, d, device=dev, dtype=torch.bfloat16)
+    outs2 = [torch.empty(U, nq, d, device=dev, dtype=torch.bfloat16) for _ in range(2)]
+    gathered = torch.empty(U, nq, d, device=dev, dtype=torch.bfloat16)
+    pending = [None, None]  # (work, finish) of the all-to-all reading outs2[i]
 
     def chunk_step(i):
         for j in range(T + 1):
             q, kk, vv = sets[(i * (T + 1) + j) % n_sets]
-            mem.attend_qkv(q, kk, vv, k_top, pb.MODE_CACHE_UPDATE if j == T else pb.MODE_DENOISE, out=out)
+            mode = pb.MODE_CACHE_UPDATE if j == T else pb.MODE_DENOISE
+            if lay is None:
+                mem.attend_qkv(q, kk, vv, k_top, mode, out=out)
+                continue
+            o = outs2[j & 1]
+            if pending[j & 1] is not None:  # the exchange still reading this buffer
+                pending[j & 1][0].wait()
+                pending[j & 1][1]()
+                pending[j & 1] = None
+            mem.attend_qkv(q, kk, vv, k_top, mode, out=o)
+            pending[j & 1] = lay.exchange(o, out=gathered, async_op=True)
+
+    def drain():
+        for i in range(2):
+            if pending[i] is not None:
+                pending[i][0].wait()
+                pending[i][1]()
+                pending[i] = None
 
     # fill the memory to steady state (sinks + full dynamic set + full window), untimed
     i = 0
@@ -217,6 +249,7 @@ def run_ours(args, rank, world, local_rank):
         i += 1
     for w in range(args.warmup):
         chunk_step(w)
+    drain()
     torch.cuda.synchronize()
 
     inf = mem.info()
@@ -244,6 +277,7 @@ def run_ours(args, rank, world, local_rank):
     e0.record(stream)
     for s in range(args.steps):
         chunk_step(s)
+    drain()  # the timed region ends after the last output exchange
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -309,6 +343,8 @@ def run_ours(args, rank, world, local_rank):
                     stream.wait_event(copied[i])  # outs[i] has been read back
                 mem.attend_qkv(dq, dk, dv, k_top, pb.MODE_CACHE_UPDATE if j == T else pb.MODE_DENOISE,
                                out=outs[i])
+                if lay is not None:  # every head of this rank's batch element, then D2H of that
+                    outs[i].copy_(lay.exchange(outs[i]))
                 done = torch.cuda.Event()
                 done.record(stream)
                 cs.wait_event(done)
@@ -334,7 +370,8 @@ def run_ours(args, rank, world, local_rank):
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e,
                "steps": e2e_steps, "api": "paper_2604_21221_b200.Memory.attend_qkv "
                "(-> pbsa_attend_qkv) with pinned host Q/K/V in (compute stream, per call) "
-               "and O out (copy stream, overlapping the next call)"}
+               "and O out (copy stream, overlapping the next call)"
+               + ("; N>1: O all-to-all to the batch element's rank before the read-back" if lay else "")}
     clk = clocks.stop()
 
     # ---------------------------------------------------------------- CPU baseline (rank 0, N=1)
