@@ -10,13 +10,13 @@
 // selected indices and s_t are bit-exact with oracle/pbsa_oracle.cpp.  The only transcendental
 // is the fp64 exp; see DESIGN.md "bit-exactness" for the residual-risk argument.
 //
-// Two kernels:
-//   score_select_kernel  CTA = unit x up to 8 query-block rows.  Phase 1: logits, thread per key
-//                        block (fp64 query reps in smem, each key element converted once).
-//                        Phase 2: warp per row: softmax (fp64 exp, sequential ascending denominator
-//                        on lane 0 exactly like the oracle), 4-pass 8-bit radix select on the fp32
-//                        probability bits, ballot compaction of the winners
+// Kernels (short/medium key lists, e.g. config 2):
+//   logits_rm_kernel     thread per key block x 8 query rows, ascending-c fp64 dot products
+//   row_select_kernel    warp per row: softmax (fp64 exp, sequential ascending denominator on lane 0
+//                        exactly like the oracle), 4-pass 8-bit radix select on the fp32 probability
+//                        bits, ballot compaction of the winners; A_t rows at the k=0 pass
 //   aggregate_kernel     thread per key block, ascending-row fp64 column sums (k=0 pass only)
+// and a key-major variant for long windows (config 5) below.
 #include <cfloat>
 
 #include "internal.h"
@@ -38,7 +38,8 @@ __device__ void warp_softmax(const float* z, int n, double* e, uint32_t* out_bit
     for (int j = lane; j < n; j += 32) m = fmaxf(m, z[j]);
     m = warp_max(m);
     const double dm = static_cast<double>(m);
-    for (int j = lane; j < n; j += 32) e[j] = exp(static_cast<double>(z[j]) - dm);
+#pragma unroll 4
+    for (int j = lane; j < n; j += 32) e[j] = exp(static_cast<double>(z[j]) - dm);  // independent: 4 in flight
     __syncwarp();
     double denom = 0.0;
     if (lane == 0) {  // ascending-j fp64 accumulation, exactly as tensor.cpp:96-102
@@ -60,6 +61,7 @@ __device__ void warp_softmax(const float* z, int n, double* e, uint32_t* out_bit
         for (; j < n; ++j) denom = __dadd_rn(denom, e[j]);
     }
     denom = __shfl_sync(0xffffffffu, denom, 0);
+#pragma unroll 4
     for (int j = lane; j < n; j += 32) {
         const float p = __double2float_rn(__ddiv_rn(e[j], denom));
         if (out_bits) out_bits[j] = __float_as_uint(p);
@@ -157,67 +159,136 @@ struct ScoreParams {
 
 constexpr int kMaxRows = 8;
 
-// One CTA = one unit x up to 8 query-block rows.  Phase 1 (all 256 threads): coarse logits of the
-// rows against every key block, thread per key, ascending-k fp64 dot products -- the query reps are
-// converted to fp64 once into shared memory and each key element once, so the DFMA chains are not
-// starved by float->double conversions.  Phase 2 (warp per row): softmax, Top-K, optional A_t row.
+// ---------------------------------------------------------------------------------------------
+// Short/medium key lists (config 2: 312 / 546 keys): two launches with full-machine parallelism.
+//   logits_rm_kernel  CTA = unit x 8 query rows x 32 keys; the key tile is staged once in shared
+//                     memory as fp64 (transposed, key index fastest) and the 8 query rows as fp64;
+//                     warp = row, lane = key: one ascending-c fp64 dot product per thread.
+//                     Row-major logits z[U][nqb][n_keys] go to the workspace (L2-resident).
+//   row_select_kernel warp per row: the oracle's softmax + radix Top-K (+ the full-row A_t of the
+//                     k=0 pass) straight from z.
+constexpr int kLogitKeys = 128;  // keys (= threads) per CTA
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst))),
+                 "l"(gsrc)
+                 : "memory");
+}
+
+// Thread = key, 8 query rows per thread (8 independent ascending-c fp64 chains, each key element
+// converted once).  The CTA's 128 key rows are staged with cp.async into shared memory, 16-byte
+// chunk c4 of key j stored at chunk c4 ^ (j & 7): the staging stores and the per-thread LDS.128
+// row reads are both bank-conflict free.  Query rows are fp64 broadcasts.
 template <int D>
-__global__ void __launch_bounds__(256) score_select_kernel(const ScoreParams p) {
+__global__ void __launch_bounds__(kLogitKeys) logits_rm_kernel(const ScoreParams p, float* __restrict__ z) {
     extern __shared__ __align__(16) uint8_t smem[];
-    const int tid = threadIdx.x, warp = tid / 32, lane = tid & 31;
-    const int u = blockIdx.y, i0 = blockIdx.x * p.rows;
-    const int nr = min(p.rows, p.nqb - i0);
-    const int n = p.n_keys;
-    double* qd = reinterpret_cast<double*>(smem);                 // [kMaxRows][D]
-    uint8_t* rows_base = smem + static_cast<size_t>(kMaxRows) * D * 8;
-    for (int e = tid; e < kMaxRows * D; e += blockDim.x) {
-        const int r = e / D, c = e % D;
-        qd[e] = r < nr ? static_cast<double>(p.qc[(static_cast<int64_t>(u) * p.nqb + i0 + r) * D + c]) : 0.0;
+    double* qs = reinterpret_cast<double*>(smem);                            // [kMaxRows][D]
+    float4* ks = reinterpret_cast<float4*>(smem + kMaxRows * D * 8);         // [kLogitKeys][D/4] swizzled
+    constexpr int C4 = D / 4;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int u = blockIdx.z, i0 = blockIdx.y * kMaxRows, j0 = blockIdx.x * kLogitKeys;
+    const int nr = min(kMaxRows, p.nqb - i0);
+    const int nk = min(kLogitKeys, p.n_keys - j0);
+    // every load is issued before any is waited on: slot ids (one per thread), then the key rows
+    // (warp w copies rows w, w+4, ...) and the query rows
+    const int my_slot = tid < nk ? __ldg(p.keys + static_cast<int64_t>(u) * p.key_stride + j0 + tid) : 0;
+    {
+        __shared__ int slots[kLogitKeys];
+        slots[tid] = my_slot;
+        __syncthreads();
+#pragma unroll 4
+        for (int kk = warp; kk < nk; kk += kLogitKeys / 32) {
+            const float4* kr = reinterpret_cast<const float4*>(p.krep + u * p.kru + static_cast<int64_t>(slots[kk]) * D);
+            for (int c4 = lane; c4 < C4; c4 += 32) cp_async16(ks + kk * C4 + (c4 ^ (kk & 7)), kr + c4);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    __syncthreads();
-    for (int j = tid; j < n; j += blockDim.x) {
-        const int slot = __ldg(p.keys + static_cast<int64_t>(u) * p.key_stride + j);
-        const float4* kr = reinterpret_cast<const float4*>(p.krep + u * p.kru + static_cast<int64_t>(slot) * D);
-        double acc[kMaxRows];
+    {
+        constexpr int Q4 = kMaxRows * D / 4;
+        float4 qv[Q4 / kLogitKeys];
 #pragma unroll
-        for (int r = 0; r < kMaxRows; ++r) acc[r] = 0.0;
-#pragma unroll 2
-        for (int c4 = 0; c4 < D / 4; ++c4) {
-            const float4 kv = __ldg(kr + c4);
-            const double k0 = kv.x, k1 = kv.y, k2 = kv.z, k3 = kv.w;
-#pragma unroll
-            for (int r = 0; r < kMaxRows; ++r) {  // ascending c per row; fp32 x fp32 is exact in fp64
-                const double* q = qd + r * D + 4 * c4;
-                acc[r] = __fma_rn(q[0], k0, acc[r]);
-                acc[r] = __fma_rn(q[1], k1, acc[r]);
-                acc[r] = __fma_rn(q[2], k2, acc[r]);
-                acc[r] = __fma_rn(q[3], k3, acc[r]);
-            }
+        for (int t = 0; t < Q4 / kLogitKeys; ++t) {
+            const int e4 = tid + t * kLogitKeys, r = (e4 * 4) / D;
+            qv[t] = r < nr ? __ldg(reinterpret_cast<const float4*>(p.qc + (static_cast<int64_t>(u) * p.nqb + i0) * D) + e4)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
-        for (int r = 0; r < kMaxRows; ++r)
-            if (r < nr) {
-                float* z = reinterpret_cast<float*>(rows_base + p.per_warp * r + static_cast<size_t>(n) * 8);
-                z[j] = __fmul_rn(__double2float_rn(acc[r]), p.scale);
-            }
+        for (int t = 0; t < Q4 / kLogitKeys; ++t) {
+            const int e4 = tid + t * kLogitKeys;
+            qs[4 * e4] = qv[t].x;
+            qs[4 * e4 + 1] = qv[t].y;
+            qs[4 * e4 + 2] = qv[t].z;
+            qs[4 * e4 + 3] = qv[t].w;
+        }
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
-    if (warp >= nr) return;
-    const int64_t row = static_cast<int64_t>(u) * p.nqb + i0 + warp;
-    uint8_t* base = rows_base + p.per_warp * warp;
+    if (tid >= nk) return;
+    double acc[kMaxRows];
+#pragma unroll
+    for (int r = 0; r < kMaxRows; ++r) acc[r] = 0.0;
+    const float4* krow = ks + tid * C4;
+#pragma unroll 2
+    for (int c4 = 0; c4 < C4; ++c4) {
+        const float4 kv = krow[c4 ^ (tid & 7)];
+        const double k0 = kv.x, k1 = kv.y, k2 = kv.z, k3 = kv.w;
+#pragma unroll
+        for (int r = 0; r < kMaxRows; ++r) {  // ascending c per row; fp32 x fp32 is exact in fp64
+            const double2 qa = *reinterpret_cast<const double2*>(qs + r * D + 4 * c4);
+            const double2 qb = *reinterpret_cast<const double2*>(qs + r * D + 4 * c4 + 2);
+            acc[r] = __fma_rn(qa.x, k0, acc[r]);
+            acc[r] = __fma_rn(qa.y, k1, acc[r]);
+            acc[r] = __fma_rn(qb.x, k2, acc[r]);
+            acc[r] = __fma_rn(qb.y, k3, acc[r]);
+        }
+    }
+    const int64_t zr = (static_cast<int64_t>(u) * p.nqb + i0) * p.n_keys + j0 + tid;
+#pragma unroll
+    for (int r = 0; r < kMaxRows; ++r)
+        if (r < nr) z[zr + static_cast<int64_t>(r) * p.n_keys] = __fmul_rn(__double2float_rn(acc[r]), p.scale);
+}
+
+// split = 2 (k=0 pass with selection): warps w and w+4 share row w -- one runs the local-window
+// softmax + Top-K, the other the full-row softmax (A_t): the two sequential fp64 denominators run
+// concurrently instead of back to back.
+template <int SPLIT>
+__global__ void __launch_bounds__(256) row_select_kernel(const ScoreParams p, const float* __restrict__ z) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int kRowsPerCta = kMaxRows / SPLIT;
+    const int role = SPLIT == 2 ? warp / kRowsPerCta : 0;  // 0: selection (and A_t if SPLIT == 1), 1: A_t
+    const int64_t row = static_cast<int64_t>(blockIdx.x) * kRowsPerCta + warp % kRowsPerCta;
+    if (row >= static_cast<int64_t>(p.units) * p.nqb) return;
+    const int n = p.n_keys;
+    uint8_t* base = smem + p.per_warp * warp;
     double* e = reinterpret_cast<double*>(base);
-    float* z = reinterpret_cast<float*>(base + static_cast<size_t>(n) * 8);
-    uint32_t* pb = reinterpret_cast<uint32_t*>(base + static_cast<size_t>(n) * 12);
+    float* zr = reinterpret_cast<float*>(base + static_cast<size_t>(n) * 8);
+    uint32_t* pb = reinterpret_cast<uint32_t*>(zr + ((n + 3) & ~3));
     uint32_t* hist = pb + p.n_local;
+    // the row's logits into shared memory (all loads in flight at once; rows are n*4 bytes apart,
+    // 16-byte aligned when n % 4 == 0)
+    const float* zg = z + row * n;
     bool bad = false;
-    for (int j = lane; j < n; j += 32) bad |= z[j] != z[j];
-    if (p.status != nullptr && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(p.status, 1);
+    if ((n & 3) == 0) {
+        const float4* z4 = reinterpret_cast<const float4*>(zg);
+        float4* s4 = reinterpret_cast<float4*>(zr);
+#pragma unroll 4
+        for (int j = lane; j < n / 4; j += 32) s4[j] = __ldg(z4 + j);
+    } else {
+#pragma unroll 4
+        for (int j = lane; j < n; j += 32) zr[j] = __ldg(zg + j);
+    }
     __syncwarp();
-    if (p.k > 0 && p.n_local > 0) {
-        warp_softmax(z + p.local_off, p.n_local, e, pb, nullptr);
+    for (int j = lane; j < n; j += 32) {
+        const float v = zr[j];
+        bad |= v != v;
+    }
+    if (p.status != nullptr && role == 0 && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(p.status, 1);
+    if (role == 0 && p.k > 0 && p.n_local > 0) {
+        warp_softmax(zr + p.local_off, p.n_local, e, pb, nullptr);
         warp_topk(pb, p.n_local, p.k, hist, p.sel + row * p.k);
     }
-    if (p.arows != nullptr) warp_softmax(z, n, e, nullptr, p.arows + row * n);
+    if (p.arows != nullptr && (SPLIT == 1 || role == 1)) warp_softmax(zr, n, e, nullptr, p.arows + row * n);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -468,18 +539,33 @@ int launch_score_select(const float* qc, const float* krep, int64_t kru, const i
                 if (int rc = softmax_rows(0, n_keys, arows, do_select ? nullptr : status)) return rc;
             }
         } else {
-        const size_t smem = qbytes + per_warp * rows;
-        dim3 grid((nqb + rows - 1) / rows, units);
-        if (d == 128) {
-            if (int rc = ensure_smem(reinterpret_cast<const void*>(score_select_kernel<128>), smem, "score_select"))
-                return rc;
-            score_select_kernel<128><<<grid, 256, smem, s>>>(p);
-        } else {
-            if (int rc = ensure_smem(reinterpret_cast<const void*>(score_select_kernel<64>), smem, "score_select"))
-                return rc;
-            score_select_kernel<64><<<grid, 256, smem, s>>>(p);
-        }
-        if (int rc = check_launch("score_select_kernel")) return rc;
+            // row-major logits into the workspace (after the A_t rows), then warp-per-row select
+            const int64_t rt = static_cast<int64_t>(units) * nqb;
+            float* z = static_cast<float*>(ws) + static_cast<size_t>(rt) * n_keys;
+            dim3 g1((n_keys + kLogitKeys - 1) / kLogitKeys, (nqb + kMaxRows - 1) / kMaxRows, units);
+            const size_t lsmem = static_cast<size_t>(kMaxRows) * d * 8 + static_cast<size_t>(kLogitKeys) * d * 4;
+            if (d == 128) {
+                if (int rc = ensure_smem(reinterpret_cast<const void*>(logits_rm_kernel<128>), lsmem, "logits_rm"))
+                    return rc;
+                logits_rm_kernel<128><<<g1, kLogitKeys, lsmem, s>>>(p, z);
+            } else {
+                if (int rc = ensure_smem(reinterpret_cast<const void*>(logits_rm_kernel<64>), lsmem, "logits_rm"))
+                    return rc;
+                logits_rm_kernel<64><<<g1, kLogitKeys, lsmem, s>>>(p, z);
+            }
+            if (int rc = check_launch("logits_rm_kernel")) return rc;
+            p.per_warp = (static_cast<size_t>(n_keys) * 12 + 16 + static_cast<size_t>(n_local) * 4 + 1024 + 15) & ~size_t(15);
+            const size_t smem = p.per_warp * kMaxRows;
+            if (do_select && arows != nullptr) {
+                if (int rc = ensure_smem(reinterpret_cast<const void*>(row_select_kernel<2>), smem, "row_select"))
+                    return rc;
+                row_select_kernel<2><<<static_cast<unsigned>((rt + kMaxRows / 2 - 1) / (kMaxRows / 2)), 256, smem, s>>>(p, z);
+            } else {
+                if (int rc = ensure_smem(reinterpret_cast<const void*>(row_select_kernel<1>), smem, "row_select"))
+                    return rc;
+                row_select_kernel<1><<<static_cast<unsigned>((rt + kMaxRows - 1) / kMaxRows), 256, smem, s>>>(p, z);
+            }
+            if (int rc = check_launch("row_select_kernel")) return rc;
         }
     }
     if (s_t) {
