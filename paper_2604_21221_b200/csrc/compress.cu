@@ -10,6 +10,7 @@
 // 256-byte (d=128) warp load; rows are unrolled 4-deep for memory-level parallelism.  The fp64
 // adds (one per element) stay far below the DADD rate at HBM speed.
 #include "internal.h"
+#include "ptx.cuh"
 
 namespace pbsa {
 namespace {
@@ -156,6 +157,60 @@ __global__ void __launch_bounds__(256) write_chunk_kernel(const bf16* __restrict
     }
 }
 
+// Bulk-copy form of write_chunk_kernel (the fused ingest, one PBSA call's Q/K/V pass): CTA per
+// block.  One thread moves the block's b contiguous K, V (and Q) rows into shared memory with 1-D
+// TMA bulk copies (b*d*2 bytes each, one mbarrier), streams K and V back out to the pool slot with
+// two bulk stores, while thread c sums column c of K (threads d..2d-1: of Q) over the b rows in
+// ascending token order in fp64 -- the same numerics as compress_kernel.  ~45 KB in flight per CTA
+// instead of a few KB of warp loads: this kernel runs at HBM speed at config 2 and config 5.
+template <int D, bool WITH_Q>
+__global__ void __launch_bounds__(2 * D) write_chunk_bulk_kernel(const bf16* __restrict__ kc,
+                                                                 const bf16* __restrict__ vc,
+                                                                 const bf16* __restrict__ qcur,
+                                                                 const int32_t* __restrict__ stage, int bpc, int b,
+                                                                 int units, int n_slots, bf16* __restrict__ kp,
+                                                                 bf16* __restrict__ vp, float* __restrict__ krep,
+                                                                 float* __restrict__ qrep) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ __align__(8) uint64_t bar;
+    const int tid = threadIdx.x;
+    const int u = blockIdx.x / bpc, i = blockIdx.x % bpc;
+    const int slot = __ldg(stage + static_cast<int64_t>(u) * bpc + i);
+    const uint32_t bytes = static_cast<uint32_t>(b) * D * 2;
+    const int64_t src_off = (static_cast<int64_t>(u) * bpc + i) * b * D;
+    const int64_t dst_off = (static_cast<int64_t>(u) * n_slots + slot) * 64 * D;
+    bf16* ks = reinterpret_cast<bf16*>(smem);
+    bf16* vs = reinterpret_cast<bf16*>(smem + bytes);
+    bf16* qs = reinterpret_cast<bf16*>(smem + 2 * bytes);
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        fence_barrier_init();
+        mbar_arrive_expect_tx(&bar, (WITH_Q ? 3u : 2u) * bytes);
+        bulk_g2s(ks, kc + src_off, bytes, &bar);
+        bulk_g2s(vs, vc + src_off, bytes, &bar);
+        if (WITH_Q) bulk_g2s(qs, qcur + src_off, bytes, &bar);
+    }
+    __syncthreads();
+    mbar_wait(&bar, 0);
+    if (tid == 0) {  // K and V rows [0, b) of the slot; rows >= b stay zero
+        bulk_s2g(kp + dst_off, ks, bytes);
+        bulk_s2g(vp + dst_off, vs, bytes);
+        bulk_commit();
+    }
+    const int c = tid % D;
+    const bool is_q = tid >= D;
+    if (!is_q || WITH_Q) {
+        const bf16* col = (is_q ? qs : ks) + c;
+        double acc = 0.0;
+#pragma unroll 4
+        for (int t = 0; t < b; ++t) acc += static_cast<double>(__bfloat162float(col[t * D]));
+        const double r = __ddiv_rn(acc, static_cast<double>(b));
+        if (is_q) qrep[(static_cast<int64_t>(u) * bpc + i) * D + c] = __double2float_rn(r);
+        else krep[(static_cast<int64_t>(u) * n_slots + slot) * D + c] = __double2float_rn(r);
+    }
+    if (tid == 0) bulk_wait_read0();  // shared memory must outlive the bulk stores' reads
+}
+
 }  // namespace
 
 int launch_compress(const bf16* x, int64_t xu, int64_t xb, const int32_t* map, int nb, int units,
@@ -175,6 +230,25 @@ int launch_write_chunk(const bf16* kc, const bf16* vc, const bf16* q, const int3
                        cudaStream_t s) {
     const int64_t warps = static_cast<int64_t>(bpc) * units;
     if (warps == 0) return 0;
+    const size_t smem = (q ? 3 : 2) * static_cast<size_t>(b) * d * 2;
+    if (smem <= 200 * 1024 && warps < (int64_t(1) << 31)) {
+#define PBSA_WCB(DD, WQ)                                                                                        \
+    do {                                                                                                         \
+        if (int rc = ensure_smem(reinterpret_cast<const void*>(write_chunk_bulk_kernel<DD, WQ>), smem,          \
+                                 "write_chunk"))                                                                 \
+            return rc;                                                                                           \
+        write_chunk_bulk_kernel<DD, WQ><<<static_cast<int>(warps), 2 * DD, smem, s>>>(kc, vc, q, stage, bpc, b, \
+                                                                                      units, n_slots, kp, vp,   \
+                                                                                      krep, qrep);              \
+    } while (0)
+        if (d == 128) {
+            if (q) PBSA_WCB(128, true); else PBSA_WCB(128, false);
+        } else {
+            if (q) PBSA_WCB(64, true); else PBSA_WCB(64, false);
+        }
+#undef PBSA_WCB
+        return check_launch("write_chunk_bulk_kernel");
+    }
     const int grid = static_cast<int>((warps + 7) / 8);
 #define PBSA_WC(DD, WQ) write_chunk_kernel<DD, WQ><<<grid, 256, 0, s>>>(kc, vc, q, stage, bpc, b, units, n_slots, kp, vp, krep, qrep)
     if (d == 128) {
