@@ -131,6 +131,27 @@ int pbsa_mem_status(const pbsa_mem* m, int* flags, void* stream);
  * slots and compresses K and Q (K1), then K2 -> K3 (-> K4) as pbsa_attend. */
 int pbsa_attend_qkv(pbsa_mem* m, const void* q, const void* k_chunk, const void* v_chunk, int k_top,
                     float scale, int mode, void* o, float* lse, void* stream);
+/* Chunk latents in the reference's Latent4D layout (proj/include/pbsa/tensor.hpp:30-47: (t, h, w, d)
+ * row-major, d = heads * head_dim), one per batch element: [batch][T][H][W][heads*d]
+ * bf16, blocked by blockify's (B_t, B_h, B_w) (proj/include/pbsa/blockify.hpp:11-67; block id
+ * (nt*N_h + nh)*N_w + nw, in-block index (dt*B_h + dh)*B_w + dw).  Unit u = e*heads + h. */
+typedef struct pbsa_latent_geom {
+    int batch, t, h, w, heads, head_dim, block_t, block_h, block_w;
+} pbsa_latent_geom;
+/* Host-only validation (no device work): the make_block_layout checks of blockify.cpp:7-36
+ * (non-divisible axis -> PBSA_EINVAL naming the axis) plus the library's limits; returns the
+ * blocks per chunk and tokens per block. */
+int pbsa_latent_blocks(const pbsa_latent_geom* g, int* blocks_per_chunk, int* block_tokens);
+/* pbsa_attend_qkv on chunk latents: the ingest gathers each (head, block) with one 5-D TMA box
+ * (blockify fused), K3 loads Q blocks the same way and writes O rows straight back to their latent
+ * positions (unblockify fused).  q, k_lat, v_lat, o: [batch][T][H][W][heads*d] bf16 with
+ * batch*heads == units, T*H*W == blocks_per_chunk * b of the memory; lse (nullable) stays
+ * [units][n_q] in block order.  Results are bit-identical to pbsa_attend_qkv on the blockified
+ * per-head tensors. */
+int pbsa_attend_latent(pbsa_mem* m, const void* q, const void* k_lat, const void* v_lat,
+                       const pbsa_latent_geom* g, int k_top, float scale, int mode, void* o, float* lse,
+                       void* stream);
+
 /* last selection of pbsa_attend (device): [units][blocks_per_chunk][k] ascending, and last s_t */
 int pbsa_last_selection(const pbsa_mem* m, const int32_t** sel, int* k, const float** s_t,
                         int* n_keys);

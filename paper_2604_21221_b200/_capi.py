@@ -31,6 +31,12 @@ class MemInfo(C.Structure):
     ]
 
 
+class LatentGeom(C.Structure):
+    """pbsa_latent_geom: chunk latents [batch][T][H][W][heads*head_dim] blocked by (B_t, B_h, B_w)."""
+    _fields_ = [("batch", _i32), ("t", _i32), ("h", _i32), ("w", _i32), ("heads", _i32),
+                ("head_dim", _i32), ("block_t", _i32), ("block_h", _i32), ("block_w", _i32)]
+
+
 _SIGS = {
     "pbsa_last_error": (C.c_char_p, []),
     "pbsa_version": (_i32, []),
@@ -49,6 +55,8 @@ _SIGS = {
     "pbsa_mem_commit": (_i32, [_vp, _vp, _vp]),
     "pbsa_attend": (_i32, [_vp, _vp, _i32, _f32, _i32, _vp, _vp, _vp]),
     "pbsa_attend_qkv": (_i32, [_vp, _vp, _vp, _vp, _i32, _f32, _i32, _vp, _vp, _vp]),
+    "pbsa_latent_blocks": (_i32, [C.POINTER(LatentGeom), C.POINTER(_i32), C.POINTER(_i32)]),
+    "pbsa_attend_latent": (_i32, [_vp, _vp, _vp, _vp, C.POINTER(LatentGeom), _i32, _f32, _i32, _vp, _vp, _vp]),
     "pbsa_last_selection": (_i32, [_vp, C.POINTER(_vp), C.POINTER(_i32), C.POINTER(_vp),
                                    C.POINTER(_i32)]),
     "pbsa_mem_profile": (_i32, [_vp, _i32, _i32]),

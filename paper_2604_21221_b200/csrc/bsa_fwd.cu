@@ -61,6 +61,8 @@ struct BsaParams {
     float* lse;
     float scale_log2;
     int max_list, bm_words;
+    int lat;        // q / o are chunk latents (LatentGeom lg), not block-major [units][n_q][d]
+    LatentGeom lg;
     long long* trace;  // perf experiments only: per-event clock64 stamps of CTA 0 (null = off)
     int ablate;  // perf experiments only (PBSA_ABLATE): 1 no softmax math, 2 no K/V loads, 3 no MMAs
     // schedule: `whole_waves` rounds of one whole tile per CTA (tile = cta + w * grid), then the
@@ -296,9 +298,18 @@ __global__ void __launch_bounds__(kThreads, 2)
                     if (elect_one()) {
                         mbar_arrive_expect_tx(q_full, qbytes);
                         for (int r = 0; r < (fm.has2 ? 2 : 1); ++r)
-                            for (int h = 0; h < L::kHalves; ++h)
-                                tma_load_3d(q_smem + h * 16384 + r * 8192, &tm_q, q_full, h * 64, 0,
-                                            fm.u * p.nqb + fm.qb0 + r);
+                            for (int h = 0; h < L::kHalves; ++h) {
+                                if (p.lat) {  // the query block is one 5-D box of the latent (blockify)
+                                    const int qb = fm.qb0 + r, e = fm.u / p.lg.heads, hd = fm.u % p.lg.heads;
+                                    const int nw = qb % p.lg.nw(), nh = (qb / p.lg.nw()) % p.lg.nh();
+                                    const int nt = qb / (p.lg.nw() * p.lg.nh());
+                                    tma_load_5d(q_smem + h * 16384 + r * 8192, &tm_q, q_full, hd * D + h * 64,
+                                                nw * p.lg.bw, nh * p.lg.bh, nt * p.lg.bt, e);
+                                } else {
+                                    tma_load_3d(q_smem + h * 16384 + r * 8192, &tm_q, q_full, h * 64, 0,
+                                                fm.u * p.nqb + fm.qb0 + r);
+                                }
+                            }
                     }
                     __syncwarp();
                     ++q_uses;
@@ -565,9 +576,19 @@ __global__ void __launch_bounds__(kThreads, 2)
 
             // ---------------------------------------------------------- epilogue
             const int64_t orow_idx = (static_cast<int64_t>(u) * p.nqb + qb) * p.b + rr;
+            // output row: block-major, or (unblockify fused) the token's position in the latent
+            int64_t orow_off = orow_idx * D;
+            if (p.lat) {
+                const int e = u / p.lg.heads, hd = u % p.lg.heads;
+                const int nw = qb % p.lg.nw(), nh = (qb / p.lg.nw()) % p.lg.nh(), nt = qb / (p.lg.nw() * p.lg.nh());
+                const int dw = rr % p.lg.bw, dh = (rr / p.lg.bw) % p.lg.bh, dt = rr / (p.lg.bw * p.lg.bh);
+                const int64_t tok = ((static_cast<int64_t>(e) * p.lg.T + nt * p.lg.bt + dt) * p.lg.H + nh * p.lg.bh + dh) *
+                                        p.lg.W + nw * p.lg.bw + dw;
+                orow_off = (tok * p.lg.heads + hd) * D;
+            }
             if (fm.whole) {
                 const float inv = l > 0.0f ? 1.0f / l : 0.0f;
-                bf16* orow = p.o + orow_idx * D;
+                bf16* orow = p.o + orow_off;
 #pragma unroll 1
                 for (int c0 = 0; c0 < D; c0 += 32) {
                     uint32_t ov[32];
@@ -646,7 +667,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                     }
                     const float inv = Ls > 0.0f ? 1.0f / Ls : 0.0f;
                     if (valid) {
-                        bf16* orow = p.o + orow_idx * D;
+                        bf16* orow = p.o + orow_off;
 #pragma unroll 1
                         for (int c0 = 0; c0 < D; c0 += 8) {
                             float acc8[8];
@@ -701,7 +722,10 @@ int launch_impl(const bf16* q, const bf16* kp, const bf16* vp, BsaParams p, cuda
     using L = Layout<D, NSK, NSV>;
     alignas(64) CUtensorMap tq, tk, tv;
     std::string err;
-    {
+    if (p.lat) {
+        if (!encode_latent_tmap(&tq, q, p.lg, 64, true, &err))
+            return set_error(PBSA_ECUDA, "tensor map Q (latent): " + err);
+    } else {
         const uint64_t dims[3] = {static_cast<uint64_t>(D), static_cast<uint64_t>(p.b),
                                   static_cast<uint64_t>(p.units) * p.nqb};
         const uint64_t strides[2] = {static_cast<uint64_t>(D) * 2, static_cast<uint64_t>(p.b) * D * 2};
@@ -766,8 +790,11 @@ namespace pbsa {
 int launch_bsa_fwd(const bf16* q, const bf16* k_pool, const bf16* v_pool, int n_slots,
                    const int32_t* dense, int dense_stride, int n_dense, const int32_t* local,
                    int local_stride, int n_local, const int32_t* sel, int k, int nqb, int b, int d,
-                   int units, float scale, bf16* o, float* lse, void* ws, size_t ws_bytes, cudaStream_t s) {
+                   int units, float scale, bf16* o, float* lse, void* ws, size_t ws_bytes, cudaStream_t s,
+                   const LatentGeom* lat) {
     BsaParams p{};
+    p.lat = lat != nullptr;
+    if (lat) p.lg = *lat;
     p.units = units;
     p.nqb = nqb;
     p.b = b;

@@ -48,8 +48,9 @@ int check_launch(const char* what) {
     return PBSA_OK;
 }
 
-bool encode_tmap_bf16(void* tmap, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
-                      const uint32_t* box, std::string* err) {
+namespace {
+bool encode_tmap_impl(void* tmap, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                      const uint32_t* box, bool swizzle128, std::string* err) {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     static std::once_flag once;
     std::call_once(once, [] {
@@ -73,13 +74,31 @@ bool encode_tmap_bf16(void* tmap, const void* base, int rank, const uint64_t* di
     }
     const CUresult r = fn(reinterpret_cast<CUtensorMap*>(tmap), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
                           static_cast<cuuint32_t>(rank), const_cast<void*>(base), gd, gs, bx, es,
-                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
         *err = "cuTensorMapEncodeTiled failed (CUresult " + std::to_string(static_cast<int>(r)) + ")";
         return false;
     }
     return true;
+}
+}  // namespace
+
+bool encode_tmap_bf16(void* tmap, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                      const uint32_t* box, std::string* err) {
+    return encode_tmap_impl(tmap, base, rank, dims, strides, box, true, err);
+}
+
+bool encode_latent_tmap(void* tmap, const void* base, const LatentGeom& g, int box_d, bool swizzle128,
+                        std::string* err) {
+    const uint64_t row = static_cast<uint64_t>(g.heads) * g.d;
+    const uint64_t dims[5] = {row, static_cast<uint64_t>(g.W), static_cast<uint64_t>(g.H),
+                              static_cast<uint64_t>(g.T), static_cast<uint64_t>(g.batch)};
+    const uint64_t strides[4] = {row * 2, row * 2 * g.W, row * 2 * g.W * g.H, row * 2 * g.W * g.H * g.T};
+    const uint32_t box[5] = {static_cast<uint32_t>(box_d), static_cast<uint32_t>(g.bw), static_cast<uint32_t>(g.bh),
+                             static_cast<uint32_t>(g.bt), 1u};
+    return encode_tmap_impl(tmap, base, 5, dims, strides, box, swizzle128, err);
 }
 
 }  // namespace pbsa
@@ -452,7 +471,7 @@ int pbsa_mem_commit(pbsa_mem* m, const float* s_t, void* stream) {
 namespace {
 
 int attend_impl(pbsa_mem* m, const void* q, int k_top, float scale, int mode, void* o, float* lse, void* stream,
-                bool q_compressed) {
+                bool q_compressed, const LatentGeom* lat) {
     PBSA_REQUIRE(m != nullptr && q != nullptr && o != nullptr, "attend: null pointer");
     PBSA_REQUIRE(mode == PBSA_MODE_DENOISE || mode == PBSA_MODE_CACHE_UPDATE, "attend: unknown mode");
     PBSA_REQUIRE(k_top >= 0, "attend: k_top must be >= 0");
@@ -492,7 +511,7 @@ int attend_impl(pbsa_mem* m, const void* q, int k_top, float scale, int mode, vo
     if (int rc = launch_bsa_fwd(static_cast<const bf16*>(q), m->k_pool, m->v_pool, m->S, m->dev.dense,
                                 m->C + bpc, n_p + bpc, m->dev.l_slot, m->Lcap, n_l, m->sel, k, bpc, b, d, U,
                                 scale, static_cast<bf16*>(o), lse, use_stream_k() ? m->k3ws : nullptr,
-                                m->k3ws_bytes, s))
+                                m->k3ws_bytes, s, lat))
         return rc;
     prof_mark(m, 3, s);
     // (d) persistent-memory update after the k=0 pass
@@ -509,7 +528,59 @@ extern "C" {
 
 int pbsa_attend(pbsa_mem* m, const void* q, int k_top, float scale, int mode, void* o, float* lse,
                 void* stream) {
-    return attend_impl(m, q, k_top, scale, mode, o, lse, stream, false);
+    return attend_impl(m, q, k_top, scale, mode, o, lse, stream, false, nullptr);
+}
+
+int pbsa_latent_blocks(const pbsa_latent_geom* g, int* blocks_per_chunk, int* block_tokens) {
+    PBSA_REQUIRE(g != nullptr, "latent_blocks: null geometry");
+    PBSA_REQUIRE(g->batch >= 1 && g->t >= 1 && g->h >= 1 && g->w >= 1 && g->heads >= 1,
+                 "latent_blocks: latent dimensions must be positive");
+    PBSA_REQUIRE(g->block_t >= 1 && g->block_h >= 1 && g->block_w >= 1, "make_block_layout: block extents must be positive");
+    // blockify.cpp:7-36: every axis must divide exactly (no padding)
+    if (g->t % g->block_t != 0)
+        return set_error(PBSA_EINVAL, "make_block_layout: T (" + std::to_string(g->t) + ") not divisible by B_t (" +
+                                          std::to_string(g->block_t) + ")");
+    if (g->h % g->block_h != 0)
+        return set_error(PBSA_EINVAL, "make_block_layout: H (" + std::to_string(g->h) + ") not divisible by B_h (" +
+                                          std::to_string(g->block_h) + ")");
+    if (g->w % g->block_w != 0)
+        return set_error(PBSA_EINVAL, "make_block_layout: W (" + std::to_string(g->w) + ") not divisible by B_w (" +
+                                          std::to_string(g->block_w) + ")");
+    PBSA_REQUIRE(g->head_dim == 64 || g->head_dim == 128, "latent_blocks: head_dim must be 64 or 128");
+    const int b = g->block_t * g->block_h * g->block_w;
+    PBSA_REQUIRE(b <= 64, "latent_blocks: a block holds at most 64 tokens (one pool slot)");
+    PBSA_REQUIRE(g->block_t <= 256 && g->block_h <= 256 && g->block_w <= 256, "latent_blocks: block extent > 256");
+    if (blocks_per_chunk) *blocks_per_chunk = (g->t / g->block_t) * (g->h / g->block_h) * (g->w / g->block_w);
+    if (block_tokens) *block_tokens = b;
+    return PBSA_OK;
+}
+
+int pbsa_attend_latent(pbsa_mem* m, const void* q, const void* k_lat, const void* v_lat,
+                       const pbsa_latent_geom* g, int k_top, float scale, int mode, void* o, float* lse,
+                       void* stream) {
+    PBSA_REQUIRE(m != nullptr && q != nullptr && k_lat != nullptr && v_lat != nullptr && o != nullptr,
+                 "attend_latent: null pointer");
+    int nqb = 0, b = 0;
+    if (int rc = pbsa_latent_blocks(g, &nqb, &b)) return rc;
+    PBSA_REQUIRE(g->batch * g->heads == m->units, "attend_latent: batch * heads != memory units");
+    PBSA_REQUIRE(g->head_dim == m->d, "attend_latent: head_dim != memory head_dim");
+    PBSA_REQUIRE(b == m->b, "attend_latent: block tokens != memory block size");
+    PBSA_REQUIRE(nqb == m->bpc, "attend_latent: blocks per chunk != memory blocks_per_chunk");
+    PBSA_REQUIRE(aligned16(q) && aligned16(k_lat) && aligned16(v_lat) && aligned16(o),
+                 "attend_latent: tensors must be 16-byte aligned");
+    const LatentGeom lg{g->batch, g->t, g->h, g->w, g->heads, g->head_dim, g->block_t, g->block_h, g->block_w};
+    cudaStream_t s = as_stream(stream);
+    const bool prof = m->prof_on && m->prof_write < m->prof_max;
+    if (prof) cudaEventRecord(m->ev_write[static_cast<size_t>(m->prof_write) * 2], s);
+    if (int rc = launch_ingest_latent(static_cast<const bf16*>(k_lat), static_cast<const bf16*>(v_lat),
+                                      static_cast<const bf16*>(q), lg, m->dev.stage, m->S, m->k_pool, m->v_pool,
+                                      m->krep, m->qc, s))
+        return rc;
+    if (prof) {
+        cudaEventRecord(m->ev_write[static_cast<size_t>(m->prof_write) * 2 + 1], s);
+        ++m->prof_write;
+    }
+    return attend_impl(m, q, k_top, scale, mode, o, lse, stream, true, &lg);
 }
 
 int pbsa_attend_qkv(pbsa_mem* m, const void* q, const void* k_chunk, const void* v_chunk, int k_top,
@@ -528,7 +599,7 @@ int pbsa_attend_qkv(pbsa_mem* m, const void* q, const void* k_chunk, const void*
         cudaEventRecord(m->ev_write[static_cast<size_t>(m->prof_write) * 2 + 1], s);
         ++m->prof_write;
     }
-    return attend_impl(m, q, k_top, scale, mode, o, lse, stream, true);
+    return attend_impl(m, q, k_top, scale, mode, o, lse, stream, true, nullptr);
 }
 
 int pbsa_mem_status(const pbsa_mem* m, int* flags, void* stream) {

@@ -211,6 +211,59 @@ __global__ void __launch_bounds__(2 * D) write_chunk_bulk_kernel(const bf16* __r
     if (tid == 0) bulk_wait_read0();  // shared memory must outlive the bulk stores' reads
 }
 
+// write_chunk_bulk_kernel reading Latent4D chunk latents: the block's b tokens of head h are one
+// 5-D TMA box {d, B_w, B_h, B_t, 1} at (h*d, nw*B_w, nh*B_h, nt*B_t, e), which lands in shared
+// memory already in block-major in-block order (dt, dh, dw) -- blockify (blockify.cpp:38-65) is
+// the TMA gather itself.  Then exactly the bulk kernel's slot store and fp64 column sums.
+template <int D, bool WITH_Q>
+__global__ void __launch_bounds__(2 * D) ingest_latent_kernel(const __grid_constant__ CUtensorMap tm_k,
+                                                              const __grid_constant__ CUtensorMap tm_v,
+                                                              const __grid_constant__ CUtensorMap tm_q,
+                                                              const LatentGeom g, const int32_t* __restrict__ stage,
+                                                              int n_slots, bf16* __restrict__ kp, bf16* __restrict__ vp,
+                                                              float* __restrict__ krep, float* __restrict__ qrep) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ __align__(8) uint64_t bar;
+    const int tid = threadIdx.x;
+    const int bpc = g.nqb(), b = g.b();
+    const int u = blockIdx.x / bpc, i = blockIdx.x % bpc;
+    const int e = u / g.heads, h = u % g.heads;
+    const int nw = i % g.nw(), nh = (i / g.nw()) % g.nh(), nt = i / (g.nw() * g.nh());
+    const int slot = __ldg(stage + static_cast<int64_t>(u) * bpc + i);
+    const uint32_t bytes = static_cast<uint32_t>(b) * D * 2;
+    const int64_t dst_off = (static_cast<int64_t>(u) * n_slots + slot) * 64 * D;
+    bf16* ks = reinterpret_cast<bf16*>(smem);
+    bf16* vs = reinterpret_cast<bf16*>(smem + bytes);
+    bf16* qs = reinterpret_cast<bf16*>(smem + 2 * bytes);
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        fence_barrier_init();
+        mbar_arrive_expect_tx(&bar, (WITH_Q ? 3u : 2u) * bytes);
+        tma_load_5d(ks, &tm_k, &bar, h * D, nw * g.bw, nh * g.bh, nt * g.bt, e);
+        tma_load_5d(vs, &tm_v, &bar, h * D, nw * g.bw, nh * g.bh, nt * g.bt, e);
+        if (WITH_Q) tma_load_5d(qs, &tm_q, &bar, h * D, nw * g.bw, nh * g.bh, nt * g.bt, e);
+    }
+    __syncthreads();
+    mbar_wait(&bar, 0);
+    if (tid == 0) {
+        bulk_s2g(kp + dst_off, ks, bytes);
+        bulk_s2g(vp + dst_off, vs, bytes);
+        bulk_commit();
+    }
+    const int c = tid % D;
+    const bool is_q = tid >= D;
+    if (!is_q || WITH_Q) {
+        const bf16* col = (is_q ? qs : ks) + c;
+        double acc = 0.0;
+#pragma unroll 4
+        for (int t = 0; t < b; ++t) acc += static_cast<double>(__bfloat162float(col[t * D]));
+        const double r = __ddiv_rn(acc, static_cast<double>(b));
+        if (is_q) qrep[(static_cast<int64_t>(u) * bpc + i) * D + c] = __double2float_rn(r);
+        else krep[(static_cast<int64_t>(u) * n_slots + slot) * D + c] = __double2float_rn(r);
+    }
+    if (tid == 0) bulk_wait_read0();
+}
+
 }  // namespace
 
 int launch_compress(const bf16* x, int64_t xu, int64_t xb, const int32_t* map, int nb, int units,
@@ -258,6 +311,35 @@ int launch_write_chunk(const bf16* kc, const bf16* vc, const bf16* q, const int3
     }
 #undef PBSA_WC
     return check_launch("write_chunk_kernel");
+}
+
+int launch_ingest_latent(const bf16* k_lat, const bf16* v_lat, const bf16* q_lat, const LatentGeom& g,
+                         const int32_t* stage, int n_slots, bf16* kp, bf16* vp, float* krep, float* qrep,
+                         cudaStream_t s) {
+    const int64_t ctas = static_cast<int64_t>(g.batch) * g.heads * g.nqb();
+    if (ctas == 0) return 0;
+    alignas(64) CUtensorMap tk, tv, tq;
+    std::string err;
+    if (!encode_latent_tmap(&tk, k_lat, g, g.d, false, &err) || !encode_latent_tmap(&tv, v_lat, g, g.d, false, &err) ||
+        (q_lat && !encode_latent_tmap(&tq, q_lat, g, g.d, false, &err)))
+        return set_error(PBSA_ECUDA, "ingest_latent: tensor map: " + err);
+    if (!q_lat) tq = tk;
+    const size_t smem = (q_lat ? 3 : 2) * static_cast<size_t>(g.b()) * g.d * 2;
+    if (smem > 200 * 1024) return set_error(PBSA_EUNSUPPORTED, "ingest_latent: block too large for shared memory");
+#define PBSA_IL(DD, WQ)                                                                                         \
+    do {                                                                                                         \
+        if (int rc = ensure_smem(reinterpret_cast<const void*>(ingest_latent_kernel<DD, WQ>), smem, "ingest")) \
+            return rc;                                                                                           \
+        ingest_latent_kernel<DD, WQ><<<static_cast<int>(ctas), 2 * DD, smem, s>>>(tk, tv, tq, g, stage, n_slots, \
+                                                                                  kp, vp, krep, qrep);          \
+    } while (0)
+    if (g.d == 128) {
+        if (q_lat) PBSA_IL(128, true); else PBSA_IL(128, false);
+    } else {
+        if (q_lat) PBSA_IL(64, true); else PBSA_IL(64, false);
+    }
+#undef PBSA_IL
+    return check_launch("ingest_latent_kernel");
 }
 
 }  // namespace pbsa

@@ -19,6 +19,22 @@ int ensure_smem(const void* kernel, size_t bytes, const char* what);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Chunk latents in the reference's Latent4D layout (tensor.hpp:30-47: (t, h, w, d) row-major with
+// d = heads * d_head), one per batch element: [batch][T][H][W][heads * d] bf16.
+// Blocks follow blockify.cpp:7-65: block id (nt * N_h + nh) * N_w + nw, in-block token index
+// (dt * B_h + dh) * B_w + dw; unit u = e * heads + h.
+struct LatentGeom {
+    int batch, T, H, W, heads, d, bt, bh, bw;
+    __host__ __device__ int nt() const { return T / bt; }
+    __host__ __device__ int nh() const { return H / bh; }
+    __host__ __device__ int nw() const { return W / bw; }
+    __host__ __device__ int nqb() const { return nt() * nh() * nw(); }
+    __host__ __device__ int b() const { return bt * bh * bw; }
+};
+// 5-D tensor map over a chunk latent with a box of one block of one head ({box_d, bw, bh, bt, 1})
+bool encode_latent_tmap(void* tmap, const void* base, const LatentGeom& g, int box_d, bool swizzle128,
+                        std::string* err);
+
 // K1
 int launch_compress(const bf16* x, int64_t x_unit_stride, int64_t x_block_stride, const int32_t* map,
                     int n_blocks, int units, int b, int d, float* reps, int64_t reps_unit_stride,
@@ -27,6 +43,10 @@ int launch_compress(const bf16* x, int64_t x_unit_stride, int64_t x_block_stride
 int launch_write_chunk(const bf16* kc, const bf16* vc, const bf16* q, const int32_t* stage, int bpc, int b,
                        int d, int units, int n_slots, bf16* k_pool, bf16* v_pool, float* krep, float* qrep,
                        cudaStream_t s);
+// the same fused ingest reading the chunk's K/V/Q latents directly (blockify fused into the TMA box)
+int launch_ingest_latent(const bf16* k_lat, const bf16* v_lat, const bf16* q_lat, const LatentGeom& g,
+                         const int32_t* stage, int n_slots, bf16* k_pool, bf16* v_pool, float* krep, float* qrep,
+                         cudaStream_t s);
 // K2
 size_t score_select_workspace(int units, int nqb, int n_keys);
 int launch_score_select(const float* qc, const float* krep, int64_t krep_unit_stride,
@@ -34,10 +54,13 @@ int launch_score_select(const float* qc, const float* krep, int64_t krep_unit_st
                         int n_local, int k, int nqb, int units, int d, float scale, int32_t* sel,
                         float* s_t, void* ws, size_t ws_bytes, cudaStream_t s, int* status = nullptr);
 // K3
+// lat != null: q and o are chunk latents (Q blocks gathered by a 5-D TMA box, O rows scattered back
+// to their latent positions in the epilogue -- unblockify fused); lse stays [units][n_q] block-major
 int launch_bsa_fwd(const bf16* q, const bf16* k_pool, const bf16* v_pool, int n_slots,
                    const int32_t* dense, int dense_stride, int n_dense, const int32_t* local,
                    int local_stride, int n_local, const int32_t* sel, int k, int nqb, int b, int d,
-                   int units, float scale, bf16* o, float* lse, void* ws, size_t ws_bytes, cudaStream_t s);
+                   int units, float scale, bf16* o, float* lse, void* ws, size_t ws_bytes, cudaStream_t s,
+                   const LatentGeom* lat = nullptr);
 size_t bsa_fwd_workspace(int units, int nqb, int d);
 int launch_debug_tile(const bf16* q, const bf16* k, const bf16* v, int d, float* s_out,
                       float* o_out, cudaStream_t s);

@@ -168,6 +168,32 @@ def debug_tile(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor):
     return s, o
 
 
+def latent_geom(shape, heads: int, head_dim: int, block_shape) -> "_capi.LatentGeom":
+    """pbsa_latent_geom of a chunk latent of `shape` ([batch,] T, H, W, heads*head_dim), validated by
+    pbsa_latent_blocks (make_block_layout's divisibility rules, blockify.cpp:7-36)."""
+    shape = tuple(int(x) for x in shape)
+    if len(shape) == 4:
+        shape = (1,) + shape
+    if len(shape) != 5:
+        raise PbsaError("latent: expected [batch,] T, H, W, heads*head_dim")
+    batch, t, h, w, cd = shape
+    if heads <= 0 or cd != heads * head_dim:
+        raise PbsaError(f"latent: last dim {cd} != heads ({heads}) * head_dim ({head_dim})")
+    bt, bh, bw = (int(x) for x in block_shape)
+    g = _capi.LatentGeom(batch, t, h, w, heads, head_dim, bt, bh, bw)
+    nqb, b = C.c_int(), C.c_int()
+    check(LIB.pbsa_latent_blocks(C.byref(g), C.byref(nqb), C.byref(b)))
+    return g
+
+
+def latent_blocks(shape, heads: int, head_dim: int, block_shape) -> tuple[int, int]:
+    """(blocks per chunk, tokens per block) of a chunk latent (host only)."""
+    g = latent_geom(shape, heads, head_dim, block_shape)
+    nqb, b = C.c_int(), C.c_int()
+    check(LIB.pbsa_latent_blocks(C.byref(g), C.byref(nqb), C.byref(b)))
+    return nqb.value, b.value
+
+
 class Memory:
     """Device-resident PBSA memory for `units` heads: PersistentMemory (capacity C blocks, sinks =
     first chunk) + LocalWindow (window_chunks chunks) + the K/V slot pool."""
@@ -272,6 +298,27 @@ class Memory:
         check(LIB.pbsa_attend_qkv(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), int(k_top),
                                   0.0 if scale is None else float(scale), int(mode), o.data_ptr(),
                                   _ptr(lse), _stream()))
+        return (o, lse) if want_lse else o
+
+    def attend_latent(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, block_shape, k_top: int,
+                      mode: int = MODE_DENOISE, scale: float | None = None, out: torch.Tensor | None = None,
+                      want_lse: bool = False):
+        """attend_qkv on chunk latents in the reference's Latent4D layout (tensor.hpp:30-47, d =
+        heads * head_dim): q / k / v [batch, T, H, W, heads*d] (or [T, H, W, heads*d] for batch 1)
+        bf16, blocked by block_shape = (B_t, B_h, B_w) as blockify.cpp does.  The blockify gather
+        and the unblockify scatter of O run inside the kernels (5-D TMA boxes / epilogue stores);
+        the result is bit-identical to attend_qkv on the blockified per-head tensors."""
+        geom = latent_geom(q.shape, self.units // (1 if q.dim() == 4 else q.shape[0]), self.d, block_shape)
+        for name, t in (("q", q), ("k", k), ("v", v)):
+            _need(t, torch.bfloat16, name)
+            if t.shape != q.shape:
+                raise PbsaError(f"attend_latent: {name} must have q's shape {tuple(q.shape)}")
+        o = torch.empty_like(q) if out is None else out
+        lse = torch.empty(self.units, self.blocks_per_chunk * self.b, device=q.device,
+                          dtype=torch.float32) if want_lse else None
+        check(LIB.pbsa_attend_latent(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), C.byref(geom),
+                                     int(k_top), 0.0 if scale is None else float(scale), int(mode),
+                                     o.data_ptr(), _ptr(lse), _stream()))
         return (o, lse) if want_lse else o
 
     def commit(self, s_t: torch.Tensor) -> None:

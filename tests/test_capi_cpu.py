@@ -62,3 +62,23 @@ def test_product_package_does_not_import_the_oracle():
                 text = open(os.path.join(dirpath, f)).read()
                 for pat in (r"^\s*(from|import)\s+oracle", r"liboracle", r"\borc_[a-z]", r"_ref/"):
                     assert not re.search(pat, text, flags=re.M), (f, pat)
+
+
+@pytest.mark.skipif(not os.path.exists(LIB), reason="library not built")
+def test_latent_geometry_follows_make_block_layout():
+    """Chunk-latent blocking (pbsa_latent_blocks) = blockify.cpp:7-36's layout rules, host only."""
+    from paper_2604_21221_b200 import PbsaError, latent_blocks
+    # Wan2.1-1.3B chunk: 3 latent frames of 30 x 52, 12 heads x 128, (1, 15, 4) blocks
+    assert latent_blocks((3, 30, 52, 12 * 128), 12, 128, (1, 15, 4)) == (78, 60)
+    assert latent_blocks((2, 3, 30, 52, 12 * 128), 12, 128, (1, 15, 4)) == (78, 60)
+    assert latent_blocks((2, 16, 16, 64), 1, 64, (1, 8, 8)) == (8, 64)   # config 1 (2-frame chunk)
+    for shape, blk, axis in [((3, 30, 52, 1536), (2, 15, 4), b"T"), ((3, 30, 52, 1536), (1, 7, 4), b"H"),
+                             ((3, 30, 52, 1536), (1, 15, 5), b"W")]:
+        with pytest.raises(PbsaError, match="not divisible"):
+            latent_blocks(shape, 12, 128, blk)
+        from paper_2604_21221_b200 import _capi
+        assert axis + b" (" in _capi.LIB.pbsa_last_error()
+    with pytest.raises(PbsaError, match="at most 64"):
+        latent_blocks((3, 30, 52, 1536), 12, 128, (3, 15, 4))     # 180 tokens > one 64-row slot
+    with pytest.raises(PbsaError, match="heads"):
+        latent_blocks((3, 30, 52, 1000), 12, 128, (1, 15, 4))

@@ -291,3 +291,58 @@ def test_errors_are_loud(pb):
     kp = torch.zeros(1, 4, 64, 128, dtype=torch.bfloat16, device="cuda")
     with pytest.raises(pb.PbsaError):
         pb.attention_sparse(q, kp, kp, None, None, None, 61)
+
+
+# ------------------------------------------------------------------ chunk latents (blockify fused)
+def _latent_vs_blocked(pb, batch, heads, d, T, H, W, blk, C, Wc, n_chunks, k_top, seed):
+    """attend_latent on raw Latent4D chunks == attend_qkv on the oracle-blockified per-head
+    tensors (blockify.cpp:38-65 restated, pinned to the reference): outputs bit-identical after
+    unblockify, selections and memory ids identical."""
+    g = np.random.default_rng(seed)
+    nqb, b = pb.latent_blocks((batch, T, H, W, heads * d), heads, d, blk)
+    U = batch * heads
+    ma = pb.Memory(U, C, Wc, nqb, b, d)
+    mb = pb.Memory(U, C, Wc, nqb, b, d)
+
+    def blocked(lat):  # [batch, T, H, W, heads*d] -> [U, nqb*b, d] (unit = e*heads + h)
+        out = []
+        for e in range(batch):
+            xb = orc.blockify(lat[e], blk)                       # [nqb, b, heads*d]
+            for h in range(heads):
+                out.append(xb[:, :, h * d:(h + 1) * d].reshape(nqb * b, d))
+        return np.stack(out)
+
+    def unblocked(ob):  # [U, nqb*b, d] -> [batch, T, H, W, heads*d]
+        lat = np.zeros((batch, T, H, W, heads * d), np.float32)
+        for e in range(batch):
+            xb = np.concatenate([ob[e * heads + h].reshape(nqb, b, d) for h in range(heads)], axis=2)
+            lat[e] = orc.unblockify(xb, (T, H, W, heads * d), blk)
+        return lat
+
+    for c in range(n_chunks):
+        for mode in (pb.MODE_DENOISE, pb.MODE_CACHE_UPDATE):
+            lat = [bf16_round(g.standard_normal((batch, T, H, W, heads * d)).astype(np.float32)) for _ in range(3)]
+            ob = ma.attend_qkv(*(dev(blocked(x)) for x in lat), k_top, mode)
+            ol = mb.attend_latent(*(dev(x) for x in lat), blk, k_top, mode)
+            torch.cuda.synchronize()
+            np.testing.assert_array_equal(unblocked(ob.float().cpu().numpy()), ol.float().cpu().numpy())
+            sa, sb = ma.last_selection()[0], mb.last_selection()[0]
+            assert (sa is None) == (sb is None)
+            if sa is not None:
+                assert torch.equal(sa, sb)
+        pa, la = ma.assemble()
+        pbb, lb = mb.assemble()
+        assert torch.equal(pa, pbb) and torch.equal(la, lb)
+    ma.close()
+    mb.close()
+
+
+def test_attend_latent_matches_blocked_small(pb):
+    _latent_vs_blocked(pb, batch=2, heads=2, d=128, T=2, H=6, W=8, blk=(1, 3, 4), C=16, Wc=2, n_chunks=4,
+                       k_top=3, seed=41)
+
+
+def test_attend_latent_matches_blocked_wan_blocks(pb):
+    """(1, 15, 4) = 60-token blocks of the Wan-1.3B layout, d = 64 variant with 3-frame chunks."""
+    _latent_vs_blocked(pb, batch=1, heads=3, d=64, T=3, H=30, W=8, blk=(1, 15, 4), C=24, Wc=2, n_chunks=4,
+                       k_top=4, seed=42)
