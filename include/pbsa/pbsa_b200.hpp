@@ -226,6 +226,42 @@ public:
                 cudaStream_t s = nullptr) {
         detail::check(pbsa_attend(m_, q, k_top, static_cast<float>(scale), mode, o, lse, s));
     }
+    // write_chunk + attend fused (one ingest pass over Q, K, V): device [units][bpc*b][d] bf16
+    void attend_qkv(const void* q, const void* k, const void* v, int k_top, int mode, void* o,
+                    float* lse = nullptr, double scale = 0.0, cudaStream_t s = nullptr) {
+        detail::check(pbsa_attend_qkv(m_, q, k, v, k_top, static_cast<float>(scale), mode, o, lse, s));
+    }
+    // the same on device chunk latents [batch][T][H][W][heads*d] bf16 (blockify / unblockify fused)
+    void attend_latent(const void* q, const void* k, const void* v, const pbsa_latent_geom& g, int k_top, int mode,
+                       void* o, float* lse = nullptr, double scale = 0.0, cudaStream_t s = nullptr) {
+        detail::check(pbsa_attend_latent(m_, q, k, v, &g, k_top, static_cast<float>(scale), mode, o, lse, s));
+    }
+    // host convenience on the reference's own types: one batch element's chunk as Latent4D (t, h, w,
+    // heads*d) fp32 (rounded to bf16 on upload), blocked by `shape` like blockify; returns O as a
+    // Latent4D of the same shape.  Synchronous (uploads, runs on the default stream, downloads).
+    Latent4D attend_latent(const Latent4D& q, const Latent4D& k, const Latent4D& v, const BlockShape& shape,
+                           int heads, int k_top, int mode, double scale = 0.0) {
+        if (k.t != q.t || k.h != q.h || k.w != q.w || k.d != q.d || v.t != q.t || v.h != q.h || v.w != q.w ||
+            v.d != q.d)
+            throw std::invalid_argument("attend_latent: q, k, v must have the same (t, h, w, d)");
+        if (heads <= 0 || q.d % static_cast<std::size_t>(heads) != 0)
+            throw std::invalid_argument("attend_latent: d is not a multiple of heads");
+        pbsa_latent_geom g{1, static_cast<int>(q.t), static_cast<int>(q.h), static_cast<int>(q.w), heads,
+                           static_cast<int>(q.d / heads), static_cast<int>(shape.b_t), static_cast<int>(shape.b_h),
+                           static_cast<int>(shape.b_w)};
+        detail::check(pbsa_latent_blocks(&g, nullptr, nullptr));
+        detail::DevBuf<uint16_t> dq(q.size()), dk(q.size()), dv(q.size()), dout(q.size());
+        const auto hq = detail::bf16_of(q.data), hk = detail::bf16_of(k.data), hv = detail::bf16_of(v.data);
+        dq.upload(hq.data(), hq.size());
+        dk.upload(hk.data(), hk.size());
+        dv.upload(hv.data(), hv.size());
+        attend_latent(dq.p, dk.p, dv.p, g, k_top, mode, dout.p, nullptr, scale, nullptr);
+        std::vector<uint16_t> ho(q.size());
+        detail::cuda(cudaMemcpy(ho.data(), dout.p, ho.size() * 2, cudaMemcpyDeviceToHost), "D2H");
+        Latent4D out(q.t, q.h, q.w, q.d);
+        for (std::size_t i = 0; i < ho.size(); ++i) out.data[i] = detail::from_bf16(ho[i]);
+        return out;
+    }
     void commit(const float* s_t, cudaStream_t s = nullptr) { detail::check(pbsa_mem_commit(m_, s_t, s)); }
     // assemble_kv as block ids: persistent (sinks id asc, dynamic id asc), local
     void assemble(int unit, std::vector<int64_t>* persistent, std::vector<int64_t>* local) const {

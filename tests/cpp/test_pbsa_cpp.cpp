@@ -115,6 +115,60 @@ int main() {
         for (std::size_t i = 1; i < L.size(); ++i) EXPECT(L[i] > L[i - 1]);  // FIFO order
         EXPECT(L.front() == 4 * bpc);                                 // chunks 4, 5 in the window
     }
+    // Latent4D drop-in: attend_latent on (t, h, w, heads*d) chunks == attend_qkv on the blocked
+    // per-head tensors (blockify.cpp order: block (nt*N_h + nh)*N_w + nw, token (dt*B_h + dh)*B_w + dw)
+    {
+        const int heads = 2, d = 64, T = 2, H = 4, Wd = 6, bt = 1, bh = 2, bw = 3, bpc = 8, b = 6;
+        const int U = heads, C = 2 * bpc, Wc = 1;
+        pbsa::Memory ml(U, C, Wc, bpc, b, d), mq(U, C, Wc, bpc, b, d);
+        auto fill = [&](int seed) {
+            pbsa::Latent4D x(T, H, Wd, heads * d);
+            for (std::size_t i = 0; i < x.size(); ++i)
+                x.data[i] = pbsa::detail::from_bf16(pbsa::detail::to_bf16(std::sin(0.013 * i + seed)));
+            return x;
+        };
+        auto blocked = [&](const pbsa::Latent4D& x) {  // [heads][bpc*b][d]
+            std::vector<uint16_t> out(static_cast<std::size_t>(heads) * bpc * b * d);
+            for (int hh = 0; hh < heads; ++hh)
+                for (int nt = 0; nt < T / bt; ++nt)
+                    for (int nh = 0; nh < H / bh; ++nh)
+                        for (int nw = 0; nw < Wd / bw; ++nw)
+                            for (int dt = 0; dt < bt; ++dt)
+                                for (int dh = 0; dh < bh; ++dh)
+                                    for (int dw = 0; dw < bw; ++dw) {
+                                        const int blk = (nt * (H / bh) + nh) * (Wd / bw) + nw;
+                                        const int tok = (dt * bh + dh) * bw + dw;
+                                        for (int c = 0; c < d; ++c)
+                                            out[((static_cast<std::size_t>(hh) * bpc + blk) * b + tok) * d + c] =
+                                                pbsa::detail::to_bf16(x.at(nt * bt + dt, nh * bh + dh, nw * bw + dw, hh * d + c));
+                                    }
+            return out;
+        };
+        bool same = true;
+        for (int c = 0; c < 4; ++c) {
+            const int mode = (c & 1) ? PBSA_MODE_CACHE_UPDATE : PBSA_MODE_DENOISE;
+            auto q = fill(3 * c), k = fill(3 * c + 1), v = fill(3 * c + 2);
+            pbsa::Latent4D ol = ml.attend_latent(q, k, v, pbsa::BlockShape{bt, bh, bw}, heads, 2, mode);
+            pbsa::detail::DevBuf<uint16_t> dq(U * bpc * b * d), dk(dq.n), dv(dq.n), dout(dq.n);
+            const auto hq = blocked(q), hk = blocked(k), hv = blocked(v);
+            dq.upload(hq.data(), hq.size());
+            dk.upload(hk.data(), hk.size());
+            dv.upload(hv.data(), hv.size());
+            mq.attend_qkv(dq.p, dk.p, dv.p, 2, mode, dout.p);
+            std::vector<uint16_t> ob(dq.n);
+            pbsa::detail::cuda(cudaMemcpy(ob.data(), dout.p, ob.size() * 2, cudaMemcpyDeviceToHost), "D2H");
+            const auto ol_blocked = blocked(ol);
+            for (std::size_t i = 0; i < ob.size(); ++i) same &= ob[i] == ol_blocked[i];
+        }
+        EXPECT(same);
+        bool threw = false;
+        try {
+            ml.attend_latent(fill(0), fill(1), fill(2), pbsa::BlockShape{1, 3, 3}, heads, 2, 0);  // 4 % 3 != 0
+        } catch (const std::invalid_argument& e) {
+            threw = std::string(e.what()).find("not divisible") != std::string::npos;
+        }
+        EXPECT(threw);
+    }
     std::printf("PASS %d\n", n_ok);
     return 0;
 }
