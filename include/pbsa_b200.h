@@ -164,6 +164,17 @@ int pbsa_last_selection(const pbsa_mem* m, const int32_t** sel, int* k, const fl
 int pbsa_mem_profile(pbsa_mem* m, int enable, int max_calls);
 int pbsa_mem_profile_read(pbsa_mem* m, double* stage_ms, int* n_attend, int* n_write);
 
+/* PBT1 tensor files (reference proj/include/pbsa/tensor.hpp:62-101, proj/src/tensor_io.cpp):
+ * "PBT1" | dtype 0x01 (f32 LE) | rank u8 | rank x u64 LE dims | row-major payload.  Errors return
+ * PBSA_EINVAL with a message that starts with the reference's TensorIoError::Kind name (OpenFailed,
+ * BadMagic, BadDtype, Truncated, TrailingData, BadShape).  write / info / read are host-only;
+ * load_bf16 streams the payload through pinned staging to the device and converts to bf16 there
+ * (synchronises `stream` before returning; dst: device, 16-byte aligned, capacity in elements). */
+int pbsa_pbt1_write(const char* path, const float* data, int rank, const uint64_t* dims);
+int pbsa_pbt1_info(const char* path, int* rank, uint64_t* dims, int max_rank);
+int pbsa_pbt1_read(const char* path, float* out, uint64_t capacity);
+int pbsa_pbt1_load_bf16(const char* path, void* dst, uint64_t capacity, void* stream);
+
 /* cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault) on `stream` (state export for tests) */
 int pbsa_copy(void* dst, const void* src, size_t bytes, void* stream);
 

@@ -116,4 +116,32 @@ int ref_read_matrix(const char* path, float* out, int64_t cap, int64_t* rows, in
     });
 }
 
+// PBT1 through the reference's own writer / reader (tests/test_pbt1.py); the read returns the
+// TensorIoError::Kind as 10 + kind on format errors.
+int ref_write_latent(const char* path, const float* p, int64_t t, int64_t h, int64_t w, int64_t d) {
+    return guard([&] {
+        pbsa::Latent4D x(static_cast<std::size_t>(t), static_cast<std::size_t>(h), static_cast<std::size_t>(w),
+                         static_cast<std::size_t>(d));
+        if (x.size()) std::memcpy(x.data.data(), p, sizeof(float) * x.size());
+        pbsa::write_tensor(path, x);
+    });
+}
+
+int ref_read_tensor(const char* path, float* out, int64_t cap, int64_t* rank, int64_t* dims) {
+    try {
+        auto tf = pbsa::read_tensor(path);
+        *rank = static_cast<int64_t>(tf.dims.size());
+        for (std::size_t i = 0; i < tf.dims.size() && i < 8; ++i) dims[i] = static_cast<int64_t>(tf.dims[i]);
+        if (static_cast<int64_t>(tf.data.size()) <= cap && !tf.data.empty())
+            std::memcpy(out, tf.data.data(), sizeof(float) * tf.data.size());
+        return 0;
+    } catch (const pbsa::TensorIoError& e) {
+        g_err = e.what();
+        return 10 + static_cast<int>(e.kind());
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
 }  // extern "C"

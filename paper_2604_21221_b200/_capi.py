@@ -63,6 +63,10 @@ _SIGS = {
     "pbsa_mem_profile_read": (_i32, [_vp, C.POINTER(C.c_double), C.POINTER(_i32), C.POINTER(_i32)]),
     "pbsa_mem_status": (_i32, [_vp, C.POINTER(_i32), _vp]),
     "pbsa_copy": (_i32, [_vp, _vp, C.c_size_t, _vp]),
+    "pbsa_pbt1_write": (_i32, [C.c_char_p, _vp, _i32, C.POINTER(C.c_uint64)]),
+    "pbsa_pbt1_info": (_i32, [C.c_char_p, C.POINTER(_i32), C.POINTER(C.c_uint64), _i32]),
+    "pbsa_pbt1_read": (_i32, [C.c_char_p, _vp, C.c_uint64]),
+    "pbsa_pbt1_load_bf16": (_i32, [C.c_char_p, _vp, C.c_uint64, _vp]),
     "pbsa_debug_tile": (_i32, [_vp, _vp, _vp, _i32, _vp, _vp, _vp]),
 }
 

@@ -168,6 +168,58 @@ def debug_tile(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor):
     return s, o
 
 
+# ---- PBT1 tensor files (reference tensor.hpp:62-101, tensor_io.cpp) -------------------------
+class TensorIoError(PbsaError):
+    """PBT1 format / IO error; .kind is the reference's TensorIoError::Kind name."""
+
+    KINDS = ("OpenFailed", "BadMagic", "BadDtype", "Truncated", "TrailingData", "BadShape")
+
+    def __init__(self, msg: str):
+        super().__init__(msg)
+        self.kind = msg.split(":", 1)[0] if msg.split(":", 1)[0] in self.KINDS else None
+
+
+def _pbt1(rc: int) -> None:
+    if rc == _capi.PBSA_EINVAL:
+        raise TensorIoError(LIB.pbsa_last_error().decode())
+    check(rc)
+
+
+def write_tensor(path: str, x) -> None:
+    """write_tensor (tensor_io.cpp:46-54): any-rank float32 array -> PBT1 file."""
+    import numpy as np
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.float32))
+    dims = (C.c_uint64 * max(a.ndim, 1))(*a.shape)
+    _pbt1(LIB.pbsa_pbt1_write(str(path).encode(), a.ctypes.data if a.size else None, a.ndim, dims))
+
+
+def tensor_dims(path: str) -> tuple[int, ...]:
+    r = C.c_int()
+    dims = (C.c_uint64 * 16)()
+    _pbt1(LIB.pbsa_pbt1_info(str(path).encode(), C.byref(r), dims, 16))
+    return tuple(int(dims[i]) for i in range(r.value))
+
+
+def read_tensor(path: str):
+    """read_tensor (tensor_io.cpp:56-108): PBT1 file -> float32 array of the file's dims."""
+    import numpy as np
+    dims = tensor_dims(path)
+    n = 0 if not dims else int(np.prod(dims, dtype=np.uint64))
+    a = np.empty(n, np.float32)
+    _pbt1(LIB.pbsa_pbt1_read(str(path).encode(), a.ctypes.data if n else None, n))
+    return a.reshape(dims) if dims else a
+
+
+def load_bf16(path: str, device=None) -> torch.Tensor:
+    """A PBT1 file straight into device memory as bf16 (pinned staging, async copies, on-device
+    conversion), e.g. a chunk latent for Memory.attend_latent."""
+    dims = tensor_dims(path)
+    out = torch.empty(dims, dtype=torch.bfloat16, device=device or "cuda")
+    _pbt1(LIB.pbsa_pbt1_load_bf16(str(path).encode(), out.data_ptr() if out.numel() else None,
+                                  out.numel(), _stream()))
+    return out
+
+
 def latent_geom(shape, heads: int, head_dim: int, block_shape) -> "_capi.LatentGeom":
     """pbsa_latent_geom of a chunk latent of `shape` ([batch,] T, H, W, heads*head_dim), validated by
     pbsa_latent_blocks (make_block_layout's divisibility rules, blockify.cpp:7-36)."""
