@@ -42,6 +42,8 @@ class RolloutConfig:
     head_dim: int = 128
     seed: int = 7
     trace_units: int = 1                     # heads recorded in the trace (unit 0..n-1)
+    latent: bool = True                      # chunks stay (t, h, w, d) latents (pbsa_attend_latent);
+                                             # False: blockify in torch + pbsa_attend_qkv
 
     def validate(self):
         ts = list(self.timesteps)
@@ -133,6 +135,18 @@ class ToyDenoiser:
             out.append(y)
         return out
 
+    def qkv_tokens(self, layer: int, x: torch.Tensor, t: float):
+        """x: [n_tok, d_model] bf16 in any token order -> q, k, v [n_tok, heads*head_dim]: for a
+        (t, h, w) token order these ARE the Latent4D chunk latents pbsa_attend_latent consumes."""
+        wq, wk, wv, _ = self.w[layer]
+        xf = x.float()
+        xt = (xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + 1e-6) * (1.0 + 0.1 * t)).to(x.dtype)
+        return [xt @ w for w in (wq, wk, wv)]
+
+    def project_out_tokens(self, layer: int, o: torch.Tensor, x: torch.Tensor) -> torch.Tensor:
+        """o: [n_tok, heads*head_dim] -> residual update of x [n_tok, d_model]."""
+        return x + (o @ self.w[layer][3]) * (1.0 / self.cfg.layers)
+
     def project_out(self, layer: int, o: torch.Tensor, x: torch.Tensor) -> torch.Tensor:
         """o: [heads, n_tok, head_dim] -> residual update of x."""
         wo = self.w[layer][3]
@@ -162,33 +176,37 @@ def run_inference(cfg: RolloutConfig, denoiser: ToyDenoiser | None = None, trace
         x = torch.randn(dims, device=device, generator=g).to(torch.bfloat16)  # x ~ N(0, I)
         e0 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for jj, t in enumerate(cfg.timesteps):
-            j = len(cfg.timesteps) - jj  # j = T .. 1
-            xb = blockify_tokens(x, cfg.block_shape)
-            h = xb
+        def layer_stack(xin, t, mode, scores_rec=None):
+            """All layers of the toy denoiser on one chunk; returns the chunk latent out."""
+            nonlocal calls
+            dm = cfg.d_model
+            h = xin.reshape(-1, dm) if cfg.latent else blockify_tokens(xin, cfg.block_shape)
             for layer, mem in enumerate(mems):
-                q, k, v = den.qkv(layer, h, t)
                 n_l = mem.info().n_l
                 k_top = pbsa.topk_count(n_l, cfg.topk_ratio) if n_l else 0
-                o = mem.attend_qkv(q, k, v, k_top, pbsa.MODE_DENOISE)
-                h = den.project_out(layer, o, h)
+                if cfg.latent:  # (t, h, w) tokens: blockify / unblockify happen inside the kernels
+                    q, k, v = den.qkv_tokens(layer, h, t)
+                    o = mem.attend_latent(q.view(dims), k.view(dims), v.view(dims), cfg.block_shape, k_top, mode)
+                    h = den.project_out_tokens(layer, o.view(-1, dm), h)
+                else:
+                    q, k, v = den.qkv(layer, h, t)
+                    o = mem.attend_qkv(q, k, v, k_top, mode)
+                    h = den.project_out(layer, o, h)
+                if scores_rec is not None and layer == 0 and mode == pbsa.MODE_CACHE_UPDATE:
+                    _, s_t = mem.last_selection()
+                    scores_rec["scores"] = [[float(v_) for v_ in s_t[u].tolist()] for u in range(cfg.trace_units)]
                 calls += 1
-            x0_hat = unblockify_tokens(h, dims, cfg.block_shape)
+            return h.view(dims) if cfg.latent else unblockify_tokens(h, dims, cfg.block_shape)
+
+        for jj, t in enumerate(cfg.timesteps):
+            j = len(cfg.timesteps) - jj  # j = T .. 1
+            x0_hat = layer_stack(x, t, pbsa.MODE_DENOISE)
             rec = {"chunk": i, "j": j, "t": t, "cache_updated": j == 1, "grad_enabled": False}
             if j == 1:
                 frames.append(x0_hat)
                 # k = 0 pass on the clean chunk: scores, push/evict, Top-C (Alg. 1 lines 9-10)
-                hb = blockify_tokens(x0_hat, cfg.block_shape)
                 before = [_ids(m, cfg.trace_units) for m in mems[:1]]
-                for layer, mem in enumerate(mems):
-                    q, k, v = den.qkv(layer, hb, 0.0)
-                    n_l = mem.info().n_l
-                    k_top = pbsa.topk_count(n_l, cfg.topk_ratio) if n_l else 0
-                    o = mem.attend_qkv(q, k, v, k_top, pbsa.MODE_CACHE_UPDATE)
-                    if layer == 0 and record_scores:
-                        _, s_t = mem.last_selection()
-                        rec["scores"] = [[float(v_) for v_ in s_t[u].tolist()] for u in range(cfg.trace_units)]
-                    hb = den.project_out(layer, o, hb)
+                layer_stack(x0_hat, 0.0, pbsa.MODE_CACHE_UPDATE, rec if record_scores else None)
                 p_ids, l_ids = _ids(mems[0], cfg.trace_units)
                 prev_l = before[0][1]
                 rec["evicted"] = [sorted(set(prev_l[u]) - set(l_ids[u])) for u in range(cfg.trace_units)]

@@ -55,7 +55,7 @@ def test_rollout_trace_invariants_and_determinism():
     frames, trace, timing = ro.run_inference(cfg)
     ro.check_trace(cfg, trace)
     assert len(frames) == cfg.num_chunks
-    assert timing["pbsa_calls"] == cfg.num_chunks * len(cfg.timesteps) * cfg.layers
+    assert timing["pbsa_calls"] == cfg.num_chunks * (len(cfg.timesteps) + 1) * cfg.layers  # + the k=0 pass
     upd = [r for r in trace if r["cache_updated"]]
     # C = 4 frames = 8 blocks (sinks = first chunk of 8), window 2 chunks: first eviction at push 3
     assert [len(r["evicted"][0]) for r in upd[:3]] == [0, 0, 8]
@@ -63,4 +63,17 @@ def test_rollout_trace_invariants_and_determinism():
     frames2, trace2, _ = ro.run_inference(cfg)
     assert trace2 == trace  # bit-identical traces (scores included)
     for a, b in zip(frames, frames2):
+        assert torch.equal(a, b)
+
+
+@pytest.mark.gpu
+def test_rollout_latent_path_equals_blocked_path():
+    """The driver on chunk latents (pbsa_attend_latent: blockify / unblockify inside the kernels)
+    and on torch-blockified per-head tensors (pbsa_attend_qkv) produce identical traces and frames."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    fa, ta, _ = ro.run_inference(small_cfg(latent=True))
+    fb, tb, _ = ro.run_inference(small_cfg(latent=False))
+    assert ta == tb
+    for a, b in zip(fa, fb):
         assert torch.equal(a, b)
