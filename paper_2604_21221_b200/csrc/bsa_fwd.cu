@@ -202,6 +202,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = misc[0];
+    // programmatic dependent launch: everything above (barriers, TMEM, tensor-map prefetch, Q
+    // padding) overlapped the previous kernel; its outputs (selections, Q) are visible from here
+    pdl_wait();
 
     if (warp == 0) {
         // ============================================================== TMA producer
@@ -767,7 +770,9 @@ int launch_impl(const bf16* q, const bf16* kp, const bf16* vp, BsaParams p, cuda
         if (p.whole_waves == 0) p.grid = p.tail_grid;
     }
     if (p.grid <= 0) return 0;
-    bsa_fwd_kernel<D, NSK, NSV, B, POLY><<<p.grid, kThreads, smem, s>>>(tq, tk, tv, p);
+    if (launch_pdl(bsa_fwd_kernel<D, NSK, NSV, B, POLY>, dim3(p.grid), dim3(kThreads), smem, s, tq, tk, tv, p) !=
+        cudaSuccess)
+        return check_launch("bsa_fwd_kernel");
     return check_launch("bsa_fwd_kernel");
 }
 

@@ -85,6 +85,11 @@ bool encode_tmap_impl(void* tmap, const void* base, int rank, const uint64_t* di
 }
 }  // namespace
 
+bool pdl_enabled() {
+    static const bool on = !(getenv("PBSA_PDL") && atoi(getenv("PBSA_PDL")) == 0);
+    return on;
+}
+
 bool encode_tmap_bf16(void* tmap, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
                       const uint32_t* box, std::string* err) {
     return encode_tmap_impl(tmap, base, rank, dims, strides, box, true, err);

@@ -171,6 +171,7 @@ __global__ void __launch_bounds__(2 * D) write_chunk_bulk_kernel(const bf16* __r
                                                                  int units, int n_slots, bf16* __restrict__ kp,
                                                                  bf16* __restrict__ vp, float* __restrict__ krep,
                                                                  float* __restrict__ qrep) {
+    pdl_wait();  // programmatic dependent launch: upstream outputs are visible from here on
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ __align__(8) uint64_t bar;
     const int tid = threadIdx.x;
@@ -222,6 +223,7 @@ __global__ void __launch_bounds__(2 * D) ingest_latent_kernel(const __grid_const
                                                               const LatentGeom g, const int32_t* __restrict__ stage,
                                                               int n_slots, bf16* __restrict__ kp, bf16* __restrict__ vp,
                                                               float* __restrict__ krep, float* __restrict__ qrep) {
+    pdl_wait();  // programmatic dependent launch: upstream outputs are visible from here on
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ __align__(8) uint64_t bar;
     const int tid = threadIdx.x;
@@ -290,9 +292,8 @@ int launch_write_chunk(const bf16* kc, const bf16* vc, const bf16* q, const int3
         if (int rc = ensure_smem(reinterpret_cast<const void*>(write_chunk_bulk_kernel<DD, WQ>), smem,          \
                                  "write_chunk"))                                                                 \
             return rc;                                                                                           \
-        write_chunk_bulk_kernel<DD, WQ><<<static_cast<int>(warps), 2 * DD, smem, s>>>(kc, vc, q, stage, bpc, b, \
-                                                                                      units, n_slots, kp, vp,   \
-                                                                                      krep, qrep);              \
+        launch_pdl(write_chunk_bulk_kernel<DD, WQ>, dim3(static_cast<unsigned>(warps)), dim3(2 * DD), smem, s, kc,  \
+                   vc, q, stage, bpc, b, units, n_slots, kp, vp, krep, qrep);                                   \
     } while (0)
         if (d == 128) {
             if (q) PBSA_WCB(128, true); else PBSA_WCB(128, false);
@@ -330,8 +331,8 @@ int launch_ingest_latent(const bf16* k_lat, const bf16* v_lat, const bf16* q_lat
     do {                                                                                                         \
         if (int rc = ensure_smem(reinterpret_cast<const void*>(ingest_latent_kernel<DD, WQ>), smem, "ingest")) \
             return rc;                                                                                           \
-        ingest_latent_kernel<DD, WQ><<<static_cast<int>(ctas), 2 * DD, smem, s>>>(tk, tv, tq, g, stage, n_slots, \
-                                                                                  kp, vp, krep, qrep);          \
+        launch_pdl(ingest_latent_kernel<DD, WQ>, dim3(static_cast<unsigned>(ctas)), dim3(2 * DD), smem, s, tk, tv, \
+                   tq, g, stage, n_slots, kp, vp, krep, qrep);                                                  \
     } while (0)
     if (g.d == 128) {
         if (q_lat) PBSA_IL(128, true); else PBSA_IL(128, false);

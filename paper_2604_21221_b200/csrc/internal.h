@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 
 #include "../../include/pbsa_b200.h"
 
@@ -18,6 +19,26 @@ int check_launch(const char* what);
 int ensure_smem(const void* kernel, size_t bytes, const char* what);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Programmatic dependent launch: every hot-path kernel is launched with programmatic stream
+// serialization and executes pdl_wait() (griddepcontrol.wait) before it touches data produced
+// upstream (measured effect at config 2: ~1 %, within run-to-run noise).  PBSA_PDL=0 disables it.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // Chunk latents in the reference's Latent4D layout (tensor.hpp:30-47: (t, h, w, d) row-major with
 // d = heads * d_head), one per batch element: [batch][T][H][W][heads * d] bf16.

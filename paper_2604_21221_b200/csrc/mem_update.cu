@@ -15,6 +15,7 @@
 //
 // Roofline: HBM (candidate scores + slot tables); launch-latency bound at Wan-1.3B shape.
 #include "internal.h"
+#include "ptx.cuh"
 
 namespace pbsa {
 namespace {
@@ -40,6 +41,7 @@ __global__ void mem_init_kernel(MemDev m, int C, int Lcap, int bpc, int S) {
 }
 
 __global__ void __launch_bounds__(256) mem_commit_kernel(const CommitParams p) {
+    pdl_wait();  // programmatic dependent launch: upstream outputs are visible from here on
     extern __shared__ __align__(16) uint8_t smem[];
     const int u = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
     const int C = p.C, Lcap = p.Lcap, bpc = p.bpc, S = p.S;
@@ -201,7 +203,7 @@ int launch_mem_commit(const MemDev& m, const float* s_t, int units, int C, int L
                         static_cast<size_t>(bpc) * 4 + static_cast<size_t>(S) * 4 + static_cast<size_t>(C) * 16 + 64;
     if (smem > 227 * 1024) return set_error(PBSA_EUNSUPPORTED, "mem_commit: memory geometry too large for one CTA");
     if (int rc = ensure_smem(reinterpret_cast<const void*>(mem_commit_kernel), smem, "mem_commit")) return rc;
-    mem_commit_kernel<<<units, 256, smem, s>>>(p);
+    launch_pdl(mem_commit_kernel, dim3(units), dim3(256), smem, s, p);
     return check_launch("mem_commit_kernel");
 }
 

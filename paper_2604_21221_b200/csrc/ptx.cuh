@@ -24,6 +24,12 @@ __device__ __forceinline__ bool elect_one() {
     return pred != 0;
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// No kernel triggers its dependents early (griddepcontrol.launch_dependents): measured, early
+// triggers let K3's large-smem CTAs claim SMs while the preceding small kernel still had CTAs to
+// place (3.36 -> 3.46 ms/chunk).  The attribute alone overlaps the launch itself.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ---------------------------------------------------------------- mbarrier
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");

@@ -20,6 +20,7 @@
 #include <cfloat>
 
 #include "internal.h"
+#include "ptx.cuh"
 
 namespace pbsa {
 namespace {
@@ -181,6 +182,7 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
 // row reads are both bank-conflict free.  Query rows are fp64 broadcasts.
 template <int D>
 __global__ void __launch_bounds__(kLogitKeys) logits_rm_kernel(const ScoreParams p, float* __restrict__ z) {
+    pdl_wait();  // programmatic dependent launch: upstream outputs are visible from here on
     extern __shared__ __align__(16) uint8_t smem[];
     double* qs = reinterpret_cast<double*>(smem);                            // [kMaxRows][D]
     float4* ks = reinterpret_cast<float4*>(smem + kMaxRows * D * 8);         // [kLogitKeys][D/4] swizzled
@@ -253,6 +255,7 @@ __global__ void __launch_bounds__(kLogitKeys) logits_rm_kernel(const ScoreParams
 // concurrently instead of back to back.
 template <int SPLIT>
 __global__ void __launch_bounds__(256) row_select_kernel(const ScoreParams p, const float* __restrict__ z) {
+    pdl_wait();  // programmatic dependent launch: upstream outputs are visible from here on
     extern __shared__ __align__(16) uint8_t smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int kRowsPerCta = kMaxRows / SPLIT;
@@ -305,6 +308,7 @@ constexpr int kKeysPerThread = 4;
 
 template <int D>
 __global__ void __launch_bounds__(256, 2) logits_t_kernel(const ScoreParams p, float* __restrict__ zt) {
+    pdl_wait();  // programmatic dependent launch: upstream outputs are visible from here on
     __shared__ __align__(16) double qd[kMaxRows * D];
     const int u = blockIdx.y, i0 = blockIdx.x * kMaxRows;
     const int nr = min(kMaxRows, p.nqb - i0);
@@ -372,6 +376,7 @@ __global__ void __launch_bounds__(256, 2) logits_t_kernel(const ScoreParams p, f
 __global__ void __launch_bounds__(128) row_denom_kernel(const float* __restrict__ zt, int64_t rt, int off, int n,
                                                         float* __restrict__ mrow, double* __restrict__ drow,
                                                         int* status) {
+    pdl_wait();  // programmatic dependent launch: upstream outputs are visible from here on
     const int lane = threadIdx.x & 31;
     const int64_t R = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const bool live = R < rt;
@@ -433,6 +438,7 @@ __global__ void __launch_bounds__(128) row_denom_kernel(const float* __restrict_
 __global__ void __launch_bounds__(256) row_prob_kernel(const float* __restrict__ zt, int64_t rt, int off, int n,
                                                        const float* __restrict__ mrow,
                                                        const double* __restrict__ drow, float* __restrict__ out) {
+    pdl_wait();  // programmatic dependent launch: upstream outputs are visible from here on
     __shared__ float tile[32][33];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int j0 = blockIdx.x * 32;
@@ -464,6 +470,7 @@ __global__ void __launch_bounds__(256) row_prob_kernel(const float* __restrict__
 // works on them; staging rows in shared memory measured slower -- it caps residency at 8 warps/SM).
 __global__ void __launch_bounds__(256) topk_rows_kernel(const float* __restrict__ prob, int n, int k, int64_t rows,
                                                         int32_t* __restrict__ sel) {
+    pdl_wait();  // programmatic dependent launch: upstream outputs are visible from here on
     __shared__ uint32_t hist[8][256];
     const int warp = threadIdx.x >> 5;
     const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + warp;
@@ -473,6 +480,7 @@ __global__ void __launch_bounds__(256) topk_rows_kernel(const float* __restrict_
 
 __global__ void aggregate_kernel(const float* __restrict__ arows, int n_keys, int nqb, int units,
                                  float* __restrict__ s_t) {
+    pdl_wait();  // programmatic dependent launch: upstream outputs are visible from here on
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     const int u = blockIdx.y;
     if (j >= n_keys) return;
@@ -517,22 +525,24 @@ int launch_score_select(const float* qc, const float* krep, int64_t kru, const i
             float* zt = static_cast<float*>(ws) + static_cast<size_t>(rt) * n_keys;
             float* prob = zt + static_cast<size_t>(rt) * n_keys;
             dim3 g1((nqb + kMaxRows - 1) / kMaxRows, units, (n_keys + 256 * kKeysPerThread - 1) / (256 * kKeysPerThread));
-            if (d == 128) logits_t_kernel<128><<<g1, 256, 0, s>>>(p, zt);
-            else logits_t_kernel<64><<<g1, 256, 0, s>>>(p, zt);
+            if (d == 128) launch_pdl(logits_t_kernel<128>, g1, dim3(256), 0, s, p, zt);
+            else launch_pdl(logits_t_kernel<64>, g1, dim3(256), 0, s, p, zt);
             if (int rc = check_launch("logits_t_kernel")) return rc;
             float* mrow = prob + static_cast<size_t>(rt) * n_keys;
             double* drow = reinterpret_cast<double*>(mrow + ((rt + 1) & ~int64_t(1)));
             const int gr = static_cast<int>((rt + 127) / 128);
             auto softmax_rows = [&](int off, int n, float* out, int* st) -> int {
-                row_denom_kernel<<<gr, 128, 0, s>>>(zt, rt, off, n, mrow, drow, st);
+                launch_pdl(row_denom_kernel, dim3(gr), dim3(128), 0, s, static_cast<const float*>(zt), rt, off, n, mrow, drow, st);
                 if (int rc = check_launch("row_denom_kernel")) return rc;
                 dim3 g2((n + 31) / 32, static_cast<unsigned>((rt + 31) / 32));
-                row_prob_kernel<<<g2, 256, 0, s>>>(zt, rt, off, n, mrow, drow, out);
+                launch_pdl(row_prob_kernel, g2, dim3(256), 0, s, static_cast<const float*>(zt), rt, off, n,
+                           static_cast<const float*>(mrow), static_cast<const double*>(drow), out);
                 return check_launch("row_prob_kernel");
             };
             if (do_select) {
                 if (int rc = softmax_rows(local_off, n_local, prob, status)) return rc;
-                topk_rows_kernel<<<static_cast<int>((rt + 7) / 8), 256, 0, s>>>(prob, n_local, k, rt, sel);
+                launch_pdl(topk_rows_kernel, dim3(static_cast<unsigned>((rt + 7) / 8)), dim3(256), 0, s,
+                           static_cast<const float*>(prob), n_local, k, rt, sel);
                 if (int rc = check_launch("topk_rows_kernel")) return rc;
             }
             if (arows != nullptr) {
@@ -547,11 +557,11 @@ int launch_score_select(const float* qc, const float* krep, int64_t kru, const i
             if (d == 128) {
                 if (int rc = ensure_smem(reinterpret_cast<const void*>(logits_rm_kernel<128>), lsmem, "logits_rm"))
                     return rc;
-                logits_rm_kernel<128><<<g1, kLogitKeys, lsmem, s>>>(p, z);
+                launch_pdl(logits_rm_kernel<128>, g1, dim3(kLogitKeys), lsmem, s, p, z);
             } else {
                 if (int rc = ensure_smem(reinterpret_cast<const void*>(logits_rm_kernel<64>), lsmem, "logits_rm"))
                     return rc;
-                logits_rm_kernel<64><<<g1, kLogitKeys, lsmem, s>>>(p, z);
+                launch_pdl(logits_rm_kernel<64>, g1, dim3(kLogitKeys), lsmem, s, p, z);
             }
             if (int rc = check_launch("logits_rm_kernel")) return rc;
             p.per_warp = (static_cast<size_t>(n_keys) * 12 + 16 + static_cast<size_t>(n_local) * 4 + 1024 + 15) & ~size_t(15);
@@ -559,18 +569,20 @@ int launch_score_select(const float* qc, const float* krep, int64_t kru, const i
             if (do_select && arows != nullptr) {
                 if (int rc = ensure_smem(reinterpret_cast<const void*>(row_select_kernel<2>), smem, "row_select"))
                     return rc;
-                row_select_kernel<2><<<static_cast<unsigned>((rt + kMaxRows / 2 - 1) / (kMaxRows / 2)), 256, smem, s>>>(p, z);
+                launch_pdl(row_select_kernel<2>, dim3(static_cast<unsigned>((rt + kMaxRows / 2 - 1) / (kMaxRows / 2))),
+                           dim3(256), smem, s, p, static_cast<const float*>(z));
             } else {
                 if (int rc = ensure_smem(reinterpret_cast<const void*>(row_select_kernel<1>), smem, "row_select"))
                     return rc;
-                row_select_kernel<1><<<static_cast<unsigned>((rt + kMaxRows - 1) / kMaxRows), 256, smem, s>>>(p, z);
+                launch_pdl(row_select_kernel<1>, dim3(static_cast<unsigned>((rt + kMaxRows - 1) / kMaxRows)), dim3(256),
+                           smem, s, p, static_cast<const float*>(z));
             }
             if (int rc = check_launch("row_select_kernel")) return rc;
         }
     }
     if (s_t) {
         dim3 grid((n_keys + 127) / 128, units);
-        aggregate_kernel<<<grid, 128, 0, s>>>(arows, n_keys, nqb, units, s_t);
+        launch_pdl(aggregate_kernel, grid, dim3(128), 0, s, static_cast<const float*>(arows), n_keys, nqb, units, s_t);
         if (int rc = check_launch("aggregate_kernel")) return rc;
     }
     return 0;
