@@ -33,6 +33,7 @@
 //
 // Roofline: tensor core.  Executed FLOPs per tile = 4 * 128 * 64 * d * |union list|.
 #include <cfloat>
+#include <cstdio>
 #include <cstdlib>
 
 #include "internal.h"
@@ -42,6 +43,7 @@ namespace pbsa {
 namespace {
 
 constexpr int kThreads = 192;
+constexpr int kRing = 2;  // partial-output slots per CTA (stream-K tail: first and last fragment)
 constexpr uint32_t kTmemCols = 256;
 // a block whose row sum (against the running max) exceeds this takes the exact rescale path
 constexpr float kOverflowSum = 65536.0f;
@@ -61,6 +63,7 @@ struct BsaParams {
     float* lse;
     float scale_log2;
     int max_list, bm_words;
+    int list16;     // visible-list entries are 16-bit (n_slots < 16384)
     int lat;        // q / o are chunk latents (LatentGeom lg), not block-major [units][n_q][d]
     LatentGeom lg;
     long long* trace;  // perf experiments only: per-event clock64 stamps of CTA 0 (null = off)
@@ -70,8 +73,8 @@ struct BsaParams {
     int tiles_per_unit, n_tiles, grid;
     int whole_waves, tail_base, tail_grid;
     int64_t vlen, vtotal;  // virtual length of one tile (upper bound of its list) and of the tail
-    float* part_o;         // [2*grid][128][D] fp32 (null -> whole tiles only)
-    float* part_ml;        // [2*grid][2][128]
+    float* part_o;         // [kRing*grid][128][D] fp32 (null -> whole tiles only)
+    float* part_ml;        // [kRing*grid][2][128]
     int* counters;         // [n_tiles], zero between launches
 };
 
@@ -99,8 +102,9 @@ struct Layout {
     static constexpr uint32_t kOffMisc = kOffMeta + 2 * sizeof(FragMeta);
     static constexpr uint32_t kOffList = kOffMisc + 16;
     static constexpr uint32_t kSColBase = D;  // S0 at D, S1 at D + 64
-    static size_t bytes(int max_list, int bm_words) {
-        return 1024 + kOffList + 2 * static_cast<size_t>(max_list) * 4 + 2 * static_cast<size_t>(bm_words) * 4;
+    static size_t bytes(int max_list, int bm_words, int entry_bytes) {
+        const size_t lb = (2 * static_cast<size_t>(max_list) * entry_bytes + 15) & ~size_t(15);
+        return 1024 + kOffList + lb + 2 * static_cast<size_t>(bm_words) * 4;
     }
 };
 
@@ -153,8 +157,21 @@ __global__ void __launch_bounds__(kThreads, 2)
     uint64_t* list_empty = list_full + 2;
     FragMeta* meta = reinterpret_cast<FragMeta*>(smem + L::kOffMeta);
     uint32_t* misc = reinterpret_cast<uint32_t*>(smem + L::kOffMisc);  // [0] tmem base, [1] merge flag
-    int32_t* lists = reinterpret_cast<int32_t*>(smem + L::kOffList);  // [max_list]
-    uint32_t* bm = reinterpret_cast<uint32_t*>(lists + 2 * p.max_list);  // [2][bm_words] (producer only)
+    // visible lists, double-buffered: [2][max_list] entries of 4 bytes (slot | mask << 24) or, when
+    // the pool has < 16384 slots, 2 bytes (slot | mask << 14) -- halves the footprint of long lists
+    // (config 5: 3238 entries) so two CTAs still fit an SM
+    uint8_t* lists = smem + L::kOffList;
+    const int esz = p.list16 ? 2 : 4;
+    const int mshift = p.list16 ? 14 : 24;
+    uint32_t* bm = reinterpret_cast<uint32_t*>(lists + ((2 * static_cast<size_t>(p.max_list) * esz + 15) & ~size_t(15)));
+    auto list_put = [&](uint8_t* base, int i, int slot, int mask) {
+        if (p.list16) reinterpret_cast<uint16_t*>(base)[i] = static_cast<uint16_t>(slot | (mask << 14));
+        else reinterpret_cast<int32_t*>(base)[i] = slot | (mask << 24);
+    };
+    auto list_slot = [&](const uint8_t* base, int i) {
+        return p.list16 ? static_cast<int>(reinterpret_cast<const uint16_t*>(base)[i] & 0x3FFF)
+                        : (reinterpret_cast<const int32_t*>(base)[i] & 0xFFFFFF);
+    };
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int cta = blockIdx.x;
@@ -220,7 +237,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             for (int f = 0; f < n_frag; ++f) {
                 const int lb = f & 1;
                 mbar_wait(list_empty + lb, ((f >> 1) & 1) ^ 1);
-                int32_t* list = lists + lb * p.max_list;
+                uint8_t* list = lists + static_cast<size_t>(lb) * p.max_list * esz;
                 // ---------------------------------------------------------- fragment schedule
                 const bool tail_frag = p.part_o != nullptr && f >= p.whole_waves;
                 const int tile = tail_frag ? my_first_tile + (f - p.whole_waves) : cta + f * p.grid;
@@ -250,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                     }
                 }
                 for (int e = lane; e < p.n_dense; e += 32)
-                    list[e] = __ldg(p.dense + static_cast<int64_t>(u) * p.dense_stride + e) | (3 << 24);
+                    list_put(list, e, __ldg(p.dense + static_cast<int64_t>(u) * p.dense_stride + e), 3);
                 __syncwarp();
                 int run = p.n_dense;
                 {
@@ -273,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                             un &= un - 1;
                             const int idx = w * 32 + bit;
                             const int mask = static_cast<int>((a >> bit) & 1u) | (static_cast<int>((c >> bit) & 1u) << 1);
-                            list[pos++] = __ldg(loc + idx) | (mask << 24);
+                            list_put(list, pos++, __ldg(loc + idx), mask);
                         }
                         run += __shfl_sync(0xffffffffu, incl, 31);
                     }
@@ -320,7 +337,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                         const int j = jg + idx;
                         const int s = j % NSV;
                         mbar_wait(v_empty + s, ((j / NSV) & 1) ^ 1);
-                        const int row0 = (fm.u * p.n_slots + (list[fm.e0 + idx] & 0xFFFFFF)) * 64;
+                        const int row0 = (fm.u * p.n_slots + list_slot(list, fm.e0 + idx)) * 64;
                         if (elect_one()) {
                             if (p.ablate == 2) {  // experiment: no K/V traffic
                                 mbar_arrive(v_full + s);
@@ -336,7 +353,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                         const int j = jg + idx;
                         const int s = j % NSK;
                         mbar_wait(k_empty + s, ((j / NSK) & 1) ^ 1);
-                        const int row0 = (fm.u * p.n_slots + (list[fm.e0 + idx] & 0xFFFFFF)) * 64;
+                        const int row0 = (fm.u * p.n_slots + list_slot(list, fm.e0 + idx)) * 64;
                         if (elect_one()) {
                             if (p.ablate == 2) {
                                 mbar_arrive(k_full + s);
@@ -449,7 +466,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         int jg = 0;
         for (int f = 0; f < n_frag; ++f) {
             const int lb = f & 1;
-            const int32_t* list = lists + lb * p.max_list;
+            const uint8_t* list = lists + static_cast<size_t>(lb) * p.max_list * esz;
             mbar_wait(list_full + lb, (f >> 1) & 1);
             const FragMeta fm = meta[lb];
             const int nf = fm.e1 - fm.e0;
@@ -459,7 +476,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 
             // ---------------------------------------------------------- online softmax
             float m = -INFINITY, l = 0.0f;
-            const uint32_t list_s = smem_u32(list + fm.e0);
+            const uint32_t list_s = smem_u32(list) + fm.e0 * esz;
             for (int idx = 0; idx < nf; ++idx) {
                 const int j = jg + idx;
                 const int buf = j & 1;
@@ -469,7 +486,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                 tc_fence_after();
                 const uint32_t t_s = t_o + L::kSColBase + buf * 64;
                 // rows of one warp all lie in one half -> visibility is warp-uniform
-                const bool vis = ((ld_shared_u32(list_s + idx * 4) >> (24 + half)) & 1) && p.ablate != 1;
+                const uint32_t ent = p.list16 ? ld_shared_u16(list_s + idx * 2) : ld_shared_u32(list_s + idx * 4);
+                const bool vis = ((ent >> (mshift + half)) & 1) && p.ablate != 1;
                 if (vis) {
                     uint32_t pk[32];
                     float sv[64];
@@ -745,12 +763,22 @@ int launch_impl(const bf16* q, const bf16* kp, const bf16* vp, BsaParams p, cuda
         if (!encode_tmap_bf16(&tv, vp, 2, dims, strides, box, &err))
             return set_error(PBSA_ECUDA, "tensor map V: " + err);
     }
-    const size_t smem = L::bytes(p.max_list, p.bm_words);
+    const size_t smem = L::bytes(p.max_list, p.bm_words, p.list16 ? 2 : 4);
     if (smem > 227 * 1024)
         return set_error(PBSA_EUNSUPPORTED, "bsa_fwd: visible list too long for shared memory");
     if (int rc = ensure_smem(reinterpret_cast<const void*>(bsa_fwd_kernel<D, NSK, NSV, B, POLY>), smem, "bsa_fwd"))
         return rc;
-    const int slots = 2 * num_sms();
+    // persistent grid = the CTAs that are actually co-resident: __launch_bounds__(kThreads, 2) keeps
+    // registers at two CTAs per SM, so shared memory decides
+    int per_sm = 2;
+    {
+        int dev = 0, sm_smem = 0, reserved = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+        cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+        if (sm_smem > 0 && 2 * (smem + static_cast<size_t>(reserved)) > static_cast<size_t>(sm_smem)) per_sm = 1;
+    }
+    const int slots = per_sm * num_sms();
     p.grid = p.n_tiles < slots ? p.n_tiles : slots;
     p.whole_waves = 0;
     p.tail_base = 0;
@@ -779,7 +807,7 @@ int launch_impl(const bf16* q, const bf16* kp, const bf16* vp, BsaParams p, cuda
 }  // namespace
 
 size_t bsa_fwd_workspace(int units, int nqb, int d) {
-    const size_t slots = 2 * static_cast<size_t>(2 * num_sms());
+    const size_t slots = kRing * static_cast<size_t>(2 * num_sms());
     const size_t tiles = static_cast<size_t>(units) * ((nqb + 1) / 2);
     return slots * 128 * d * 4 + slots * 256 * 4 + tiles * 4 + 256;
 }
@@ -821,6 +849,7 @@ int launch_bsa_fwd(const bf16* q, const bf16* k_pool, const bf16* v_pool, int n_
         p.trace = g_trace;
     }
     p.bm_words = (n_local + 31) / 32 + 1;
+    p.list16 = n_slots < 16384;
     p.max_list = n_dense + (p.k > 0 ? (2 * p.k < n_local ? 2 * p.k : n_local) : 0);
     p.tiles_per_unit = (nqb + 1) / 2;
     p.n_tiles = units * p.tiles_per_unit;
@@ -829,7 +858,7 @@ int launch_bsa_fwd(const bf16* q, const bf16* k_pool, const bf16* v_pool, int n_
     if (ws != nullptr) {
         if (ws_bytes < bsa_fwd_workspace(units, nqb, d))
             return set_error(PBSA_EINVAL, "bsa_fwd: workspace too small");
-        const size_t slots = 2 * static_cast<size_t>(2 * num_sms());
+        const size_t slots = kRing * static_cast<size_t>(2 * num_sms());
         p.part_o = static_cast<float*>(ws);
         p.part_ml = p.part_o + slots * 128 * d;
         p.counters = reinterpret_cast<int*>(p.part_ml + slots * 256);

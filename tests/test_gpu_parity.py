@@ -164,6 +164,11 @@ def test_bsa_fwd_growing_scores_rescale_path(pb):
     _bsa_case(pb, 1, 4, 64, 64, 10, 8, 3, seed=33, k_ramp=True)
 
 
+def test_bsa_fwd_wide_pool_32bit_lists(pb):
+    """>= 16384 pool slots: visible lists fall back to 32-bit entries."""
+    _bsa_case(pb, 1, 4, 60, 128, 10, 16390, 8, seed=23)
+
+
 def test_bsa_fwd_hybrid_two_waves_and_tail(pb):
     """Two full waves of whole tiles (2 x 296 CTA slots on a B200) then a stream-K tail."""
     _bsa_case(pb, 70, 17, 60, 128, 5, 12, 3, seed=22)
