@@ -277,6 +277,26 @@ def attention_sparse(q_blocks, k_store, v_store, vis, scale=None, qmask=None, wa
     return (out, lse) if want_lse else out
 
 
+def attention_sparse_backward(q_blocks, k_store, v_store, vis, d_out, scale=None):
+    """Gradients (dq [nqb, bq, d], dk, dv [n_store, bkv, d]) of attention_sparse for upstream
+    d_out [nqb, bq, d]; fp64 inside (see pbsa_oracle.h)."""
+    q, k, v, g = _f32(q_blocks), _f32(k_store), _f32(v_store), _f32(d_out)
+    nqb, bq, d = q.shape
+    n_store, bkv = k.shape[0], k.shape[1]
+    vis = np.ascontiguousarray(vis, np.int32)
+    n_vis = vis.shape[1]
+    scale = attention_scale(d) if scale is None else scale
+    dq = np.zeros((nqb, bq, d), np.float32)
+    dk = np.zeros((n_store, bkv, d), np.float32)
+    dv = np.zeros_like(dk)
+    L = lib()
+    L.orc_attention_sparse_backward.argtypes = [_f32p, _i64, _i64, _f32p, _f32p, _i64, _i32p, _i64, _i64,
+                                                C.c_float, _f32p, _f32p, _f32p, _f32p, _i64]
+    _chk(L.orc_attention_sparse_backward(q, nqb, bq, k, v, bkv, vis.reshape(-1) if n_vis else
+                                         np.zeros(1, np.int32), n_vis, d, scale, g, dq, dk, dv, n_store))
+    return dq, dk, dv
+
+
 def flop_count(nq, np_, nl, b, k_sel, d):
     dn, sp, r = C.c_double(), C.c_double(), C.c_double()
     L = lib()

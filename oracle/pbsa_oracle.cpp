@@ -376,6 +376,58 @@ int orc_attention_sparse(const float* q, int64_t nqb, int64_t bq, const float* k
     return 0;
 }
 
+int orc_attention_sparse_backward(const float* q, int64_t nqb, int64_t bq, const float* k, const float* v,
+                                  int64_t bkv, const int32_t* vis, int64_t n_vis, int64_t d, float scale,
+                                  const float* d_out, float* dq, float* dk, float* dv, int64_t n_store) {
+    if (nqb < 0 || bq <= 0 || bkv <= 0 || d <= 0 || n_vis < 0 || n_store < 0)
+        return fail("attention_sparse_backward: bad geometry");
+    std::vector<double> dk64(static_cast<size_t>(n_store * bkv * d), 0.0), dv64(dk64.size(), 0.0);
+    const int64_t nt = n_vis * bkv;
+    std::vector<double> s(static_cast<size_t>(nt)), p(s.size()), dp(s.size());
+    for (int64_t r = 0; r < nqb * bq; ++r) {  // sequential: dk / dv accumulate in row order
+        const int64_t qb = r / bq;
+        const float* qrow = q + r * d;
+        const float* grow = d_out + r * d;
+        double m = -std::numeric_limits<double>::infinity();
+        for (int64_t j = 0; j < n_vis; ++j)
+            for (int64_t t = 0; t < bkv; ++t) {
+                const int64_t g = vis[qb * n_vis + j];
+                const int64_t i = j * bkv + t;
+                s[i] = dot64(qrow, k + (g * bkv + t) * d, d) * static_cast<double>(scale);
+                dp[i] = dot64(grow, v + (g * bkv + t) * d, d);
+                m = std::max(m, s[i]);
+            }
+        double l = 0.0;
+        for (int64_t i = 0; i < nt; ++i) l += (p[i] = std::exp(s[i] - m));
+        double D = 0.0;
+        for (int64_t i = 0; i < nt; ++i) D += (p[i] /= l) * dp[i];
+        double* dqr = nullptr;
+        std::vector<double> dq64(static_cast<size_t>(d), 0.0);
+        dqr = dq64.data();
+        for (int64_t j = 0; j < n_vis; ++j) {
+            const int64_t g = vis[qb * n_vis + j];
+            for (int64_t t = 0; t < bkv; ++t) {
+                const int64_t i = j * bkv + t;
+                const double ds = p[i] * (dp[i] - D);
+                const float* kr = k + (g * bkv + t) * d;
+                double* dkr = dk64.data() + (g * bkv + t) * d;
+                double* dvr = dv64.data() + (g * bkv + t) * d;
+                for (int64_t c = 0; c < d; ++c) {
+                    dqr[c] += ds * kr[c];
+                    dkr[c] += ds * static_cast<double>(scale) * qrow[c];
+                    dvr[c] += p[i] * grow[c];
+                }
+            }
+        }
+        for (int64_t c = 0; c < d; ++c) dq[r * d + c] = static_cast<float>(dqr[c] * static_cast<double>(scale));
+    }
+    for (size_t i = 0; i < dk64.size(); ++i) {
+        dk[i] = static_cast<float>(dk64[i]);
+        dv[i] = static_cast<float>(dv64[i]);
+    }
+    return 0;
+}
+
 int orc_flop_count(int64_t nq, int64_t np, int64_t nl, int64_t b, int64_t k_sel, int64_t d,
                    double* dense, double* sparse, double* ratio) {
     if (nq <= 0 || b <= 0 || d <= 0 || np < 0 || nl < 0 || k_sel < 0)

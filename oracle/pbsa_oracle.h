@@ -86,6 +86,15 @@ int orc_attention_reference(const float* q, int64_t nq, const float* k, const fl
 int orc_attention_sparse(const float* q, int64_t nqb, int64_t bq, const float* k, const float* v,
                          int64_t bkv, const int32_t* vis, int64_t n_vis, int64_t d, float scale,
                          const uint8_t* qmask, float* out, float* lse);
+/* Gradient of attention_sparse (the reference ships no backward; this is the derivative of the
+ * dense masked attention SPEC.md:358-366 restricted to the visible blocks, i.e. of Eq. 3-5
+ * PAPER.md:128-143): dq, dk, dv for upstream d_out, all in fp64 (scores s = scale * q.k, p =
+ * softmax over the row's visible tokens, dP = d_out.v, D = sum p*dP, dS = p*(dP - D);
+ * dq = scale * sum dS k, dk = scale * sum dS q, dv = sum p d_out).  dk / dv [n_store, bkv, d]
+ * accumulate over every query row that sees the block (caller zero-initialises them). */
+int orc_attention_sparse_backward(const float* q, int64_t nqb, int64_t bq, const float* k, const float* v,
+                                  int64_t bkv, const int32_t* vis, int64_t n_vis, int64_t d, float scale,
+                                  const float* d_out, float* dq, float* dk, float* dv, int64_t n_store);
 /* SPEC.md:385-393 */
 int orc_flop_count(int64_t nq, int64_t np, int64_t nl, int64_t b, int64_t k_sel, int64_t d,
                    double* dense, double* sparse, double* ratio);

@@ -334,3 +334,30 @@ def test_flop_count_properties():
         k = max(1, math.ceil(nl // 64 * 0.0625))
         assert orc.flop_count(n_c, npt, nl, 64, k, 64)[2] > 1
     assert orc.kv_length(10752 // 2, 2, 0.25) - 10752 == 2688
+
+
+def test_attention_sparse_backward_matches_autograd():
+    """The backward oracle (no reference implementation exists) is pinned to the derivative of
+    the dense masked attention by torch autograd in float64."""
+    import torch
+    g = np.random.default_rng(11)
+    nqb, bq, bkv, d, n_store = 3, 5, 4, 8, 6
+    q = g.standard_normal((nqb, bq, d)).astype(np.float32)
+    k = g.standard_normal((n_store, bkv, d)).astype(np.float32)
+    v = g.standard_normal((n_store, bkv, d)).astype(np.float32)
+    do = g.standard_normal((nqb, bq, d)).astype(np.float32)
+    vis = np.array([[0, 2, 5], [1, 2, 3], [4, 0, 5]], np.int32)
+    dq, dk, dv = orc.attention_sparse_backward(q, k, v, vis, do)
+    qt = torch.tensor(q, dtype=torch.float64, requires_grad=True)
+    kt = torch.tensor(k, dtype=torch.float64, requires_grad=True)
+    vt = torch.tensor(v, dtype=torch.float64, requires_grad=True)
+    scale = orc.attention_scale(d)
+    outs = []
+    for i in range(nqb):
+        kk = kt[vis[i]].reshape(-1, d)
+        vv = vt[vis[i]].reshape(-1, d)
+        outs.append(torch.softmax(qt[i] @ kk.T * scale, -1) @ vv)
+    (torch.stack(outs) * torch.tensor(do, dtype=torch.float64)).sum().backward()
+    np.testing.assert_allclose(dq, qt.grad.numpy(), rtol=1e-5, atol=1e-6)
+    np.testing.assert_allclose(dk, kt.grad.numpy(), rtol=1e-5, atol=1e-6)
+    np.testing.assert_allclose(dv, vt.grad.numpy(), rtol=1e-5, atol=1e-6)

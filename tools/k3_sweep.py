@@ -29,7 +29,7 @@ for u in range(U):
     for t in range(0, nqb, 2):
         un += nd + len(set(sc[u, t].tolist()) | set(sc[u, t + 1].tolist()))
 exe = 4.0 * 128 * 64 * d * un
-for sk in (True, False):
+for sk in ((True,) if os.environ.get("PBSA_SWEEP_SK_ONLY") else (True, False)):
     for _ in range(3):
         pb.attention_sparse(q, kp, vp, dense, local, sel, b, stream_k=sk)
     torch.cuda.synchronize()
