@@ -76,6 +76,21 @@ int pbsa_bsa_fwd(const void* q, const void* k_pool, const void* v_pool, int n_sl
                  int k, int nqb, int b, int d, int units, float scale, void* o, float* lse,
                  void* workspace, size_t workspace_bytes, void* stream);
 
+/* (c') block-sparse attention backward -- the gradient of pbsa_bsa_fwd (the training path of
+ * Alg. 2; the reference has no backward, the oracle is the derivative of
+ * attention_sparse).  Inputs as pbsa_bsa_fwd plus the forward's o, its natural-log lse
+ * [units][n_q] and the upstream gradient d_o [units][n_q][d] bf16.  Outputs f32: dq
+ * [units][n_q][d]; dk_pool / dv_pool [units][n_slots][64][d] -- rows [0, b) of every slot in the
+ * dense list or the local window are written (zero if no query block saw it), other slots are left
+ * untouched.  workspace: pbsa_bsa_bwd_workspace() bytes (any contents). */
+size_t pbsa_bsa_bwd_workspace(int units, int nqb, int b, int n_local);
+int pbsa_bsa_bwd(const void* q, const void* k_pool, const void* v_pool, int n_slots,
+                 const int32_t* dense_slots, int dense_stride, int n_dense,
+                 const int32_t* local_slots, int local_stride, int n_local, const int32_t* sel,
+                 int k, int nqb, int b, int d, int units, float scale, const void* o, const void* d_o,
+                 const float* lse, float* dq, float* dk_pool, float* dv_pool, void* workspace,
+                 size_t workspace_bytes, void* stream);
+
 /* (d) persistent memory -- replaces memory.PersistentMemory / LocalWindow / push_chunk /
  * update_persistent / assemble_kv (Eq. 9).  Device-resident
  * state for `units` heads: the slot pools, representatives and the P / L / stage slot tables.

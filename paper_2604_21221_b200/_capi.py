@@ -47,6 +47,9 @@ _SIGS = {
     "pbsa_bsa_fwd_workspace": (C.c_size_t, [_i32, _i32, _i32]),
     "pbsa_bsa_fwd": (_i32, [_vp, _vp, _vp, _i32, _vp, _i32, _i32, _vp, _i32, _i32, _vp, _i32,
                             _i32, _i32, _i32, _i32, _f32, _vp, _vp, _vp, C.c_size_t, _vp]),
+    "pbsa_bsa_bwd_workspace": (C.c_size_t, [_i32, _i32, _i32, _i32]),
+    "pbsa_bsa_bwd": (_i32, [_vp, _vp, _vp, _i32, _vp, _i32, _i32, _vp, _i32, _i32, _vp, _i32,
+                            _i32, _i32, _i32, _i32, _f32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, C.c_size_t, _vp]),
     "pbsa_mem_create": (_i32, [C.POINTER(_vp), _i32, _i32, _i32, _i32, _i32, _i32]),
     "pbsa_mem_destroy": (_i32, [_vp]),
     "pbsa_mem_reset": (_i32, [_vp, _vp]),

@@ -256,6 +256,37 @@ size_t pbsa_bsa_fwd_workspace(int units, int nqb, int d) {
     return bsa_fwd_workspace(units, nqb, d);
 }
 
+size_t pbsa_bsa_bwd_workspace(int units, int nqb, int b, int n_local) {
+    if (units < 0 || nqb < 0 || b < 1 || b > 64 || n_local < 0) return 0;
+    return bsa_bwd_workspace(units, nqb, b, n_local);
+}
+
+int pbsa_bsa_bwd(const void* q, const void* k_pool, const void* v_pool, int n_slots,
+                 const int32_t* dense_slots, int dense_stride, int n_dense,
+                 const int32_t* local_slots, int local_stride, int n_local, const int32_t* sel,
+                 int k, int nqb, int b, int d, int units, float scale, const void* o, const void* d_o,
+                 const float* lse, float* dq, float* dk_pool, float* dv_pool, void* workspace,
+                 size_t workspace_bytes, void* stream) {
+    if (int rc = check_d(d)) return rc;
+    PBSA_REQUIRE(b >= 1 && b <= 64, "bsa_bwd: block size b must be in [1, 64]");
+    PBSA_REQUIRE(nqb >= 0 && units >= 0 && n_slots >= 1, "bsa_bwd: bad counts");
+    PBSA_REQUIRE(n_dense >= 0 && n_local >= 0 && k >= 0 && k <= n_local, "bsa_bwd: bad visibility counts");
+    PBSA_REQUIRE(n_dense == 0 || (dense_slots != nullptr && dense_stride >= n_dense), "bsa_bwd: dense list");
+    PBSA_REQUIRE(k == 0 || (local_slots != nullptr && sel != nullptr && local_stride >= n_local),
+                 "bsa_bwd: local list / selection");
+    PBSA_REQUIRE(static_cast<int64_t>(units) * n_slots * 64 < (int64_t(1) << 31), "bsa_bwd: pool too large for 32-bit TMA rows");
+    PBSA_REQUIRE(q && k_pool && v_pool && o && d_o && lse && dq && dk_pool && dv_pool && workspace,
+                 "bsa_bwd: null pointer");
+    PBSA_REQUIRE(aligned16(q) && aligned16(k_pool) && aligned16(v_pool) && aligned16(o) && aligned16(d_o) &&
+                     aligned16(dq) && aligned16(dk_pool) && aligned16(dv_pool) && aligned16(workspace),
+                 "bsa_bwd: tensors must be 16-byte aligned");
+    if (!(scale > 0.0f)) scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(d)));
+    return launch_bsa_bwd(static_cast<const bf16*>(q), static_cast<const bf16*>(k_pool), static_cast<const bf16*>(v_pool),
+                          n_slots, dense_slots, dense_stride, n_dense, local_slots, local_stride, n_local, sel, k, nqb,
+                          b, d, units, scale, static_cast<const bf16*>(o), static_cast<const bf16*>(d_o), lse, dq,
+                          dk_pool, dv_pool, workspace, workspace_bytes, as_stream(stream));
+}
+
 int pbsa_bsa_fwd(const void* q, const void* k_pool, const void* v_pool, int n_slots,
                  const int32_t* dense_slots, int dense_stride, int n_dense,
                  const int32_t* local_slots, int local_stride, int n_local, const int32_t* sel,

@@ -83,6 +83,13 @@ int launch_bsa_fwd(const bf16* q, const bf16* k_pool, const bf16* v_pool, int n_
                    int units, float scale, bf16* o, float* lse, void* ws, size_t ws_bytes, cudaStream_t s,
                    const LatentGeom* lat = nullptr);
 size_t bsa_fwd_workspace(int units, int nqb, int d);
+// K3 backward: dq [units][n_q][d], dk / dv [units][n_slots][64][d] f32 (rows of visible slots written)
+size_t bsa_bwd_workspace(int units, int nqb, int b, int n_local);
+int launch_bsa_bwd(const bf16* q, const bf16* k_pool, const bf16* v_pool, int n_slots, const int32_t* dense,
+                   int dense_stride, int n_dense, const int32_t* local, int local_stride, int n_local,
+                   const int32_t* sel, int k, int nqb, int b, int d, int units, float scale, const bf16* o,
+                   const bf16* d_o, const float* lse, float* dq, float* dk, float* dv, void* ws, size_t ws_bytes,
+                   cudaStream_t s);
 int launch_debug_tile(const bf16* q, const bf16* k, const bf16* v, int d, float* s_out,
                       float* o_out, cudaStream_t s);
 // K4

@@ -158,6 +158,38 @@ def _workspace(nbytes: int, device) -> torch.Tensor:
     return t
 
 
+def attention_sparse_backward(q: torch.Tensor, k_pool: torch.Tensor, v_pool: torch.Tensor,
+                              dense_slots: torch.Tensor | None, local_slots: torch.Tensor | None,
+                              sel: torch.Tensor | None, b: int, o: torch.Tensor, lse: torch.Tensor,
+                              d_o: torch.Tensor, scale: float | None = None):
+    """Gradient of attention_sparse (pbsa_bsa_bwd): returns (dq [units, n_q, d], dk_pool, dv_pool
+    [units, n_slots, 64, d]) in float32.  o / lse are the forward's outputs (want_lse=True)."""
+    for name, t in (("q", q), ("k_pool", k_pool), ("v_pool", v_pool), ("o", o), ("d_o", d_o)):
+        _need(t, torch.bfloat16, name)
+    _need(lse, torch.float32, "lse")
+    units, nq, d = q.shape
+    if nq % b:
+        raise PbsaError(f"attention_sparse_backward: n_q ({nq}) not divisible by b ({b})")
+    nqb, n_slots = nq // b, k_pool.shape[1]
+    nd = 0 if dense_slots is None else dense_slots.shape[1]
+    nl = 0 if local_slots is None else local_slots.shape[1]
+    k = 0 if sel is None else sel.shape[2]
+    for name, t in (("dense_slots", dense_slots), ("local_slots", local_slots), ("sel", sel)):
+        if t is not None:
+            _need(t, torch.int32, name)
+    dq = torch.empty(units, nq, d, device=q.device, dtype=torch.float32)
+    dk = torch.zeros(units, n_slots, 64, d, device=q.device, dtype=torch.float32)
+    dv = torch.zeros_like(dk)
+    ws = torch.empty(max(1, LIB.pbsa_bsa_bwd_workspace(units, nqb, b, nl)), dtype=torch.uint8, device=q.device)
+    scale = attention_scale(d) if scale is None else scale
+    check(LIB.pbsa_bsa_bwd(q.data_ptr(), k_pool.data_ptr(), v_pool.data_ptr(), n_slots, _ptr(dense_slots),
+                           nd if dense_slots is None else dense_slots.stride(0), nd, _ptr(local_slots),
+                           nl if local_slots is None else local_slots.stride(0), nl, _ptr(sel), k, nqb, b, d,
+                           units, float(scale), o.data_ptr(), d_o.data_ptr(), lse.data_ptr(), dq.data_ptr(),
+                           dk.data_ptr(), dv.data_ptr(), ws.data_ptr(), ws.numel(), _stream()))
+    return dq, dk, dv
+
+
 def debug_tile(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor):
     """One 128x64 tile through the tcgen05 path: returns (q k^T f32, bf16(q k^T) v f32)."""
     d = q.shape[1]

@@ -351,3 +351,51 @@ def test_attend_latent_matches_blocked_wan_blocks(pb):
     """(1, 15, 4) = 60-token blocks of the Wan-1.3B layout, d = 64 variant with 3-frame chunks."""
     _latent_vs_blocked(pb, batch=1, heads=3, d=64, T=3, H=30, W=8, blk=(1, 15, 4), C=24, Wc=2, n_chunks=4,
                        k_top=4, seed=42)
+
+
+# ------------------------------------------------------------------ (c') backward
+def _bsa_bwd_case(pb, units, nqb, b, d, n_dense, n_local, k, seed, report=False):
+    g = np.random.default_rng(seed)
+    n_slots = n_dense + n_local + 3
+    kp = np.zeros((units, n_slots, 64, d), np.float32)
+    vp = np.zeros((units, n_slots, 64, d), np.float32)
+    kp[:, :, :b] = normal_bf16(seed + 1, (units, n_slots, b, d))
+    vp[:, :, :b] = normal_bf16(seed + 2, (units, n_slots, b, d))
+    q = normal_bf16(seed + 3, (units, nqb * b, d))
+    do = normal_bf16(seed + 4, (units, nqb * b, d))
+    perm = np.stack([g.permutation(n_slots) for _ in range(units)]).astype(np.int32)
+    dense = np.ascontiguousarray(perm[:, :n_dense])
+    local = np.ascontiguousarray(perm[:, n_dense:n_dense + n_local])
+    sel = np.stack([np.stack([np.sort(g.choice(n_local, k, replace=False)) for _ in range(nqb)])
+                    for _ in range(units)]).astype(np.int32) if k else None
+    args = (dev(q), dev(kp), dev(vp), dev(dense, torch.int32) if n_dense else None,
+            dev(local, torch.int32) if n_local else None, dev(sel, torch.int32) if k else None, b)
+    o, lse = pb.attention_sparse(*args, want_lse=True)
+    dq, dk, dv = pb.attention_sparse_backward(*args, o, lse, dev(do))
+    torch.cuda.synchronize()
+    dq, dk, dv = dq.cpu().numpy(), dk.cpu().numpy(), dv.cpu().numpy()
+    worst = 0.0
+    for u in range(units):
+        vis = np.stack([np.concatenate([dense[u], local[u][sel[u][i]] if k else np.zeros(0, np.int32)])
+                        for i in range(nqb)]).astype(np.int32)
+        rq, rk, rv = orc.attention_sparse_backward(q[u].reshape(nqb, b, d), kp[u][:, :b], vp[u][:, :b], vis,
+                                                    do[u].reshape(nqb, b, d))
+        for name, got, want in (("dq", dq[u].reshape(nqb, b, d), rq), ("dk", dk[u][:, :b], rk), ("dv", dv[u][:, :b], rv)):
+            err = np.abs(got - want)
+            ref = max(np.abs(want).max(), 1e-6)
+            worst = max(worst, err.max() / ref)
+            if report:
+                print(name, u, "max", err.max() / ref, "mean", err.mean() / ref)
+            # bf16 operands (Q, K, V, dO, P, dS) with fp32 accumulation vs an fp64 oracle
+            assert err.max() <= 1e-2 * ref and err.mean() <= 1e-3 * ref, (name, u, err.max(), err.mean(), ref)
+    return worst
+
+
+@pytest.mark.parametrize("d,b", [(128, 60), (64, 64), (128, 17)])
+def test_bsa_bwd_parity(pb, d, b):
+    _bsa_bwd_case(pb, 2, 5, b, d, 6, 16, 4, seed=50 + d + b)
+
+
+def test_bsa_bwd_dense_only_and_odd_pairs(pb):
+    _bsa_bwd_case(pb, 2, 4, 60, 128, 7, 0, 0, seed=61)     # no local window, odd dense count
+    _bsa_bwd_case(pb, 1, 3, 60, 128, 5, 9, 9, seed=62)     # k = N_l, odd local count
