@@ -28,7 +28,14 @@
 namespace pbsa {
 namespace {
 
-constexpr int kBwdThreads = 192;
+// B-operand ring depth: a stage is held from its TMA load until the block's LAST MMA (dQ, or dV/dK)
+// completes -- two blocks of work later -- so two stages left the MMA warp waiting on TMA latency
+// every block; four keep the loads a full block ahead.
+constexpr int kNS = 4;
+constexpr int kBwdThreads = 320;  // warp 0 producer, warp 1 MMA, warps 2-9 elementwise
+constexpr int kEw = 8;             // elementwise warps: warp w reads TMEM lane quarter w % 4 and
+                                   // column half (w - 2) / 4 -- every element is independent (lse is
+                                   // known, no row reduction), so the halves never synchronise
 constexpr uint32_t kBwdTmemCols = 512;
 
 struct BwdParams {
@@ -85,6 +92,10 @@ __global__ void bwd_inv_kernel(const int32_t* __restrict__ sel, int units, int n
     atomicOr(inv + (static_cast<int64_t>(u) * n_local + l) * words + (i >> 5), 1u << (i & 31));
 }
 
+// TMEM column of the packed bf16 K16 step kk of a 64-key P / dS tile: the elementwise warp of column
+// half h writes its 16 packed columns at [32 h, 32 h + 16) -- inside the fp32 columns it read
+__device__ __forceinline__ uint32_t kA(int kk) { return kk < 2 ? kk * 8 : 32 + (kk - 2) * 8; }
+
 // shared-memory layout of both tcgen05 kernels: A tile (128 rows) x2, B stages, barriers, list
 template <int D>
 struct BwdLayout {
@@ -95,10 +106,10 @@ struct BwdLayout {
     // dkdv: A0 = K pair, A1 = V pair, B stages = Q x2, dO x2 (+ lse/D rows per stage)
     static constexpr uint32_t kOffA0 = 0;
     static constexpr uint32_t kOffA1 = kOffA0 + kTile;
-    static constexpr uint32_t kOffB = kOffA1 + kTile;  // [4 stages] x kBlk: stage s of operand x at (2x + s)
-    static constexpr uint32_t kOffRow = kOffB + 4 * kBlk;       // [2 stages][2][64] f32 (dkdv: lse2, D)
-    static constexpr uint32_t kOffBar = kOffRow + 2 * 2 * 64 * 4;
-    static constexpr int kNumBars = 24;
+    static constexpr uint32_t kOffB = kOffA1 + kTile;  // [2 operands][kNS stages] x kBlk
+    static constexpr uint32_t kOffRow = kOffB + 2 * kNS * kBlk;  // [kNS stages][2][64] f32 (dkdv: lse2, D)
+    static constexpr uint32_t kOffBar = kOffRow + kNS * 2 * 64 * 4;
+    static constexpr int kNumBars = 32;
     static constexpr uint32_t kOffMeta = kOffBar + kNumBars * 8;  // [2][4] ints
     static constexpr uint32_t kOffMisc = kOffMeta + 2 * 4 * 4;
     static constexpr uint32_t kOffList = kOffMisc + 16;
@@ -118,21 +129,21 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* q_s = smem + L::kOffA0;
     uint8_t* do_s = smem + L::kOffA1;
-    uint8_t* k_s = smem + L::kOffB;              // stages 0, 1
-    uint8_t* v_s = smem + L::kOffB + 2 * L::kBlk;  // stages 0, 1
+    uint8_t* k_s = smem + L::kOffB;                  // [kNS] stages
+    uint8_t* v_s = smem + L::kOffB + kNS * L::kBlk;  // [kNS] stages
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kOffBar);
     uint64_t* q_full = bars + 0;
     uint64_t* q_empty = bars + 1;
-    uint64_t* k_full = bars + 2;   // [2]
-    uint64_t* k_empty = bars + 4;  // [2]
-    uint64_t* v_full = bars + 6;   // [2]
-    uint64_t* v_empty = bars + 8;  // [2]
-    uint64_t* s_full = bars + 10;  // [2]
-    uint64_t* p_full = bars + 12;  // [2]
-    uint64_t* dq_done = bars + 14;
-    uint64_t* dq_free = bars + 15;
-    uint64_t* list_full = bars + 16;   // [2]
-    uint64_t* list_empty = bars + 18;  // [2]
+    uint64_t* k_full = bars + 2;             // [kNS]
+    uint64_t* k_empty = k_full + kNS;        // [kNS]
+    uint64_t* v_full = k_empty + kNS;        // [kNS]
+    uint64_t* v_empty = v_full + kNS;        // [kNS]
+    uint64_t* s_full = v_empty + kNS;        // [2]
+    uint64_t* p_full = s_full + 2;           // [2]
+    uint64_t* dq_done = p_full + 2;
+    uint64_t* dq_free = dq_done + 1;
+    uint64_t* list_full = dq_free + 1;       // [2]
+    uint64_t* list_empty = list_full + 2;    // [2]
     int* meta = reinterpret_cast<int*>(smem + L::kOffMeta);  // [2][4]: n, u, qb0, has2
     uint32_t* misc = reinterpret_cast<uint32_t*>(smem + L::kOffMisc);
     int32_t* lists = reinterpret_cast<int32_t*>(smem + L::kOffList);
@@ -142,12 +153,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const int n_frag = blockIdx.x < p.n_tiles ? (p.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
     if (warp == 0 && lane == 0) {
-        for (int i = 0; i < 20; ++i) mbar_init(bars + i, 1);
+        for (int i = 0; i < 2 + 4 * kNS + 8; ++i) mbar_init(bars + i, 1);
         for (int s = 0; s < 2; ++s) {
-            mbar_init(p_full + s, 4);
-            mbar_init(list_empty + s, 5);
+            mbar_init(p_full + s, kEw);
+            mbar_init(list_empty + s, kEw + 1);
         }
-        mbar_init(dq_free, 4);
+        mbar_init(dq_free, kEw);
         fence_barrier_init();
         tma_prefetch(&tm_q);
         tma_prefetch(&tm_do);
@@ -157,7 +168,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     if (warp == 1) tmem_alloc<kBwdTmemCols>(misc);
     if (warp >= 2) {  // Q / dO padding rows (>= b of each half) stay zero: TMA writes rows < b only
         const int t = threadIdx.x - 64;
-        for (int e = t; e < 2 * 128 * L::kHalves * 8; e += 128) {
+        for (int e = t; e < 2 * 128 * L::kHalves * 8; e += kEw * 32) {
             const int chunk = e & 7, rh = (e >> 3) % (128 * L::kHalves), which = (e >> 3) / (128 * L::kHalves);
             const int h = rh % L::kHalves, row = rh / L::kHalves;
             if ((row & 63) >= p.b)
@@ -235,15 +246,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             }
             __syncwarp();
             for (int idx = 0; idx < nf; ++idx) {
-                const int j = jg + idx, s = j & 1;
+                const int j = jg + idx, s = j % kNS, ph = (j / kNS) & 1;
                 const int row0 = (u * p.n_slots + (list[idx] & 0xFFFFFF)) * 64;
-                mbar_wait(k_empty + s, ((j >> 1) & 1) ^ 1);
+                mbar_wait(k_empty + s, ph ^ 1);
                 if (elect_one()) {
                     mbar_arrive_expect_tx(k_full + s, L::kBlk);
                     for (int h = 0; h < L::kHalves; ++h) tma_load_2d(k_s + s * L::kBlk + h * 8192, &tm_k, k_full + s, h * 64, row0);
                 }
                 __syncwarp();
-                mbar_wait(v_empty + s, ((j >> 1) & 1) ^ 1);
+                mbar_wait(v_empty + s, ph ^ 1);
                 if (elect_one()) {
                     mbar_arrive_expect_tx(v_full + s, L::kBlk);
                     for (int h = 0; h < L::kHalves; ++h) tma_load_2d(v_s + s * L::kBlk + h * 8192, &tm_v, v_full + s, h * 64, row0);
@@ -276,19 +287,19 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 mbar_wait(p_full + b, (x >> 1) & 1);
                 tc_fence_after();
                 const uint32_t a_tmem = tmem + 128 + b * 128;  // dS_x (bf16 pairs) over S_x
-                const uint64_t kd = kmn + (((x & 1) * L::kBlk) >> 4);
+                const uint64_t kd = kmn + (((x % kNS) * L::kBlk) >> 4);
                 if (elect_one()) {
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk)
-                        mma_ts(tmem, a_tmem + kk * 8, kd + ((kk * 2048) >> 4), idesc_o, (!first || kk > 0) ? 1u : 0u);
-                    mma_commit(k_empty + (x & 1));
+                        mma_ts(tmem, a_tmem + kA(kk), kd + ((kk * 2048) >> 4), idesc_o, (!first || kk > 0) ? 1u : 0u);
+                    mma_commit(k_empty + x % kNS);
                 }
                 __syncwarp();
             };
             for (int idx = 0; idx < nf; ++idx) {
-                const int j = jg + idx, s = j & 1, b = j & 1;
-                mbar_wait(k_full + s, (j >> 1) & 1);
-                mbar_wait(v_full + s, (j >> 1) & 1);
+                const int j = jg + idx, s = j % kNS, b = j & 1;
+                mbar_wait(k_full + s, (j / kNS) & 1);
+                mbar_wait(v_full + s, (j / kNS) & 1);
                 tc_fence_after();
                 const uint32_t st = tmem + 128 + b * 128, dpt = st + 64;
                 const uint64_t kd = kdesc + ((s * L::kBlk) >> 4), vd = vdesc + ((s * L::kBlk) >> 4);
@@ -316,9 +327,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
     } else {
         // ================================================= dS (thread = query row = TMEM lane)
-        const int quarter = warp & 3, r = quarter * 32 + lane, half = r >> 6, rr = r & 63;
+        const int quarter = warp & 3, ch = (warp - 2) >> 2, r = quarter * 32 + lane, half = r >> 6, rr = r & 63;
         const uint32_t t_row = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
         const float2 scl2 = make_float2(p.scale_log2, p.scale_log2);
+        constexpr int DH = D / 2;  // dQ columns of this warp
         int jg = 0;
         for (int f = 0; f < n_frag; ++f) {
             const int lb = f & 1;
@@ -336,28 +348,27 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 const int j = jg + idx, b = j & 1;
                 mbar_wait(s_full + b, (j >> 1) & 1);
                 tc_fence_after();
-                const uint32_t ts = t_row + 128 + b * 128;
+                const uint32_t ts = t_row + 128 + b * 128 + ch * 32;  // this warp's 32 key columns
                 const bool vis = (list[idx] >> (24 + half)) & 1;
-                uint32_t pk[32];
+                uint32_t pk[16];
                 if (vis) {
-                    float sv[64], dp[64];
+                    float sv[32], dp[32];
                     tmem_ld32(ts, *reinterpret_cast<uint32_t(*)[32]>(sv));
-                    tmem_ld32(ts + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
                     tmem_ld32(ts + 64, *reinterpret_cast<uint32_t(*)[32]>(dp));
-                    tmem_ld32(ts + 96, *reinterpret_cast<uint32_t(*)[32]>(dp + 32));
                     tmem_wait_ld();
 #pragma unroll
-                    for (int c2 = 0; c2 < 32; ++c2) {
+                    for (int c2 = 0; c2 < 16; ++c2) {
+                        const int c = ch * 32 + 2 * c2;
                         const float2 x = __ffma2_rn(make_float2(sv[2 * c2], sv[2 * c2 + 1]), scl2, nl2);
-                        float p0 = 2 * c2 < p.b ? exp2_approx(x.x) : 0.0f;
-                        float p1 = 2 * c2 + 1 < p.b ? exp2_approx(x.y) : 0.0f;
+                        const float p0 = c < p.b ? exp2_approx(x.x) : 0.0f;
+                        const float p1 = c + 1 < p.b ? exp2_approx(x.y) : 0.0f;
                         pk[c2] = pack_bf16x2(p0 * (dp[2 * c2] - dd), p1 * (dp[2 * c2 + 1] - dd));
                     }
                 } else {
 #pragma unroll
-                    for (int c = 0; c < 32; ++c) pk[c] = 0u;
+                    for (int c = 0; c < 16; ++c) pk[c] = 0u;
                 }
-                tmem_st32(ts, pk);
+                tmem_st16(ts, pk);  // dS (bf16 pairs) over the fp32 S columns this warp read
                 tmem_wait_st();
                 tc_fence_before();
                 __syncwarp();
@@ -368,7 +379,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             mbar_wait(dq_done, f & 1);
             tc_fence_after();
 #pragma unroll 1
-            for (int c0 = 0; c0 < D; c0 += 32) {
+            for (int c0 = ch * DH; c0 < ch * DH + DH; c0 += 32) {
                 uint32_t ov[32];
                 if (nf > 0) {
                     tmem_ld32(t_row + c0, ov);
@@ -413,20 +424,20 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* kp_s = smem + L::kOffA0;
     uint8_t* vp_s = smem + L::kOffA1;
-    uint8_t* q_s = smem + L::kOffB;               // stages 0, 1
-    uint8_t* do_s = smem + L::kOffB + 2 * L::kBlk;  // stages 0, 1
+    uint8_t* q_s = smem + L::kOffB;                   // [kNS] stages
+    uint8_t* do_s = smem + L::kOffB + kNS * L::kBlk;  // [kNS] stages
     float* rows_s = reinterpret_cast<float*>(smem + L::kOffRow);  // [stage][lse2 | D][64]
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::kOffBar);
     uint64_t* kv_full = bars + 0;
     uint64_t* kv_empty = bars + 1;
-    uint64_t* q_full = bars + 2;   // [2]
-    uint64_t* q_empty = bars + 4;  // [2]
-    uint64_t* s_full = bars + 6;   // [2]
-    uint64_t* p_full = bars + 8;   // [2]
-    uint64_t* acc_done = bars + 10;
-    uint64_t* acc_free = bars + 11;
-    uint64_t* list_full = bars + 12;   // [2]
-    uint64_t* list_empty = bars + 14;  // [2]
+    uint64_t* q_full = bars + 2;            // [kNS]
+    uint64_t* q_empty = q_full + kNS;       // [kNS]
+    uint64_t* s_full = q_empty + kNS;       // [2]
+    uint64_t* p_full = s_full + 2;          // [2]
+    uint64_t* acc_done = p_full + 2;
+    uint64_t* acc_free = acc_done + 1;
+    uint64_t* list_full = acc_free + 1;     // [2]
+    uint64_t* list_empty = list_full + 2;   // [2]
     int* meta = reinterpret_cast<int*>(smem + L::kOffMeta);  // [2][4]: n, u, slot A, slot B (-1)
     uint32_t* misc = reinterpret_cast<uint32_t*>(smem + L::kOffMisc);
     int32_t* lists = reinterpret_cast<int32_t*>(smem + L::kOffList);
@@ -435,12 +446,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const int n_frag = blockIdx.x < p.n_items ? (p.n_items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
     if (warp == 0 && lane == 0) {
-        for (int i = 0; i < 16; ++i) mbar_init(bars + i, 1);
+        for (int i = 0; i < 2 + 2 * kNS + 10; ++i) mbar_init(bars + i, 1);
         for (int s = 0; s < 2; ++s) {
-            mbar_init(p_full + s, 4);
-            mbar_init(list_empty + s, 5);
+            mbar_init(p_full + s, kEw);
+            mbar_init(list_empty + s, kEw + 1);
         }
-        mbar_init(acc_free, 4);
+        mbar_init(acc_free, kEw);
         fence_barrier_init();
         tma_prefetch(&tm_q);
         tma_prefetch(&tm_do);
@@ -450,8 +461,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     if (warp == 1) tmem_alloc<kBwdTmemCols>(misc);
     if (warp >= 2) {  // Q / dO stages: rows >= b stay zero (finite operands for the masked columns)
         const int t = threadIdx.x - 64;
-        for (int e = t; e < 4 * 64 * L::kHalves * 8; e += 128) {
-            const int chunk = e & 7, rh = e >> 3;  // rh over [stage 4][half][row 64]
+        for (int e = t; e < 2 * kNS * 64 * L::kHalves * 8; e += kEw * 32) {
+            const int chunk = e & 7, rh = e >> 3;  // rh over [2 kNS stages][half][row 64]
             const int row = rh % 64, hs = rh / 64;
             if (row >= p.b) *reinterpret_cast<uint4*>(q_s + hs * 8192 + row * 128 + chunk * 16) = make_uint4(0, 0, 0, 0);
         }
@@ -531,9 +542,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             __syncwarp();
             const uint32_t qbytes = L::kHalves * static_cast<uint32_t>(p.b) * 128u;
             for (int idx = 0; idx < run; ++idx) {
-                const int j = jg + idx, s = j & 1;
+                const int j = jg + idx, s = j % kNS;
                 const int qb = list[idx] & 0xFFFFFF;
-                mbar_wait(q_empty + s, ((j >> 1) & 1) ^ 1);
+                mbar_wait(q_empty + s, ((j / kNS) & 1) ^ 1);
                 if (elect_one()) {
                     mbar_arrive_expect_tx(q_full + s, 2 * qbytes + 2 * 256);
                     for (int h = 0; h < L::kHalves; ++h) {
@@ -569,26 +580,26 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             mbar_wait(kv_full, f & 1);
             tc_fence_after();
             auto issue_acc = [&](int x, bool first) {
-                const int b = x & 1;
+                const int b = x & 1, sx = x % kNS;
                 mbar_wait(p_full + b, (x >> 1) & 1);
                 tc_fence_after();
                 const uint32_t pt = tmem + 256 + b * 128, dst = pt + 64;  // P^T, dS^T (bf16 pairs)
-                const uint64_t qd = qmn + ((b * L::kBlk) >> 4), dd = domn + ((b * L::kBlk) >> 4);
+                const uint64_t qd = qmn + ((sx * L::kBlk) >> 4), dd = domn + ((sx * L::kBlk) >> 4);
                 if (elect_one()) {
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
-                        mma_ts(tmem + 128, pt + kk * 8, dd + ((kk * 2048) >> 4), idesc_o, (!first || kk > 0) ? 1u : 0u);
-                        mma_ts(tmem, dst + kk * 8, qd + ((kk * 2048) >> 4), idesc_o, (!first || kk > 0) ? 1u : 0u);
+                        mma_ts(tmem + 128, pt + kA(kk), dd + ((kk * 2048) >> 4), idesc_o, (!first || kk > 0) ? 1u : 0u);
+                        mma_ts(tmem, dst + kA(kk), qd + ((kk * 2048) >> 4), idesc_o, (!first || kk > 0) ? 1u : 0u);
                     }
-                    mma_commit(q_empty + b);
+                    mma_commit(q_empty + sx);
                 }
                 __syncwarp();
             };
             for (int idx = 0; idx < nf; ++idx) {
-                const int j = jg + idx, s = j & 1;
-                mbar_wait(q_full + s, (j >> 1) & 1);
+                const int j = jg + idx, s = j % kNS, b = j & 1;
+                mbar_wait(q_full + s, (j / kNS) & 1);
                 tc_fence_after();
-                const uint32_t st = tmem + 256 + s * 128, dpt = st + 64;
+                const uint32_t st = tmem + 256 + b * 128, dpt = st + 64;
                 const uint64_t qd = qdesc + ((s * L::kBlk) >> 4), dd = dodesc + ((s * L::kBlk) >> 4);
                 if (elect_one()) {
 #pragma unroll
@@ -598,7 +609,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                         mma_ss(st, kdesc + oa, qd + ob, idesc_s, kk > 0 ? 1u : 0u);
                         mma_ss(dpt, vdesc + oa, dd + ob, idesc_s, kk > 0 ? 1u : 0u);
                     }
-                    mma_commit(s_full + s);
+                    mma_commit(s_full + b);
                 }
                 __syncwarp();
                 if (idx > 0) issue_acc(j - 1, idx == 1);
@@ -613,8 +624,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
     } else {
         // ================================================= P^T, dS^T (thread = key row = TMEM lane)
-        const int quarter = warp & 3, r = quarter * 32 + lane, half = r >> 6, rr = r & 63;
+        const int quarter = warp & 3, ch = (warp - 2) >> 2, r = quarter * 32 + lane, half = r >> 6, rr = r & 63;
         const uint32_t t_row = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+        constexpr int DH = D / 2;
         int jg = 0;
         for (int f = 0; f < n_frag; ++f) {
             const int lb = f & 1;
@@ -624,53 +636,52 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             const int slot = half ? sb : sa;
             const bool kvalid = rr < p.b && slot >= 0;
             for (int idx = 0; idx < nf; ++idx) {
-                const int j = jg + idx, s = j & 1;
-                mbar_wait(s_full + s, (j >> 1) & 1);
+                const int j = jg + idx, bb = j & 1, s = j % kNS;
+                mbar_wait(s_full + bb, (j >> 1) & 1);
                 tc_fence_after();
-                const uint32_t ts = t_row + 256 + s * 128;
+                const uint32_t ts = t_row + 256 + bb * 128 + ch * 32;  // this warp's 32 query columns
                 const bool vis = (list[idx] >> (24 + half)) & 1;
-                uint32_t pp[32], pd[32];
+                uint32_t pp[16], pd[16];
                 if (vis) {
-                    float sv[64], dp[64];
+                    float sv[32], dp[32];
                     tmem_ld32(ts, *reinterpret_cast<uint32_t(*)[32]>(sv));
-                    tmem_ld32(ts + 32, *reinterpret_cast<uint32_t(*)[32]>(sv + 32));
                     tmem_ld32(ts + 64, *reinterpret_cast<uint32_t(*)[32]>(dp));
-                    tmem_ld32(ts + 96, *reinterpret_cast<uint32_t(*)[32]>(dp + 32));
                     tmem_wait_ld();
-                    const float* l2 = rows_s + s * 128;
+                    const float* l2 = rows_s + s * 128 + ch * 32;
                     const float* dd = l2 + 64;
 #pragma unroll
-                    for (int c2 = 0; c2 < 32; ++c2) {
+                    for (int c2 = 0; c2 < 16; ++c2) {
+                        const int c = ch * 32 + 2 * c2;
                         const float2 lq = *reinterpret_cast<const float2*>(l2 + 2 * c2);
                         const float2 dq = *reinterpret_cast<const float2*>(dd + 2 * c2);
                         const float x0 = fmaf(sv[2 * c2], p.scale_log2, -lq.x), x1 = fmaf(sv[2 * c2 + 1], p.scale_log2, -lq.y);
-                        const float p0 = (kvalid && 2 * c2 < p.b) ? exp2_approx(x0) : 0.0f;
-                        const float p1 = (kvalid && 2 * c2 + 1 < p.b) ? exp2_approx(x1) : 0.0f;
+                        const float p0 = (kvalid && c < p.b) ? exp2_approx(x0) : 0.0f;
+                        const float p1 = (kvalid && c + 1 < p.b) ? exp2_approx(x1) : 0.0f;
                         pp[c2] = pack_bf16x2(p0, p1);
                         pd[c2] = pack_bf16x2(p0 * (dp[2 * c2] - dq.x), p1 * (dp[2 * c2 + 1] - dq.y));
                     }
                 } else {
 #pragma unroll
-                    for (int c = 0; c < 32; ++c) pp[c] = pd[c] = 0u;
+                    for (int c = 0; c < 16; ++c) pp[c] = pd[c] = 0u;
                 }
-                tmem_st32(ts, pp);
-                tmem_st32(ts + 64, pd);
+                tmem_st16(ts, pp);
+                tmem_st16(ts + 64, pd);
                 tmem_wait_st();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(p_full + s);
+                if (lane == 0) mbar_arrive(p_full + bb);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(list_empty + lb);
             mbar_wait(acc_done, f & 1);
             tc_fence_after();
-            // dK = scale * acc[0, D), dV = acc[128, 128 + D): rows of this item's slots
+            // dK = scale * acc[0, D), dV = acc[128, 128 + D): this warp's column half of its rows
 #pragma unroll 1
             for (int which = 0; which < 2; ++which) {
                 float* outp = which ? p.dv : p.dk;
                 const float mul = which ? 1.0f : p.scale;
 #pragma unroll 1
-                for (int c0 = 0; c0 < D; c0 += 32) {
+                for (int c0 = ch * DH; c0 < ch * DH + DH; c0 += 32) {
                     uint32_t ov[32];
                     if (nf > 0) {
                         tmem_ld32(t_row + which * 128 + c0, ov);
