@@ -32,6 +32,7 @@ namespace {
 // completes -- two blocks of work later -- so two stages left the MMA warp waiting on TMA latency
 // every block; four keep the loads a full block ahead.
 constexpr int kNS = 4;
+constexpr int kSB = 3;  // dQ kernel: S/dP TMEM buffers (dQ 128 + 3 x 128 columns)
 constexpr int kBwdThreads = 320;  // warp 0 producer, warp 1 MMA, warps 2-9 elementwise
 constexpr int kEw = 8;             // elementwise warps: warp w reads TMEM lane quarter w % 4 and
                                    // column half (w - 2) / 4 -- every element is independent (lse is
@@ -138,9 +139,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     uint64_t* k_empty = k_full + kNS;        // [kNS]
     uint64_t* v_full = k_empty + kNS;        // [kNS]
     uint64_t* v_empty = v_full + kNS;        // [kNS]
-    uint64_t* s_full = v_empty + kNS;        // [2]
-    uint64_t* p_full = s_full + 2;           // [2]
-    uint64_t* dq_done = p_full + 2;
+    uint64_t* s_full = v_empty + kNS;        // [kSB]
+    uint64_t* p_full = s_full + kSB;         // [kSB]
+    uint64_t* dq_done = p_full + kSB;
     uint64_t* dq_free = dq_done + 1;
     uint64_t* list_full = dq_free + 1;       // [2]
     uint64_t* list_empty = list_full + 2;    // [2]
@@ -153,11 +154,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const int n_frag = blockIdx.x < p.n_tiles ? (p.n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
     if (warp == 0 && lane == 0) {
-        for (int i = 0; i < 2 + 4 * kNS + 8; ++i) mbar_init(bars + i, 1);
-        for (int s = 0; s < 2; ++s) {
-            mbar_init(p_full + s, kEw);
-            mbar_init(list_empty + s, kEw + 1);
-        }
+        for (int i = 0; i < 2 + 4 * kNS + 2 * kSB + 6; ++i) mbar_init(bars + i, 1);
+        for (int s = 0; s < kSB; ++s) mbar_init(p_full + s, kEw);
+        for (int s = 0; s < 2; ++s) mbar_init(list_empty + s, kEw + 1);
         mbar_init(dq_free, kEw);
         fence_barrier_init();
         tma_prefetch(&tm_q);
@@ -283,8 +282,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             mbar_wait(q_full, f & 1);
             tc_fence_after();
             auto issue_dq = [&](int x, bool first) {
-                const int b = x & 1;
-                mbar_wait(p_full + b, (x >> 1) & 1);
+                const int b = x % kSB;
+                mbar_wait(p_full + b, (x / kSB) & 1);
                 tc_fence_after();
                 const uint32_t a_tmem = tmem + 128 + b * 128;  // dS_x (bf16 pairs) over S_x
                 const uint64_t kd = kmn + (((x % kNS) * L::kBlk) >> 4);
@@ -297,7 +296,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 __syncwarp();
             };
             for (int idx = 0; idx < nf; ++idx) {
-                const int j = jg + idx, s = j % kNS, b = j & 1;
+                const int j = jg + idx, s = j % kNS, b = j % kSB;
                 mbar_wait(k_full + s, (j / kNS) & 1);
                 mbar_wait(v_full + s, (j / kNS) & 1);
                 tc_fence_after();
@@ -315,9 +314,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     mma_commit(s_full + b);
                 }
                 __syncwarp();
-                if (idx > 0) issue_dq(j - 1, idx == 1);
+                if (idx >= kSB - 1) issue_dq(j - (kSB - 1), idx == kSB - 1);  // kSB - 1 blocks of lookahead
             }
-            if (nf > 0) issue_dq(jg + nf - 1, nf == 1);
+            for (int x = (nf > kSB - 1 ? nf - (kSB - 1) : 0); x < nf; ++x) issue_dq(jg + x, x == 0);
             if (elect_one()) {
                 mma_commit(q_empty);
                 mma_commit(dq_done);
@@ -345,8 +344,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             const float dd = valid ? __ldg(p.drow + prow) : 0.0f;
             const float2 nl2 = make_float2(-lse2, -lse2);
             for (int idx = 0; idx < nf; ++idx) {
-                const int j = jg + idx, b = j & 1;
-                mbar_wait(s_full + b, (j >> 1) & 1);
+                const int j = jg + idx, b = j % kSB;
+                mbar_wait(s_full + b, (j / kSB) & 1);
                 tc_fence_after();
                 const uint32_t ts = t_row + 128 + b * 128 + ch * 32;  // this warp's 32 key columns
                 const bool vis = (list[idx] >> (24 + half)) & 1;
