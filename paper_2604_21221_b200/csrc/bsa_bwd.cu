@@ -32,7 +32,11 @@ namespace {
 // completes -- two blocks of work later -- so two stages left the MMA warp waiting on TMA latency
 // every block; four keep the loads a full block ahead.
 constexpr int kNS = 4;
-constexpr int kSB = 3;  // dQ kernel: S/dP TMEM buffers (dQ 128 + 3 x 128 columns)
+// dQ kernel TMEM: dQ [0, 128), Q [128, 192) and dO [192, 256) as bf16 pairs (the A operands of
+// S = Q K^T and dP = dO V^T are TMEM-resident: TS MMAs run at the N = 64 floor, SS ones do not),
+// then kSB buffers of S (64 columns) + dP (64 columns)
+constexpr int kSB = 2;
+constexpr uint32_t kQCol = 128, kDOCol = 192, kBufCol = 256;
 constexpr int kBwdThreads = 320;  // warp 0 producer, warp 1 MMA, warps 2-9 elementwise
 constexpr int kEw = 8;             // elementwise warps: warp w reads TMEM lane quarter w % 4 and
                                    // column half (w - 2) / 4 -- every element is independent (lse is
@@ -52,6 +56,8 @@ struct BwdParams {
     const float* drow;   // [units * nqb][64] rowsum(dO o O); rows >= b zero (64-row staging copies)
     const uint32_t* inv;  // [units][n_local][inv_words] query blocks selecting each local block
     int inv_words;
+    const bf16* q;       // [units][n_q][d] (dQ kernel: rows go straight to TMEM)
+    const bf16* d_o;
     float* dq;           // [units][n_q][d] f32
     float* dk;           // [units][n_slots][64][d] f32
     float* dv;
@@ -156,6 +162,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < 2 + 4 * kNS + 2 * kSB + 6; ++i) mbar_init(bars + i, 1);
         for (int s = 0; s < kSB; ++s) mbar_init(p_full + s, kEw);
+        mbar_init(q_full, kEw);  // Q / dO rows in TMEM, stored by the elementwise warps
         for (int s = 0; s < 2; ++s) mbar_init(list_empty + s, kEw + 1);
         mbar_init(dq_free, kEw);
         fence_barrier_init();
@@ -165,16 +172,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tma_prefetch(&tm_v);
     }
     if (warp == 1) tmem_alloc<kBwdTmemCols>(misc);
-    if (warp >= 2) {  // Q / dO padding rows (>= b of each half) stay zero: TMA writes rows < b only
-        const int t = threadIdx.x - 64;
-        for (int e = t; e < 2 * 128 * L::kHalves * 8; e += kEw * 32) {
-            const int chunk = e & 7, rh = (e >> 3) % (128 * L::kHalves), which = (e >> 3) / (128 * L::kHalves);
-            const int h = rh % L::kHalves, row = rh / L::kHalves;
-            if ((row & 63) >= p.b)
-                *reinterpret_cast<uint4*>((which ? do_s : q_s) + h * 16384 + row * 128 + chunk * 16) = make_uint4(0, 0, 0, 0);
-        }
-        fence_proxy_async_smem();
-    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -233,17 +230,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(list_full + lb);
             const int nf = run;
-            if (f > 0) mbar_wait(q_empty, (f - 1) & 1);
-            const uint32_t qbytes = (has2 ? 2u : 1u) * L::kHalves * static_cast<uint32_t>(p.b) * 128u;
-            if (elect_one()) {
-                mbar_arrive_expect_tx(q_full, 2 * qbytes);
-                for (int r = 0; r < (has2 ? 2 : 1); ++r)
-                    for (int h = 0; h < L::kHalves; ++h) {
-                        tma_load_3d(q_s + h * 16384 + r * 8192, &tm_q, q_full, h * 64, 0, u * p.nqb + qb0 + r);
-                        tma_load_3d(do_s + h * 16384 + r * 8192, &tm_do, q_full, h * 64, 0, u * p.nqb + qb0 + r);
-                    }
-            }
-            __syncwarp();
             for (int idx = 0; idx < nf; ++idx) {
                 const int j = jg + idx, s = j % kNS, ph = (j / kNS) & 1;
                 const int row0 = (u * p.n_slots + (list[idx] & 0xFFFFFF)) * 64;
@@ -266,8 +252,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         // ================================================= tcgen05 issuer
         constexpr uint32_t idesc_s = idesc_bf16_f32(128, 64, 0, 0);
         constexpr uint32_t idesc_o = idesc_bf16_f32(128, D, 0, 1);
-        const uint64_t qdesc = smem_desc_sw128(smem_u32(q_s), 16, 1024);
-        const uint64_t dodesc = smem_desc_sw128(smem_u32(do_s), 16, 1024);
         const uint64_t kdesc = smem_desc_sw128(smem_u32(k_s), 16, 1024);
         const uint64_t vdesc = smem_desc_sw128(smem_u32(v_s), 16, 1024);
         const uint64_t kmn = smem_desc_sw128(smem_u32(k_s), 8192, 1024);  // K as an MN-major B operand
@@ -285,7 +269,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 const int b = x % kSB;
                 mbar_wait(p_full + b, (x / kSB) & 1);
                 tc_fence_after();
-                const uint32_t a_tmem = tmem + 128 + b * 128;  // dS_x (bf16 pairs) over S_x
+                const uint32_t a_tmem = tmem + kBufCol + b * 128;  // dS_x (bf16 pairs) over S_x
                 const uint64_t kd = kmn + (((x % kNS) * L::kBlk) >> 4);
                 if (elect_one()) {
 #pragma unroll
@@ -300,15 +284,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 mbar_wait(k_full + s, (j / kNS) & 1);
                 mbar_wait(v_full + s, (j / kNS) & 1);
                 tc_fence_after();
-                const uint32_t st = tmem + 128 + b * 128, dpt = st + 64;
+                const uint32_t st = tmem + kBufCol + b * 128, dpt = st + 64;
                 const uint64_t kd = kdesc + ((s * L::kBlk) >> 4), vd = vdesc + ((s * L::kBlk) >> 4);
                 if (elect_one()) {
 #pragma unroll
                     for (int kk = 0; kk < D / 16; ++kk) {
                         const uint32_t oa = ((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
                         const uint32_t ob = ((kk >> 2) * 8192 + (kk & 3) * 32) >> 4;
-                        mma_ss(st, qdesc + oa, kd + ob, idesc_s, kk > 0 ? 1u : 0u);
-                        mma_ss(dpt, dodesc + oa, vd + ob, idesc_s, kk > 0 ? 1u : 0u);
+                        (void)oa;
+                        mma_ts(st, tmem + kQCol + kk * 8, kd + ob, idesc_s, kk > 0 ? 1u : 0u);
+                        mma_ts(dpt, tmem + kDOCol + kk * 8, vd + ob, idesc_s, kk > 0 ? 1u : 0u);
                     }
                     mma_commit(v_empty + s);
                     mma_commit(s_full + b);
@@ -317,10 +302,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 if (idx >= kSB - 1) issue_dq(j - (kSB - 1), idx == kSB - 1);  // kSB - 1 blocks of lookahead
             }
             for (int x = (nf > kSB - 1 ? nf - (kSB - 1) : 0); x < nf; ++x) issue_dq(jg + x, x == 0);
-            if (elect_one()) {
-                mma_commit(q_empty);
-                mma_commit(dq_done);
-            }
+            if (elect_one()) mma_commit(dq_done);
             __syncwarp();
             jg += nf;
         }
@@ -343,11 +325,35 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             const float lse2 = valid ? __ldg(p.lse2 + prow) : INFINITY;
             const float dd = valid ? __ldg(p.drow + prow) : 0.0f;
             const float2 nl2 = make_float2(-lse2, -lse2);
+            {   // this row's Q and dO (d columns [ch * D/2, +D/2)) into TMEM as bf16 pairs: the A
+                // operands of the tile's S and dP MMAs (the previous tile's MMAs are complete:
+                // its epilogue waited dq_done); padding rows are zero
+                constexpr int W = D / 4;  // u32 per half row
+                uint32_t qv[W], gv[W];
+#pragma unroll
+                for (int c = 0; c < W / 4; ++c) {
+                    const uint4 a = valid ? __ldg(reinterpret_cast<const uint4*>(p.q + row * D + ch * (D / 2)) + c) : make_uint4(0, 0, 0, 0);
+                    const uint4 g = valid ? __ldg(reinterpret_cast<const uint4*>(p.d_o + row * D + ch * (D / 2)) + c) : make_uint4(0, 0, 0, 0);
+                    qv[4 * c] = a.x; qv[4 * c + 1] = a.y; qv[4 * c + 2] = a.z; qv[4 * c + 3] = a.w;
+                    gv[4 * c] = g.x; gv[4 * c + 1] = g.y; gv[4 * c + 2] = g.z; gv[4 * c + 3] = g.w;
+                }
+                if constexpr (W == 32) {
+                    tmem_st32(t_row + kQCol + ch * W, qv);
+                    tmem_st32(t_row + kDOCol + ch * W, gv);
+                } else {
+                    tmem_st16(t_row + kQCol + ch * W, *reinterpret_cast<uint32_t(*)[16]>(qv));
+                    tmem_st16(t_row + kDOCol + ch * W, *reinterpret_cast<uint32_t(*)[16]>(gv));
+                }
+                tmem_wait_st();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(q_full);
+            }
             for (int idx = 0; idx < nf; ++idx) {
                 const int j = jg + idx, b = j % kSB;
                 mbar_wait(s_full + b, (j / kSB) & 1);
                 tc_fence_after();
-                const uint32_t ts = t_row + 128 + b * 128 + ch * 32;  // this warp's 32 key columns
+                const uint32_t ts = t_row + kBufCol + b * 128 + ch * 32;  // this warp's 32 key columns
                 const bool vis = (list[idx] >> (24 + half)) & 1;
                 uint32_t pk[16];
                 if (vis) {
@@ -791,6 +797,8 @@ int launch_bsa_bwd(const bf16* q, const bf16* k_pool, const bf16* v_pool, int n_
     p.drow = drow;
     p.inv = inv;
     p.inv_words = (nqb + 31) / 32;
+    p.q = q;
+    p.d_o = d_o;
     p.dq = dq;
     p.dk = dk;
     p.dv = dv;
