@@ -83,6 +83,8 @@ def load(path: str = LIB_PATH) -> C.CDLL:
             f"`python -c 'import __graft_entry__ as g; g.build()'`). There is no CPU fallback.")
     lib = C.CDLL(path)
     for name, (res, args) in _SIGS.items():
+        if path != os.path.join(HERE, "_lib", "libpbsa_b200.so") and not hasattr(lib, name):
+            continue  # an older experiment build (PBSA_LIB_PATH) may predate some entry points
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

@@ -49,7 +49,6 @@ constexpr uint32_t kTmemCols = 256;
 constexpr float kOverflowSum = 65536.0f;
 // column pairs whose exp2 runs as a polynomial on the FMA pipe instead of MUFU (bit c2 = pair c2)
 constexpr uint32_t kPolyMask = 0u;  // MUFU-only: the softmax is issue/latency-bound, not MUFU-bound
-constexpr int kPolyDefault = 0;
 
 struct BsaParams {
     int units, nqb, b, n_slots;
@@ -63,7 +62,6 @@ struct BsaParams {
     float* lse;
     float scale_log2;
     int max_list, bm_words;
-    int list16;     // visible-list entries are 16-bit (n_slots < 16384)
     int lat;        // q / o are chunk latents (LatentGeom lg), not block-major [units][n_q][d]
     LatentGeom lg;
     long long* trace;  // perf experiments only: per-event clock64 stamps of CTA 0 (null = off)
@@ -132,7 +130,7 @@ __device__ __forceinline__ int num_fragments(const BsaParams& p, int c) {
     return p.whole_waves + static_cast<int>((b - 1) / p.vlen - a / p.vlen) + 1;
 }
 
-template <int D, int NSK, int NSV, int B, uint32_t POLY>
+template <int D, int NSK, int NSV, int B, uint32_t POLY, bool L16>
 __global__ void __launch_bounds__(kThreads, 2)
     bsa_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                    const __grid_constant__ CUtensorMap tm_v, const BsaParams p) {
@@ -161,15 +159,15 @@ __global__ void __launch_bounds__(kThreads, 2)
     // the pool has < 16384 slots, 2 bytes (slot | mask << 14) -- halves the footprint of long lists
     // (config 5: 3238 entries) so two CTAs still fit an SM
     uint8_t* lists = smem + L::kOffList;
-    const int esz = p.list16 ? 2 : 4;
-    const int mshift = p.list16 ? 14 : 24;
+    constexpr int esz = L16 ? 2 : 4;
+    constexpr int mshift = L16 ? 14 : 24;
     uint32_t* bm = reinterpret_cast<uint32_t*>(lists + ((2 * static_cast<size_t>(p.max_list) * esz + 15) & ~size_t(15)));
     auto list_put = [&](uint8_t* base, int i, int slot, int mask) {
-        if (p.list16) reinterpret_cast<uint16_t*>(base)[i] = static_cast<uint16_t>(slot | (mask << 14));
+        if (L16) reinterpret_cast<uint16_t*>(base)[i] = static_cast<uint16_t>(slot | (mask << 14));
         else reinterpret_cast<int32_t*>(base)[i] = slot | (mask << 24);
     };
     auto list_slot = [&](const uint8_t* base, int i) {
-        return p.list16 ? static_cast<int>(reinterpret_cast<const uint16_t*>(base)[i] & 0x3FFF)
+        return L16 ? static_cast<int>(reinterpret_cast<const uint16_t*>(base)[i] & 0x3FFF)
                         : (reinterpret_cast<const int32_t*>(base)[i] & 0xFFFFFF);
     };
 
@@ -486,7 +484,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 tc_fence_after();
                 const uint32_t t_s = t_o + L::kSColBase + buf * 64;
                 // rows of one warp all lie in one half -> visibility is warp-uniform
-                const uint32_t ent = p.list16 ? ld_shared_u16(list_s + idx * 2) : ld_shared_u32(list_s + idx * 4);
+                const uint32_t ent = L16 ? ld_shared_u16(list_s + idx * 2) : ld_shared_u32(list_s + idx * 4);
                 const bool vis = ((ent >> (mshift + half)) & 1) && p.ablate != 1;
                 if (vis) {
                     uint32_t pk[32];
@@ -738,7 +736,7 @@ int num_sms() {
     return n;
 }
 
-template <int D, int NSK, int NSV, int B, uint32_t POLY>
+template <int D, int NSK, int NSV, int B, uint32_t POLY, bool L16>
 int launch_impl(const bf16* q, const bf16* kp, const bf16* vp, BsaParams p, cudaStream_t s) {
     using L = Layout<D, NSK, NSV>;
     alignas(64) CUtensorMap tq, tk, tv;
@@ -763,10 +761,10 @@ int launch_impl(const bf16* q, const bf16* kp, const bf16* vp, BsaParams p, cuda
         if (!encode_tmap_bf16(&tv, vp, 2, dims, strides, box, &err))
             return set_error(PBSA_ECUDA, "tensor map V: " + err);
     }
-    const size_t smem = L::bytes(p.max_list, p.bm_words, p.list16 ? 2 : 4);
+    const size_t smem = L::bytes(p.max_list, p.bm_words, L16 ? 2 : 4);
     if (smem > 227 * 1024)
         return set_error(PBSA_EUNSUPPORTED, "bsa_fwd: visible list too long for shared memory");
-    if (int rc = ensure_smem(reinterpret_cast<const void*>(bsa_fwd_kernel<D, NSK, NSV, B, POLY>), smem, "bsa_fwd"))
+    if (int rc = ensure_smem(reinterpret_cast<const void*>(bsa_fwd_kernel<D, NSK, NSV, B, POLY, L16>), smem, "bsa_fwd"))
         return rc;
     // persistent grid = the CTAs that are actually co-resident: __launch_bounds__(kThreads, 2) keeps
     // registers at two CTAs per SM, so shared memory decides
@@ -798,7 +796,7 @@ int launch_impl(const bf16* q, const bf16* kp, const bf16* vp, BsaParams p, cuda
         if (p.whole_waves == 0) p.grid = p.tail_grid;
     }
     if (p.grid <= 0) return 0;
-    if (launch_pdl(bsa_fwd_kernel<D, NSK, NSV, B, POLY>, dim3(p.grid), dim3(kThreads), smem, s, tq, tk, tv, p) !=
+    if (launch_pdl(bsa_fwd_kernel<D, NSK, NSV, B, POLY, L16>, dim3(p.grid), dim3(kThreads), smem, s, tq, tk, tv, p) !=
         cudaSuccess)
         return check_launch("bsa_fwd_kernel");
     return check_launch("bsa_fwd_kernel");
@@ -849,7 +847,6 @@ int launch_bsa_fwd(const bf16* q, const bf16* k_pool, const bf16* v_pool, int n_
         p.trace = g_trace;
     }
     p.bm_words = (n_local + 31) / 32 + 1;
-    p.list16 = n_slots < 16384;
     p.max_list = n_dense + (p.k > 0 ? (2 * p.k < n_local ? 2 * p.k : n_local) : 0);
     p.tiles_per_unit = (nqb + 1) / 2;
     p.n_tiles = units * p.tiles_per_unit;
@@ -863,24 +860,22 @@ int launch_bsa_fwd(const bf16* q, const bf16* k_pool, const bf16* v_pool, int n_
         p.part_ml = p.part_o + slots * 128 * d;
         p.counters = reinterpret_cast<int*>(p.part_ml + slots * 256);
     }
+    // 16-bit visible-list entries only where 32-bit lists would cost the second CTA per SM (long
+    // lists, e.g. config 5) and the pool is small enough to index with 14 bits
+    const size_t smem32 = Layout<128, 2, 2>::bytes(p.max_list, p.bm_words, 4);
+    const bool l16 = n_slots < 16384 && 2 * (smem32 + 1024) > 228 * 1024;
+#define PBSA_K3(DD, NS, BB)                                                                       \
+    return l16 ? launch_impl<DD, NS, NS, BB, kPolyMask, true>(q, k_pool, v_pool, p, s)            \
+               : launch_impl<DD, NS, NS, BB, kPolyMask, false>(q, k_pool, v_pool, p, s)
     if (d == 128) {
-        if (b == 60) {
-            // perf experiments only: PBSA_POLY selects the share of exp2 pairs on the FMA pipe
-            static const int poly = getenv("PBSA_POLY") ? atoi(getenv("PBSA_POLY")) : kPolyDefault;
-            switch (poly) {
-                case 0: return launch_impl<128, 2, 2, 60, 0u>(q, k_pool, v_pool, p, s);
-                case 1: return launch_impl<128, 2, 2, 60, 0x24924924u>(q, k_pool, v_pool, p, s);  // 1/3
-                case 2: return launch_impl<128, 2, 2, 60, 0x55555555u>(q, k_pool, v_pool, p, s);  // 1/2
-                case 4: return launch_impl<128, 2, 2, 60, 0x4A4A4A4Au>(q, k_pool, v_pool, p, s);  // 3/8
-                default: return launch_impl<128, 2, 2, 60, 0x11111111u>(q, k_pool, v_pool, p, s);  // 1/4
-            }
-        }
-        if (b == 64) return launch_impl<128, 2, 2, 64, kPolyMask>(q, k_pool, v_pool, p, s);
-        return launch_impl<128, 2, 2, 0, kPolyMask>(q, k_pool, v_pool, p, s);
+        if (b == 60) PBSA_K3(128, 2, 60);
+        if (b == 64) PBSA_K3(128, 2, 64);
+        PBSA_K3(128, 2, 0);
     }
-    if (b == 60) return launch_impl<64, 3, 3, 60, 0u>(q, k_pool, v_pool, p, s);
-    if (b == 64) return launch_impl<64, 3, 3, 64, 0u>(q, k_pool, v_pool, p, s);
-    return launch_impl<64, 3, 3, 0, 0u>(q, k_pool, v_pool, p, s);
+    if (b == 60) PBSA_K3(64, 3, 60);
+    if (b == 64) PBSA_K3(64, 3, 64);
+    PBSA_K3(64, 3, 0);
+#undef PBSA_K3
 }
 
 }  // namespace pbsa
