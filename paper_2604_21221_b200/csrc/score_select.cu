@@ -18,6 +18,7 @@
 //   aggregate_kernel     thread per key block, ascending-row fp64 column sums (k=0 pass only)
 // and a key-major variant for long windows (config 5) below.
 #include <cfloat>
+#include <cstdlib>
 
 #include "internal.h"
 #include "ptx.cuh"
@@ -71,11 +72,10 @@ __device__ void warp_softmax(const float* z, int n, double* e, uint32_t* out_bit
     __syncwarp();
 }
 
-// k largest of pb[0..n) (non-negative float bits => unsigned order), ties -> lower index.
-// Writes the winners' indices ascending to out[0..k).
-__device__ void warp_topk(const uint32_t* pb, int n, int k, uint32_t* hist, int32_t* out) {
+// 4-pass 8-bit radix select: the value of the k-th largest of pb[0..n) (unsigned order), and in
+// *kk_out how many elements equal to it belong to the k largest.
+__device__ uint32_t warp_kth(const uint32_t* pb, int n, int k, uint32_t* hist, int* kk_out) {
     const int lane = threadIdx.x & 31;
-    const uint32_t lt = (1u << lane) - 1u;
     uint32_t prefix = 0, pmask = 0;
     int kk = k;  // still to pick at/below the current prefix
 #pragma unroll 1
@@ -126,6 +126,17 @@ __device__ void warp_topk(const uint32_t* pb, int n, int k, uint32_t* hist, int3
         pmask |= 255u << shift;
         __syncwarp();
     }
+    *kk_out = kk;
+    return prefix;
+}
+
+// k largest of pb[0..n) (non-negative float bits => unsigned order), ties -> lower index.
+// Writes the winners' indices ascending to out[0..k).
+__device__ void warp_topk(const uint32_t* pb, int n, int k, uint32_t* hist, int32_t* out) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t lt = (1u << lane) - 1u;
+    int kk;
+    const uint32_t prefix = warp_kth(pb, n, k, hist, &kk);
     // prefix = value of the k-th largest element; take every element above it and the first kk
     // (lowest indices) equal to it.
     int run = 0, tie_run = 0;
@@ -292,6 +303,487 @@ __global__ void __launch_bounds__(256) row_select_kernel(const ScoreParams p, co
         warp_topk(pb, p.n_local, p.k, hist, p.sel + row * p.k);
     }
     if (p.arows != nullptr && (SPLIT == 1 || role == 1)) warp_softmax(zr, n, e, nullptr, p.arows + row * n);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Denoise passes (selection only, no A_t): certified fp32 ranking.
+// Only the INDICES of the k largest local-window probabilities are needed, and p_j =
+// float(e_j / denom) is non-decreasing in the exact logit z_j, so the selection is the top-k by z
+// except where keys at the k-th boundary round to the same fp32 probability (then the lower index
+// wins).  logits32_kernel computes fp32 logits z~ with the rigorous bound
+//   |z~_j - z_j| <= eps_j = scale * gamma_D * |q| * |k_j| + 2^-21 |z~_j|,  gamma_D = D * 2^-24 * 1.01
+// (fp32 FMA dot-product error, Cauchy-Schwarz, and the two fp32 roundings of the oracle's
+// float(dot64) * scale); cert_select_kernel radix-selects the k-th largest z~ (T), takes every key
+// above T + 2 eps_max + tau, drops every key below T - 2 eps_max - tau, recomputes the oracle's exact
+// logit (ascending-c fp64 dot, same roundings) for the few keys in between and ranks those exactly.
+// tau = 2^-20: two logits further apart than tau give probabilities more than 7 fp32 ulps apart
+// (exp(tau) - 1 > 2^-20.01 vs ulp <= 2^-23 for normal fp32), so no probability tie can cross the
+// boundary.  A row reruns the oracle's exact softmax + Top-K (warp_softmax / warp_topk, fp64
+// scratch in global memory) when (a) the exact gap at the boundary is <= tau, (b) boundary
+// probabilities could be subnormal (T - max z < -60), (c) more than kCertAmb keys are ambiguous,
+// (d) a logit is NaN, or (e) an exact logit falls outside its certified interval (status bit 2 --
+// never expected; a canary for the bound).
+constexpr int kCertAmb = 256;  // = kCertThreads: one ambiguous key per thread
+constexpr float kTau = 2.384185791015625e-07f;  // 2^-22
+
+// CTA = 128 keys x up to 80 query rows; warp = 8 rows, lane = 4 keys (32 fp32 accumulators): per
+// 16-byte chunk a warp issues 4 key LDS.128 + 8 broadcast query LDS.128 for 128 FFMAs, so the FMA
+// pipe, not shared memory, is the limit.  Key chunk c4 of key j is stored at c4 ^ ((j >> 2) & 7):
+// the lanes of a quarter-warp (keys 4l + t) hit 8 distinct 16-byte bank groups.  The key tile is
+// staged once for all of a unit's rows (80 >= nqb for the configs), so krep is read from L2 once.
+constexpr int kL32Warps = 10;  // 80 rows
+
+template <int D>
+__global__ void __launch_bounds__(kL32Warps * 32) logits32_kernel(const ScoreParams p, float* __restrict__ z,
+                                                                  float* __restrict__ knorm) {
+    pdl_wait();  // programmatic dependent launch: upstream outputs are visible from here on
+    extern __shared__ __align__(16) uint8_t smem[];
+    constexpr int C4 = D / 4;
+    float4* ks = reinterpret_cast<float4*>(smem);                               // [128][C4] swizzled
+    float4* qs = reinterpret_cast<float4*>(smem + kLogitKeys * D * 4);          // [80][C4]
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int u = blockIdx.z, i0 = blockIdx.y * kL32Warps * 8, j0 = blockIdx.x * kLogitKeys;
+    const int n = p.n_local;
+    const int nr = min(kL32Warps * 8, p.nqb - i0);
+    const int nk = min(kLogitKeys, n - j0);
+    __shared__ int slots[kLogitKeys];
+    if (tid < kLogitKeys)
+        slots[tid] = tid < nk ? __ldg(p.keys + static_cast<int64_t>(u) * p.key_stride + p.local_off + j0 + tid) : 0;
+    __syncthreads();
+    for (int kk = warp; kk < nk; kk += kL32Warps) {
+        const float4* kr = reinterpret_cast<const float4*>(p.krep + u * p.kru + static_cast<int64_t>(slots[kk]) * D);
+        for (int c4 = lane; c4 < C4; c4 += 32) cp_async16(ks + kk * C4 + (c4 ^ ((kk >> 2) & 7)), kr + c4);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    const float4* qg = reinterpret_cast<const float4*>(p.qc + (static_cast<int64_t>(u) * p.nqb + i0) * D);
+    for (int e4 = tid; e4 < nr * C4; e4 += kL32Warps * 32) qs[e4] = __ldg(qg + e4);
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    const int r0 = warp * 8;
+    if (r0 >= nr) return;
+    float acc[8][4], ss[4];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) acc[r][t] = 0.f;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) ss[t] = 0.f;
+    const bool norms = blockIdx.y == 0 && warp == 0;
+    const int kb = 4 * lane;  // this lane's first key; all four share (key >> 2) & 7 = lane & 7
+    const int sw = lane & 7;
+#pragma unroll 2
+    for (int c4 = 0; c4 < C4; ++c4) {
+        float4 kv[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) kv[t] = ks[(kb + t) * C4 + (c4 ^ sw)];
+        if (norms) {
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                ss[t] = fmaf(kv[t].w, kv[t].w, fmaf(kv[t].z, kv[t].z, fmaf(kv[t].y, kv[t].y, fmaf(kv[t].x, kv[t].x, ss[t]))));
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const float4 qv = qs[min(r0 + r, nr - 1) * C4 + c4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                acc[r][t] = fmaf(qv.w, kv[t].w, fmaf(qv.z, kv[t].z, fmaf(qv.y, kv[t].y, fmaf(qv.x, kv[t].x, acc[r][t]))));
+        }
+    }
+    if (norms) {  // per-CTA max key norm: cert_select bounds every key of the unit by the unit max
+        float m = 0.f;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) m = kb + t < nk ? fmaxf(m, ss[t]) : m;
+        m = warp_max(m);
+        if (lane == 0) knorm[static_cast<int64_t>(u) * gridDim.x + blockIdx.x] = sqrtf(m);
+    }
+    if (kb >= nk) return;
+    const int n4 = (n + 3) & ~3;  // row stride: 16-byte rows (the tail pads are never read as keys)
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+        if (r0 + r >= nr) break;
+        float4 o;
+        o.x = __fmul_rn(acc[r][0], p.scale);
+        o.y = __fmul_rn(acc[r][1], p.scale);
+        o.z = __fmul_rn(acc[r][2], p.scale);
+        o.w = __fmul_rn(acc[r][3], p.scale);
+        *reinterpret_cast<float4*>(z + (static_cast<int64_t>(u) * p.nqb + i0 + r0 + r) * n4 + j0 + kb) = o;
+    }
+}
+
+__device__ __forceinline__ uint32_t f2key(float v) {  // float -> unsigned, order preserving
+    const uint32_t b = __float_as_uint(v);
+    return b ^ ((b >> 31) ? 0xffffffffu : 0x80000000u);
+}
+__device__ __forceinline__ float key2f(uint32_t k) { return __uint_as_float((k >> 31) ? k ^ 0x80000000u : ~k); }
+
+// The oracle's logit for query row q and key slot `slot`: float(ascending-c fp64 dot) * scale.
+template <int D>
+__device__ __forceinline__ float exact_logit(const float* q, const float* krep, int64_t slot, float scale) {
+    const float4* q4 = reinterpret_cast<const float4*>(q);
+    const float4* k4 = reinterpret_cast<const float4*>(krep + slot * D);
+    double acc = 0.0;
+#pragma unroll 8
+    for (int c4 = 0; c4 < D / 4; ++c4) {
+        const float4 a = __ldg(q4 + c4), b = __ldg(k4 + c4);
+        acc = __fma_rn(static_cast<double>(a.x), static_cast<double>(b.x), acc);
+        acc = __fma_rn(static_cast<double>(a.y), static_cast<double>(b.y), acc);
+        acc = __fma_rn(static_cast<double>(a.z), static_cast<double>(b.z), acc);
+        acc = __fma_rn(static_cast<double>(a.w), static_cast<double>(b.w), acc);
+    }
+    return __fmul_rn(__double2float_rn(acc), scale);
+}
+
+// CTA (256 threads) per row, the row's z~ held in registers: warp w, lane l, vector i holds keys
+// (w*V4 + i)*128 + 4l .. +3 (one 16-byte load each; row stride n4 = n rounded up to 4), so every pass
+// below is register work and a warp owns a contiguous key range (ascending emission by warp scans).
+// One 1024-bin histogram over [min z~, max z~] (a monotone map, so whole bins are ordered) finds the
+// bin b* holding the k-th largest z~; at config 5 (6006 keys, N(0,1)-like logits) b* holds ~15 keys.
+// mode 2 forces the exact fallback (tests).
+constexpr int kCertThreads = 256;
+constexpr int kCertBins = 1024;
+constexpr int kCertWarps = kCertThreads / 32;
+constexpr int kCertMaxKeys = 8 * 4 * kCertThreads;  // V4 <= 8
+
+// exclusive prefix over the block of v (returns it; *total = block sum); red[kCertWarps] scratch
+__device__ __forceinline__ int block_scan(int v, int* red, int* total) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    __syncthreads();
+    if (lane == 31) red[warp] = incl;
+    __syncthreads();
+    int base = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < kCertWarps; ++w) {
+        base += w < warp ? red[w] : 0;
+        tot += red[w];
+    }
+    *total = tot;
+    return base + incl - v;
+}
+
+__device__ __forceinline__ int block_sum(int v, int* red) {
+    int tot;
+    block_scan(v, red, &tot);
+    return tot;
+}
+
+template <int D, int V4>
+__global__ void __launch_bounds__(kCertThreads, 3) cert_select_kernel(const ScoreParams p, float* __restrict__ z,
+                                                                   const float* __restrict__ kpart, int nparts,
+                                                                   int n4, double* __restrict__ escr,
+                                                                   int64_t escr_stride, int mode) {
+    pdl_wait();  // programmatic dependent launch: upstream outputs are visible from here on
+    __shared__ uint32_t hist[kCertBins];
+    __shared__ uint32_t chosen[kCertMaxKeys / 32];
+    __shared__ int red[kCertWarps];
+    __shared__ float redf[2][kCertWarps];
+    __shared__ int pick[4];
+    __shared__ int cnt;
+    __shared__ int wcnt[kCertWarps];
+    __shared__ float bound[2];
+    __shared__ double denom_s;
+    __shared__ int32_t amb[kCertAmb];
+    __shared__ float zamb[kCertAmb];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t row = blockIdx.x;
+    const int n = p.n_local, k = p.k;
+    const int u = static_cast<int>(row / p.nqb);
+    float* zg = z + row * n4;
+    const float* q = p.qc + row * D;
+    const int32_t* slots = p.keys + static_cast<int64_t>(u) * p.key_stride + p.local_off;
+    const float* kr = p.krep + u * p.kru;
+    int32_t* out = p.sel + row * k;
+    const int jw = warp * V4 * 128 + 4 * lane;  // key of (vector 0, component 0); vector i adds 128 i
+
+    float v[V4][4];
+#pragma unroll
+    for (int i = 0; i < V4; ++i) {
+        const int j = jw + 128 * i;
+        const float4 x = j < n ? *reinterpret_cast<const float4*>(zg + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+        v[i][0] = x.x;
+        v[i][1] = x.y;
+        v[i][2] = x.z;
+        v[i][3] = x.w;
+    }
+    for (int b = tid; b < kCertBins; b += kCertThreads) hist[b] = 0;
+    for (int b = tid; b < kCertMaxKeys / 32; b += kCertThreads) chosen[b] = 0;
+    if (tid < kCertWarps) wcnt[tid] = 0;
+    if (tid == 0) cnt = 0;
+    // every warp: |q|^2 (D/32 values per lane) and the unit's largest key norm (nparts CTA maxima)
+    float qq = 0.f, kmax = 0.f;
+    for (int c = lane; c < D; c += 32) qq = fmaf(q[c], q[c], qq);
+    for (int i = lane; i < nparts; i += 32) kmax = fmaxf(kmax, __ldg(kpart + static_cast<int64_t>(u) * nparts + i));
+    float zmax = -FLT_MAX, zmin = FLT_MAX;
+    int bad = 0;
+    // warp-uniform: every key this warp holds is < n (all warps but the row's last partial one)
+    const bool full = (warp + 1) * V4 * 128 <= n;
+    if (!full) {  // pad the missing keys with copies of key 0 (present in every row): they change
+                  // neither the maximum nor the minimum, and are skipped by index below
+        const float v0 = zg[0];
+#pragma unroll
+        for (int i = 0; i < V4; ++i)
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+                if (jw + 128 * i + t >= n) v[i][t] = v0;
+    }
+#pragma unroll
+    for (int i = 0; i < V4; ++i)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            bad |= v[i][t] != v[i][t];
+            zmax = fmaxf(zmax, v[i][t]);
+            zmin = fminf(zmin, v[i][t]);
+        }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) qq += __shfl_xor_sync(0xffffffffu, qq, o);
+    kmax = warp_max(kmax);
+    zmax = warp_max(zmax);
+    zmin = -warp_max(-zmin);
+    if (lane == 0) {
+        redf[0][warp] = zmax;
+        redf[1][warp] = zmin;
+    }
+    bad = block_sum(bad, red);  // (its barriers also publish the zeroed counters and redf)
+    zmax = -FLT_MAX;
+    zmin = FLT_MAX;
+#pragma unroll
+    for (int w = 0; w < kCertWarps; ++w) {
+        zmax = fmaxf(zmax, redf[0][w]);
+        zmin = fminf(zmin, redf[1][w]);
+    }
+    // eps for every key: scale * gamma_D * |q| * max|k| + 2^-21 max|z~| (norms rounded up by 2^-12,
+    // far above their fp32 error; the whole bound by 1 %)
+    const float emax = fmaf(p.scale * (static_cast<float>(D) * 5.9604645e-8f * 1.01f) * (sqrtf(qq) * 1.000244140625f),
+                            kmax * 1.000244140625f, fmaxf(fabsf(zmax), fabsf(zmin)) * 4.76837158203125e-07f) *
+                           1.01f + 1e-30f;
+    bool fallback = mode == 2 || bad != 0;
+    if (!fallback) {
+        // bin(x) is non-decreasing in x (fsub, fmul, truncation and min are monotone)
+        const float inv = static_cast<float>(kCertBins) / (zmax - zmin);
+        auto bin = [&](float x) { return min(kCertBins - 1, static_cast<int>((x - zmin) * inv)); };
+        if (full) {
+#pragma unroll
+            for (int i = 0; i < V4; ++i)
+#pragma unroll
+                for (int t = 0; t < 4; ++t) atomicAdd(&hist[bin(v[i][t])], 1u);
+        } else {
+#pragma unroll
+            for (int i = 0; i < V4; ++i)
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                    if (jw + 128 * i + t < n) atomicAdd(&hist[bin(v[i][t])], 1u);
+        }
+        __syncthreads();
+        // thread t owns bins 1023-4t .. 1020-4t (descending)
+        int c4[4], sum4 = 0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            c4[t] = static_cast<int>(hist[kCertBins - 1 - 4 * tid - t]);
+            sum4 += c4[t];
+        }
+        int tot;
+        int above = block_scan(sum4, red, &tot);
+        if (above < k && k <= above + sum4) {
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                if (above < k && k <= above + c4[t]) {
+                    pick[0] = kCertBins - 1 - 4 * tid - t;  // b*: the bin of the k-th largest z~
+                    pick[1] = above;                        // keys in bins above b*
+                }
+                above += c4[t];
+            }
+        }
+        // Two z~ at most `band` apart are at most m bins apart (the bin map's rounding moves a value
+        // by < 1e-3 bins), so keys more than m bins above b* exceed every key of b* (the k-th largest
+        // included) by more than band, and keys more than m bins below fall short by more.
+        const float band = 2.f * emax + kTau;
+        const int m = static_cast<int>(fminf(band * inv + 0.001f, 1.0e6f)) + 1;
+        __syncthreads();
+        const int bstar = pick[0];
+        if (tid == 0) {
+            int na = 0, mid_above = 0;
+            if (m <= 32) {
+                for (int b = max(0, bstar - m); b <= min(kCertBins - 1, bstar + m); ++b) {
+                    na += static_cast<int>(hist[b]);
+                    mid_above += b > bstar ? static_cast<int>(hist[b]) : 0;
+                }
+            } else {
+                na = kCertAmb + 1;
+            }
+            pick[2] = na;
+            pick[3] = pick[1] - mid_above;  // certainly in: keys more than m bins above b*
+        }
+        __syncthreads();
+        const int na = pick[2], nin = pick[3];
+        const int r = k - nin;  // slots left for the ambiguous keys (1 <= r <= na by construction)
+        const int blo = bstar - m, bhi = bstar + m;
+        fallback = na > kCertAmb || r < 1 || r > na;
+        if (!fallback) {
+            // classification: per-warp count of the certain keys, list of the ambiguous ones
+            int nt = 0;
+#pragma unroll
+            for (int i = 0; i < V4; ++i)
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    const int j = jw + 128 * i + t;
+                    const int bj = bin(v[i][t]);
+                    if (full || j < n) {
+                        nt += bj > bhi;
+                        if (bj >= blo && bj <= bhi) amb[atomicAdd(&cnt, 1)] = j;
+                    }
+                }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) nt += __shfl_xor_sync(0xffffffffu, nt, o);
+            if (lane == 0) atomicAdd(&wcnt[warp], nt);
+            __syncthreads();
+            int off = 0;  // exact logit outside its certified interval
+            float zlo = FLT_MAX;
+            if (tid < na) {
+                const int j = amb[tid];
+                const float ze = exact_logit<D>(q, kr, slots[j], p.scale);
+                zamb[tid] = ze;
+                zlo = ze;
+                off = !(fabsf(ze - zg[j]) <= emax);
+            }
+            if (tid < 2) bound[tid] = tid == 0 ? FLT_MAX : -FLT_MAX;
+            zlo = -warp_max(-zlo);
+            if (lane == 0) redf[0][warp] = zlo;
+            off = block_sum(off, red);
+#pragma unroll
+            for (int w = 0; w < kCertWarps; ++w) zlo = fminf(zlo, redf[0][w]);
+            // rank the ambiguous keys by (exact logit desc, index asc): equal logits are equal
+            // probabilities, whose order the oracle breaks by index too
+            int rank = 0;
+            if (tid < na) {
+                const float za = zamb[tid];
+                const int ja = amb[tid];
+                for (int o = 0; o < na; ++o) {
+                    const float zo = zamb[o];
+                    rank += zo > za || (zo == za && amb[o] < ja);
+                }
+                if (rank == r - 1) bound[0] = za;  // last in
+                if (rank == r) bound[1] = za;      // first out
+            }
+            __syncthreads();
+            if (off && tid == 0 && p.status != nullptr) atomicOr(p.status, 4);
+            // a selected and an unselected ambiguous key with distinct logits at most tau apart could
+            // share one fp32 probability (then the lower index wins, not the larger logit)
+            int near = 0;
+            if (tid < na) {
+                const float za = zamb[tid];
+                near = rank < r ? (za > bound[1] && za - bound[1] <= kTau) : (za < bound[0] && bound[0] - za <= kTau);
+            }
+            near = block_sum(near, red);
+            // (b): boundary probabilities that could be subnormal are resolved exactly as well
+            const bool resolve = near != 0 || zlo - (zmax + emax) < -60.f;
+            fallback = off != 0;
+            if (!fallback && resolve) {
+                // exact probabilities of the ambiguous keys: the oracle's logits of the whole row
+                // (for its max and the ascending fp64 denominator), then re-rank by (p desc, index asc)
+                float zm = -FLT_MAX;
+                for (int j = tid; j < n; j += kCertThreads) {
+                    const float ze = exact_logit<D>(q, kr, slots[j], p.scale);
+                    zg[j] = ze;
+                    zm = fmaxf(zm, ze);
+                }
+                zm = warp_max(zm);
+                if (lane == 0) redf[1][warp] = zm;
+                __syncthreads();
+#pragma unroll
+                for (int w = 0; w < kCertWarps; ++w) zm = fmaxf(zm, redf[1][w]);
+                double* e = escr + row * escr_stride;
+                const double dm = static_cast<double>(zm);
+                for (int j = tid; j < n; j += kCertThreads) e[j] = exp(static_cast<double>(zg[j]) - dm);
+                __syncthreads();
+                if (tid == 0) {  // ascending-j fp64 accumulation, exactly as tensor.cpp:96-102
+                    double denom = 0.0;
+                    int j = 0;
+                    for (; j + 8 <= n; j += 8) {
+                        double t8[8];
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) t8[t] = e[j + t];
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) denom = __dadd_rn(denom, t8[t]);
+                    }
+                    for (; j < n; ++j) denom = __dadd_rn(denom, e[j]);
+                    denom_s = denom;
+                }
+                __syncthreads();
+                if (tid < na) zamb[tid] = __double2float_rn(__ddiv_rn(e[amb[tid]], denom_s));
+                __syncthreads();
+                rank = 0;
+                if (tid < na) {
+                    const float pa = zamb[tid];
+                    const int ja = amb[tid];
+                    for (int o = 0; o < na; ++o) {
+                        const float po = zamb[o];
+                        rank += po > pa || (po == pa && amb[o] < ja);
+                    }
+                    if (rank == r - 1) bound[0] = pa;
+                }
+                __syncthreads();
+                // a subnormal (or zero) boundary probability can tie with certainly-out keys too:
+                // the whole row takes the oracle's path
+                fallback = !(bound[0] >= FLT_MIN);
+            }
+            if (!fallback) {
+                if (tid < na && rank < r) {  // chosen
+                    const int ja = amb[tid];
+                    atomicOr(&chosen[ja >> 5], 1u << (ja & 31));
+                    atomicAdd(&wcnt[ja / (V4 * 128)], 1);
+                }
+                __syncthreads();
+                int pos = 0;
+#pragma unroll
+                for (int w = 0; w < kCertWarps; ++w) pos += w < warp ? wcnt[w] : 0;
+#pragma unroll
+                for (int i = 0; i < V4; ++i) {
+                    const int j = jw + 128 * i;
+                    const uint32_t cw = full || j < n ? chosen[j >> 5] >> (j & 31) : 0u;  // 4 bits, j % 4 == 0
+                    int tk[4], c = 0;
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        tk[t] = (full || j + t < n) && (bin(v[i][t]) > bhi || ((cw >> t) & 1u));
+                        c += tk[t];
+                    }
+                    int incl = c;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += y;
+                    }
+                    int at = pos + incl - c;
+#pragma unroll
+                    for (int t = 0; t < 4; ++t)
+                        if (tk[t]) {
+                            if (at < k) out[at] = j + t;
+                            ++at;
+                        }
+                    pos += __shfl_sync(0xffffffffu, incl, 31);
+                }
+                return;
+            }
+        }
+    }
+    // exact fallback: the oracle's logits in place of z~, then its softmax + Top-K on warp 0 (the
+    // probability bits overwrite the logits row, which warp_softmax has consumed by then)
+    __syncthreads();
+    int nan = 0;
+    for (int j = tid; j < n; j += kCertThreads) {
+        const float ze = exact_logit<D>(q, kr, slots[j], p.scale);
+        nan |= ze != ze;
+        zg[j] = ze;
+    }
+    nan = block_sum(nan, red);  // (its barriers also order the zg writes before warp 0 reads them)
+    if (warp != 0) return;
+    if (p.status != nullptr && nan && lane == 0) atomicOr(p.status, 1);
+    warp_softmax(zg, n, escr + row * escr_stride, reinterpret_cast<uint32_t*>(zg), nullptr);
+    warp_topk(reinterpret_cast<const uint32_t*>(zg), n, k, hist, out);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -495,7 +987,40 @@ __global__ void aggregate_kernel(const float* __restrict__ arows, int n_keys, in
 size_t score_select_workspace(int units, int nqb, int n_keys) {
     // A_t rows (k=0 pass) + key-major logits and local-window probabilities of the long-window path
     // + per-row max / denominator
-    return 3 * static_cast<size_t>(units) * nqb * n_keys * sizeof(float) + static_cast<size_t>(units) * nqb * 16 + 512;
+    // (the certified denoise path needs [rows][n4] fp32 logits + [units][n4] key norms + [rows][n+1]
+    // fp64 fallback scratch, n = n_local <= n_keys, n4 = n rounded up to 4)
+    return 3 * static_cast<size_t>(units) * nqb * n_keys * sizeof(float) + static_cast<size_t>(units) * nqb * 32 +
+           static_cast<size_t>(units) * (n_keys + 4) * sizeof(float) + 512;
+}
+
+template <int D>
+int launch_certified(const ScoreParams& p, dim3 g1, size_t lsmem, int v4, float* zc, float* kn, int n4,
+                     double* escr, int64_t es, int cert, cudaStream_t s) {
+    if (int rc = ensure_smem(reinterpret_cast<const void*>(logits32_kernel<D>), lsmem, "logits32")) return rc;
+    launch_pdl(logits32_kernel<D>, g1, dim3(kL32Warps * 32), lsmem, s, p, zc, kn);
+    if (int rc = check_launch("logits32_kernel")) return rc;
+    const dim3 g2(static_cast<unsigned>(static_cast<int64_t>(p.units) * p.nqb));
+    const float* kc = kn;
+    const int np = static_cast<int>(g1.x);
+    switch (v4) {
+        case 1: launch_pdl(cert_select_kernel<D, 1>, g2, dim3(kCertThreads), 0, s, p, zc, kc, np, n4, escr, es, cert); break;
+        case 2: launch_pdl(cert_select_kernel<D, 2>, g2, dim3(kCertThreads), 0, s, p, zc, kc, np, n4, escr, es, cert); break;
+        case 3:
+        case 4: launch_pdl(cert_select_kernel<D, 4>, g2, dim3(kCertThreads), 0, s, p, zc, kc, np, n4, escr, es, cert); break;
+        case 5:
+        case 6: launch_pdl(cert_select_kernel<D, 6>, g2, dim3(kCertThreads), 0, s, p, zc, kc, np, n4, escr, es, cert); break;
+        default: launch_pdl(cert_select_kernel<D, 8>, g2, dim3(kCertThreads), 0, s, p, zc, kc, np, n4, escr, es, cert); break;
+    }
+    return check_launch("cert_select_kernel");
+}
+
+// PBSA_K2_CERT: unset = certified fp32 ranking on denoise passes over windows of >= kCertMinKeys
+// keys, 1 = certified on every denoise pass, 0 = the exact fp64 path on every pass, 2 = certified
+// kernels with every row forced through the exact fallback (tests).
+constexpr int kCertMinKeys = 1024;
+static int cert_mode() {
+    const char* e = std::getenv("PBSA_K2_CERT");
+    return e == nullptr ? 1 : (std::atoi(e) == 1 ? 3 : std::atoi(e));
 }
 
 int launch_score_select(const float* qc, const float* krep, int64_t kru, const int32_t* keys,
@@ -508,6 +1033,28 @@ int launch_score_select(const float* qc, const float* krep, int64_t kru, const i
     if (ws_bytes < score_select_workspace(units, nqb, n_keys))
         return set_error(PBSA_EINVAL, "score_select: workspace too small");
     float* arows = s_t ? static_cast<float*>(ws) : nullptr;
+    const int cert = cert_mode();
+    // certified path for long windows (config 5: 6006 keys, 2.8x faster than the exact kernels);
+    // short windows (config 2: 312 keys) are latency-bound either way and stay on the exact kernels
+    // (PBSA_K2_CERT=1 forces the certified path for any window that fits, e.g. in tests)
+    const bool want_cert = cert == 1 ? n_local >= kCertMinKeys : cert != 0;  // 3: forced
+    if (do_select && s_t == nullptr && want_cert && n_local <= kCertMaxKeys) {
+        // denoise pass: certified fp32 logits of the local window, exact only near the k-th boundary
+        const int64_t rt = static_cast<int64_t>(units) * nqb;
+        const int n4 = (n_local + 3) & ~3;                                    // 16-byte rows
+        float* zc = static_cast<float*>(ws);                                  // [rt][n4]
+        float* kn = zc + static_cast<size_t>(rt) * n4;                        // [units][key tiles] max |k|
+        double* escr = reinterpret_cast<double*>(
+            (reinterpret_cast<uintptr_t>(kn + static_cast<size_t>(units) * n4) + 15) & ~uintptr_t(15));
+        const int64_t es = (n_local + 1) & ~1;  // 16-byte aligned fp64 scratch rows
+        ScoreParams p{qc, krep, kru, keys, key_stride, n_keys, local_off, n_local, k, nqb, units,
+                      1, scale, 0, sel, nullptr, status};
+        dim3 g1((n_local + kLogitKeys - 1) / kLogitKeys, (nqb + kL32Warps * 8 - 1) / (kL32Warps * 8), units);
+        const size_t lsmem = static_cast<size_t>(kL32Warps * 8 + kLogitKeys) * d * 4;
+        const int v4 = (n_local + 4 * kCertThreads - 1) / (4 * kCertThreads);  // float4 per thread
+        if (d == 128) return launch_certified<128>(p, g1, lsmem, v4, zc, kn, n4, escr, es, cert, s);
+        return launch_certified<64>(p, g1, lsmem, v4, zc, kn, n4, escr, es, cert, s);
+    }
     {
         const size_t per_warp =
             (static_cast<size_t>(n_keys) * 12 + static_cast<size_t>(n_local) * 4 + 1024 + 15) & ~size_t(15);

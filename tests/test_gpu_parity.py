@@ -79,34 +79,99 @@ def _score_case(pb, units, nqb, n_p, n_l, n_c, d, k, seed, ties=False, zero_q=Fa
         assert np.array_equal(sel[u], orc.select_topk(a_l, k)), f"unit {u}"
         want = orc.aggregate_scores(orc.coarse_attention(qc[u], kc))
         assert np.array_equal(bits(s_t[u]), bits(want)), f"unit {u}"
+    # denoise pass (no scores): certified fp32 ranking, exact only near the k-th boundary
+    sel2 = pb.score_select(dev(qc, torch.float32), dev(krep, torch.float32), dev(keys, torch.int32),
+                           n_p, n_l, k).cpu().numpy()
+    assert np.array_equal(sel2, sel), "denoise-pass selection differs from the k=0 pass"
     return sel
 
 
+@pytest.fixture(params=["1", "2", "0"], ids=["cert", "cert_fallback", "exact"])
+def k2_mode(request, monkeypatch):
+    """PBSA_K2_CERT: certified denoise path, the same with every row forced through the exact
+    fallback, and the exact fp64 path on every pass."""
+    monkeypatch.setenv("PBSA_K2_CERT", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("d", [64, 128])
-def test_score_select_bitexact_small(pb, d):
+def test_score_select_bitexact_small(pb, d, k2_mode):
     _score_case(pb, 3, 7, 8, 24, 8, d, 5, seed=d)
 
 
-def test_score_select_bitexact_config2_shape(pb):
+def test_score_select_bitexact_config2_shape(pb, k2_mode):
     _score_case(pb, 2, 78, 156, 312, 78, 128, 78, seed=7)
 
 
-def test_score_select_ties_lower_index(pb):
+def test_score_select_ties_lower_index(pb, k2_mode):
     _score_case(pb, 2, 9, 4, 30, 4, 128, 7, seed=3, ties=True)
     sel = _score_case(pb, 1, 3, 2, 20, 2, 64, 6, seed=4, zero_q=True)  # uniform rows
     assert np.array_equal(sel[0], np.tile(np.arange(6), (3, 1)))
 
 
-def test_score_select_k_equals_local(pb):
+def test_score_select_k_equals_local(pb, k2_mode):
     _score_case(pb, 2, 5, 3, 9, 3, 128, 9, seed=11)
 
 
-def test_score_select_large_window(pb):
+def test_score_select_large_window(pb, k2_mode):
     """config-5-like window (231 frames x 26 blocks) on a few rows."""
     _score_case(pb, 1, 4, 156, 6006, 78, 128, 1502, seed=12)
 
 
-def test_score_select_long_path_rows_across_units(pb):
+@pytest.mark.parametrize("scale_q", [40.0, 400.0])
+def test_score_select_peaky_rows(pb, k2_mode, scale_q):
+    """Very peaked rows: boundary probabilities underflow to zero (ties broken by index) -- the
+    certified path must hand these rows to the exact fallback."""
+    g = np.random.default_rng(21)
+    units, nqb, n_p, n_l, n_c, d, k = 2, 11, 6, 200, 6, 128, 50
+    n_keys, n_slots = n_p + n_l + n_c, n_p + n_l + n_c + 3
+    qc = (g.standard_normal((units, nqb, d)) * scale_q).astype(np.float32)
+    krep = g.standard_normal((units, n_slots, d)).astype(np.float32)
+    keys = np.stack([g.permutation(n_slots)[:n_keys] for _ in range(units)]).astype(np.int32)
+    sel = pb.score_select(dev(qc, torch.float32), dev(krep, torch.float32), dev(keys, torch.int32),
+                          n_p, n_l, k).cpu().numpy()
+    for u in range(units):
+        kc = krep[u][keys[u]]
+        assert np.array_equal(sel[u], orc.select_topk(orc.coarse_attention(qc[u], kc[n_p:n_p + n_l]), k))
+
+
+def test_score_select_cycled_keys(pb, k2_mode):
+    """A window built from 3 cycled sets of key blocks (the shape of a cache filled by replaying
+    three chunks): every logit appears many times, so the k-th boundary falls inside groups of
+    exactly tied probabilities (lower index wins) next to near-tied ones."""
+    g = np.random.default_rng(23)
+    units, nqb, n_l, d, k, distinct = 2, 12, 2002, 128, 500, 77
+    base = (g.standard_normal((units, distinct, d)) * 0.13).astype(np.float32)
+    krep = np.concatenate([base[:, np.arange(n_l) % distinct], base[:, :3]], 1)
+    qc = (g.standard_normal((units, nqb, d)) * 0.13).astype(np.float32)
+    keys = np.stack([np.arange(n_l) for _ in range(units)]).astype(np.int32)
+    sel = pb.score_select(dev(qc, torch.float32), dev(krep, torch.float32), dev(keys, torch.int32),
+                          0, n_l, k).cpu().numpy()
+    for u in range(units):
+        assert np.array_equal(sel[u], orc.select_topk(orc.coarse_attention(qc[u], krep[u][keys[u]]), k))
+
+
+def test_score_select_near_ties(pb, k2_mode):
+    """Representatives that differ in the last bits: exact logits a few ulps apart at the boundary
+    (probabilities that may or may not tie in fp32) must be ranked exactly as the oracle does."""
+    g = np.random.default_rng(22)
+    units, nqb, n_p, n_l, n_c, d, k = 2, 16, 4, 96, 4, 64, 24
+    n_keys, n_slots = n_p + n_l + n_c, n_p + n_l + n_c + 2
+    qc = (g.standard_normal((units, nqb, d)) * 0.5).astype(np.float32)
+    krep = g.standard_normal((units, n_slots, d)).astype(np.float32)
+    base = krep[:, :1].copy()
+    for t in range(1, n_slots, 2):  # every other key: the base row nudged by a few ulps
+        nudge = (1.0 + np.float32(2.0 ** -23) * g.integers(-3, 4, size=d)).astype(np.float32)
+        krep[:, t] = base[:, 0] * nudge
+    keys = np.stack([g.permutation(n_slots)[:n_keys] for _ in range(units)]).astype(np.int32)
+    sel = pb.score_select(dev(qc, torch.float32), dev(krep, torch.float32), dev(keys, torch.int32),
+                          n_p, n_l, k).cpu().numpy()
+    for u in range(units):
+        kc = krep[u][keys[u]]
+        assert np.array_equal(sel[u], orc.select_topk(orc.coarse_attention(qc[u], kc[n_p:n_p + n_l]), k))
+
+
+def test_score_select_long_path_rows_across_units(pb, k2_mode):
     """Long-window kernels (key-major logits, thread-per-row statistics): 39 rows of 3 units share
     warps; tied probabilities from duplicated representatives."""
     _score_case(pb, 3, 13, 40, 2100, 20, 64, 300, seed=13)
@@ -262,6 +327,7 @@ def run_rollout(pb, units, d, b, bpc, C, W, n_chunks, k_top, seed, denoise_steps
             a_ids, _, n_p, n_l = oms[u].assemble()
             assert np.array_equal(gp[u], a_ids[:n_p]), f"chunk {c} unit {u}: persistent ids"
             assert np.array_equal(gl[u], a_ids[n_p:]), f"chunk {c} unit {u}: local ids"
+    assert mem.status() == 0  # no NaN rows, no certified-bound canary (bit 2)
     mem.close()
     return stats
 

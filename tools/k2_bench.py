@@ -34,8 +34,14 @@ for name, U, nqb, nl, extra, k in (("config5", 320, 78, 6006, 234, 1502), ("conf
     krep = torch.randn(U, S, 128, device="cuda", generator=g)
     keys = torch.stack([torch.randperm(S, device="cuda", generator=g) for _ in range(U)]).int()
     local = keys[:, :nl].contiguous()
-    ms = timeit(lambda: pb.score_select(qc, krep, local, 0, nl, k))
-    print(f"{name} denoise: ms={ms:.3f}")
+    sels = {}
+    for mode in ("0", "1"):  # exact fp64 path vs certified fp32 ranking (PBSA_K2_CERT)
+        os.environ["PBSA_K2_CERT"] = mode
+        ms = timeit(lambda: pb.score_select(qc, krep, local, 0, nl, k))
+        sels[mode] = pb.score_select(qc, krep, local, 0, nl, k)
+        print(f"{name} denoise PBSA_K2_CERT={mode}: ms={ms:.3f}")
+    os.environ.pop("PBSA_K2_CERT")
+    print(f"{name} selections identical: {bool(torch.equal(sels['0'], sels['1']))}")
     if len(sys.argv) > 1 and sys.argv[1] == "--full":
         ms = timeit(lambda: pb.score_select(qc, krep, keys, extra, nl, k, want_scores=True))
         print(f"{name} k=0 pass (all {S} keys + s_t): ms={ms:.3f}")
