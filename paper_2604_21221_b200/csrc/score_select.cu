@@ -16,7 +16,9 @@
 //                        exactly like the oracle), 4-pass 8-bit radix select on the fp32 probability
 //                        bits, ballot compaction of the winners; A_t rows at the k=0 pass
 //   aggregate_kernel     thread per key block, ascending-row fp64 column sums (k=0 pass only)
-// and a key-major variant for long windows (config 5) below.
+// a key-major variant for long windows (config 5), and for denoise passes over long windows the
+// certified fp32 ranking (logits32_kernel + cert_select_kernel), which reaches the same indices
+// with exact fp64 work only for the keys near the k-th boundary.
 #include <cfloat>
 #include <cstdlib>
 
