@@ -1057,6 +1057,11 @@ int launch_score_select(const float* qc, const float* krep, int64_t kru, const i
         if (d == 128) return launch_certified<128>(p, g1, lsmem, v4, zc, kn, n4, escr, es, cert, s);
         return launch_certified<64>(p, g1, lsmem, v4, zc, kn, n4, escr, es, cert, s);
     }
+    if (s_t == nullptr) {  // no A_t: only the local window's logits are needed
+        keys += local_off;
+        n_keys = n_local;
+        local_off = 0;
+    }
     {
         const size_t per_warp =
             (static_cast<size_t>(n_keys) * 12 + static_cast<size_t>(n_local) * 4 + 1024 + 15) & ~size_t(15);
