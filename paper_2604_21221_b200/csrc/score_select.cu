@@ -132,13 +132,40 @@ __device__ uint32_t warp_kth(const uint32_t* pb, int n, int k, uint32_t* hist, i
     return prefix;
 }
 
+// Short rows (n <= 32 * NPL): the k-th largest by a 32-step binary search on the value, the row
+// held in registers (NPL per lane) and each step one compare per value plus one warp reduction --
+// no shared-memory histograms or match/atomic traffic.
+template <int NPL>
+__device__ uint32_t warp_kth_reg(const uint32_t* pb, int n, int k, int* kk_out) {
+    const int lane = threadIdx.x & 31;
+    uint32_t v[NPL];
+#pragma unroll
+    for (int i = 0; i < NPL; ++i) v[i] = lane + 32 * i < n ? pb[lane + 32 * i] : 0u;
+    uint32_t t = 0;  // largest value with at least k elements >= it
+#pragma unroll 1
+    for (int bit = 31; bit >= 0; --bit) {
+        const uint32_t cand = t | (1u << bit);
+        int c = 0;
+#pragma unroll
+        for (int i = 0; i < NPL; ++i) c += (lane + 32 * i < n) & (v[i] >= cand);
+        if (static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<uint32_t>(c))) >= k) t = cand;
+    }
+    int gt = 0;
+#pragma unroll
+    for (int i = 0; i < NPL; ++i) gt += (lane + 32 * i < n) & (v[i] > t);
+    *kk_out = k - static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<uint32_t>(gt)));
+    return t;
+}
+
 // k largest of pb[0..n) (non-negative float bits => unsigned order), ties -> lower index.
 // Writes the winners' indices ascending to out[0..k).
 __device__ void warp_topk(const uint32_t* pb, int n, int k, uint32_t* hist, int32_t* out) {
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
     int kk;
-    const uint32_t prefix = warp_kth(pb, n, k, hist, &kk);
+    const uint32_t prefix = n <= 128   ? warp_kth_reg<4>(pb, n, k, &kk)
+                            : n <= 512 ? warp_kth_reg<16>(pb, n, k, &kk)
+                                       : warp_kth(pb, n, k, hist, &kk);
     // prefix = value of the k-th largest element; take every element above it and the first kk
     // (lowest indices) equal to it.
     int run = 0, tie_run = 0;
