@@ -151,6 +151,23 @@ def test_score_select_cycled_keys(pb, k2_mode):
         assert np.array_equal(sel[u], orc.select_topk(orc.coarse_attention(qc[u], krep[u][keys[u]]), k))
 
 
+@pytest.mark.parametrize("d,n_l,k", [(64, 1030, 257), (128, 1027, 1), (128, 1500, 1500), (64, 9001, 2250)])
+def test_score_select_long_window_defaults(pb, d, n_l, k):
+    """Default dispatch (PBSA_K2_CERT unset): windows >= 1024 keys take the certified denoise path
+    (odd lengths, k = 1, k = n), windows beyond its register capacity (9001 keys) the exact kernels."""
+    g = np.random.default_rng(n_l + k)
+    units, nqb, n_p, n_c = 2, 5, 7, 3
+    n_keys, n_slots = n_p + n_l + n_c, n_p + n_l + n_c + 4
+    qc = (g.standard_normal((units, nqb, d)) * 0.3).astype(np.float32)
+    krep = g.standard_normal((units, n_slots, d)).astype(np.float32)
+    keys = np.stack([g.permutation(n_slots)[:n_keys] for _ in range(units)]).astype(np.int32)
+    sel = pb.score_select(dev(qc, torch.float32), dev(krep, torch.float32), dev(keys, torch.int32),
+                          n_p, n_l, k).cpu().numpy()
+    for u in range(units):
+        kc = krep[u][keys[u]]
+        assert np.array_equal(sel[u], orc.select_topk(orc.coarse_attention(qc[u], kc[n_p:n_p + n_l]), k))
+
+
 def test_score_select_near_ties(pb, k2_mode):
     """Representatives that differ in the last bits: exact logits a few ulps apart at the boundary
     (probabilities that may or may not tie in fp32) must be ranked exactly as the oracle does."""
