@@ -141,18 +141,19 @@ __device__ uint32_t warp_kth_reg(const uint32_t* pb, int n, int k, int* kk_out) 
     uint32_t v[NPL];
 #pragma unroll
     for (int i = 0; i < NPL; ++i) v[i] = lane + 32 * i < n ? pb[lane + 32 * i] : 0u;
+    // (the padding values are 0, never >= a candidate, which always has a bit set, nor > t)
     uint32_t t = 0;  // largest value with at least k elements >= it
 #pragma unroll 1
     for (int bit = 31; bit >= 0; --bit) {
         const uint32_t cand = t | (1u << bit);
         int c = 0;
 #pragma unroll
-        for (int i = 0; i < NPL; ++i) c += (lane + 32 * i < n) & (v[i] >= cand);
+        for (int i = 0; i < NPL; ++i) c += v[i] >= cand;
         if (static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<uint32_t>(c))) >= k) t = cand;
     }
     int gt = 0;
 #pragma unroll
-    for (int i = 0; i < NPL; ++i) gt += (lane + 32 * i < n) & (v[i] > t);
+    for (int i = 0; i < NPL; ++i) gt += v[i] > t;
     *kk_out = k - static_cast<int>(__reduce_add_sync(0xffffffffu, static_cast<uint32_t>(gt)));
     return t;
 }
@@ -164,6 +165,8 @@ __device__ void warp_topk(const uint32_t* pb, int n, int k, uint32_t* hist, int3
     const uint32_t lt = (1u << lane) - 1u;
     int kk;
     const uint32_t prefix = n <= 128   ? warp_kth_reg<4>(pb, n, k, &kk)
+                            : n <= 256 ? warp_kth_reg<8>(pb, n, k, &kk)
+                            : n <= 384 ? warp_kth_reg<12>(pb, n, k, &kk)
                             : n <= 512 ? warp_kth_reg<16>(pb, n, k, &kk)
                                        : warp_kth(pb, n, k, hist, &kk);
     // prefix = value of the k-th largest element; take every element above it and the first kk
