@@ -231,6 +231,13 @@ public:
                     float* lse = nullptr, double scale = 0.0, cudaStream_t s = nullptr) {
         detail::check(pbsa_attend_qkv(m_, q, k, v, k_top, static_cast<float>(scale), mode, o, lse, s));
     }
+    // attend_qkv on HOST chunks (pinned): upload / compute / download pipelined across calls;
+    // o_host is valid after host_sync()
+    void attend_qkv_host(const void* q, const void* k, const void* v, int k_top, int mode, void* o_host,
+                         double scale = 0.0, cudaStream_t s = nullptr) {
+        detail::check(pbsa_attend_qkv_host(m_, q, k, v, k_top, static_cast<float>(scale), mode, o_host, s));
+    }
+    void host_sync() { detail::check(pbsa_mem_host_sync(m_)); }
     // the same on device chunk latents [batch][T][H][W][heads*d] bf16 (blockify / unblockify fused)
     void attend_latent(const void* q, const void* k, const void* v, const pbsa_latent_geom& g, int k_top, int mode,
                        void* o, float* lse = nullptr, double scale = 0.0, cudaStream_t s = nullptr) {

@@ -146,6 +146,17 @@ int pbsa_mem_status(const pbsa_mem* m, int* flags, void* stream);
  * slots and compresses K and Q (K1), then K2 -> K3 (-> K4) as pbsa_attend. */
 int pbsa_attend_qkv(pbsa_mem* m, const void* q, const void* k_chunk, const void* v_chunk, int k_top,
                     float scale, int mode, void* o, float* lse, void* stream);
+/* pbsa_attend_qkv for chunks that live in HOST memory (pinned or cudaHostRegister'ed, the
+ * [units][blocks_per_chunk*b][d] bf16 layout of pbsa_attend_qkv): the Q/K/V upload runs on an
+ * internal stream into one of two device staging sets, the compute on `stream`, and the download of
+ * O into o_host on a second internal stream, so the upload of call i+1 and the download of call i-1
+ * overlap the compute of call i.  Returns without waiting; q/k/v_host must stay unchanged and o_host
+ * unread until pbsa_mem_host_sync returns (work later enqueued on `stream` is ordered after this
+ * call's compute, not after its download). */
+int pbsa_attend_qkv_host(pbsa_mem* m, const void* q_host, const void* k_host, const void* v_host, int k_top,
+                         float scale, int mode, void* o_host, void* stream);
+/* Waits for every upload and download issued by pbsa_attend_qkv_host so far. */
+int pbsa_mem_host_sync(pbsa_mem* m);
 /* Chunk latents in the reference's Latent4D layout (proj/include/pbsa/tensor.hpp:30-47: (t, h, w, d)
  * row-major, d = heads * head_dim), one per batch element: [batch][T][H][W][heads*d]
  * bf16, blocked by blockify's (B_t, B_h, B_w) (proj/include/pbsa/blockify.hpp:11-67; block id

@@ -141,6 +141,12 @@ struct pbsa_mem {
     std::vector<cudaEvent_t> ev_attend, ev_write;
     int prof_max = 0, prof_attend = 0, prof_write = 0;
     bool prof_on = false;
+    // host-resident chunks (pbsa_attend_qkv_host): two device staging sets {q, k, v, o}, an upload
+    // and a download stream, and per set: uploaded / computed / downloaded events
+    bf16* hstage[2][4] = {};
+    cudaStream_t up = nullptr, down = nullptr;
+    cudaEvent_t ev_up[2] = {}, ev_done[2] = {}, ev_down[2] = {};
+    long long host_calls = 0;
 };
 
 namespace {
@@ -167,7 +173,28 @@ void prof_mark(pbsa_mem* m, int i, cudaStream_t s) {
     cudaEventRecord(m->ev_attend[static_cast<size_t>(m->prof_attend) * 5 + i], s);
 }
 
+void free_host_path(pbsa_mem* m) {
+    for (auto& set : m->hstage)
+        for (bf16*& p : set)
+            if (p) {
+                cudaFree(p);
+                p = nullptr;
+            }
+    for (int i = 0; i < 2; ++i)
+        for (cudaEvent_t* e : {&m->ev_up[i], &m->ev_done[i], &m->ev_down[i]})
+            if (*e) {
+                cudaEventDestroy(*e);
+                *e = nullptr;
+            }
+    for (cudaStream_t* st : {&m->up, &m->down})
+        if (*st) {
+            cudaStreamDestroy(*st);
+            *st = nullptr;
+        }
+}
+
 void free_mem(pbsa_mem* m) {
+    free_host_path(m);
     free_events(m);
     void* ptrs[] = {m->k_pool, m->v_pool, m->krep, m->dev.p_slot, m->dev.p_id, m->dev.p_score,
                     m->dev.l_slot, m->dev.l_id, m->dev.stage, m->dev.free_slot, m->dev.dense,
@@ -636,6 +663,54 @@ int pbsa_attend_qkv(pbsa_mem* m, const void* q, const void* k_chunk, const void*
         ++m->prof_write;
     }
     return attend_impl(m, q, k_top, scale, mode, o, lse, stream, true, nullptr);
+}
+
+int pbsa_attend_qkv_host(pbsa_mem* m, const void* q_host, const void* k_host, const void* v_host, int k_top,
+                         float scale, int mode, void* o_host, void* stream) {
+    PBSA_REQUIRE(m != nullptr && q_host != nullptr && k_host != nullptr && v_host != nullptr && o_host != nullptr,
+                 "attend_qkv_host: null pointer");
+    cudaStream_t s = as_stream(stream);
+    const size_t bytes = static_cast<size_t>(m->units) * m->bpc * m->b * m->d * sizeof(bf16);
+    if (m->up == nullptr) {  // first call: staging sets, copy streams, events
+        bool ok = cudaStreamCreateWithFlags(&m->up, cudaStreamNonBlocking) == cudaSuccess &&
+                  cudaStreamCreateWithFlags(&m->down, cudaStreamNonBlocking) == cudaSuccess;
+        for (int i = 0; ok && i < 2; ++i) {
+            for (int t = 0; ok && t < 4; ++t) ok = cudaMalloc(&m->hstage[i][t], bytes) == cudaSuccess;
+            ok = ok && cudaEventCreateWithFlags(&m->ev_up[i], cudaEventDisableTiming) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&m->ev_done[i], cudaEventDisableTiming) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&m->ev_down[i], cudaEventDisableTiming) == cudaSuccess;
+        }
+        if (!ok) {
+            free_host_path(m);
+            cudaGetLastError();
+            return set_error(PBSA_ECUDA, "attend_qkv_host: staging allocation failed");
+        }
+    }
+    const int b = static_cast<int>(m->host_calls & 1);
+    bf16* const* st = m->hstage[b];
+    if (m->host_calls >= 2) {  // set b was last used two calls ago
+        PBSA_CUDA(cudaStreamWaitEvent(m->up, m->ev_done[b], 0));  // its inputs are consumed
+        PBSA_CUDA(cudaStreamWaitEvent(s, m->ev_down[b], 0));      // its output has been read back
+    }
+    PBSA_CUDA(cudaMemcpyAsync(st[0], q_host, bytes, cudaMemcpyHostToDevice, m->up));
+    PBSA_CUDA(cudaMemcpyAsync(st[1], k_host, bytes, cudaMemcpyHostToDevice, m->up));
+    PBSA_CUDA(cudaMemcpyAsync(st[2], v_host, bytes, cudaMemcpyHostToDevice, m->up));
+    PBSA_CUDA(cudaEventRecord(m->ev_up[b], m->up));
+    PBSA_CUDA(cudaStreamWaitEvent(s, m->ev_up[b], 0));
+    if (int rc = pbsa_attend_qkv(m, st[0], st[1], st[2], k_top, scale, mode, st[3], nullptr, stream)) return rc;
+    PBSA_CUDA(cudaEventRecord(m->ev_done[b], s));
+    PBSA_CUDA(cudaStreamWaitEvent(m->down, m->ev_done[b], 0));
+    PBSA_CUDA(cudaMemcpyAsync(o_host, st[3], bytes, cudaMemcpyDeviceToHost, m->down));
+    PBSA_CUDA(cudaEventRecord(m->ev_down[b], m->down));
+    ++m->host_calls;
+    return PBSA_OK;
+}
+
+int pbsa_mem_host_sync(pbsa_mem* m) {
+    PBSA_REQUIRE(m != nullptr, "mem_host_sync: null memory");
+    if (m->up) PBSA_CUDA(cudaStreamSynchronize(m->up));
+    if (m->down) PBSA_CUDA(cudaStreamSynchronize(m->down));
+    return PBSA_OK;
 }
 
 int pbsa_mem_status(const pbsa_mem* m, int* flags, void* stream) {

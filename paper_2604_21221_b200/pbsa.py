@@ -384,6 +384,30 @@ class Memory:
                                   _ptr(lse), _stream()))
         return (o, lse) if want_lse else o
 
+    def attend_qkv_host(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, k_top: int,
+                        mode: int = MODE_DENOISE, out: torch.Tensor | None = None,
+                        scale: float | None = None) -> torch.Tensor:
+        """attend_qkv on HOST chunks (pbsa_attend_qkv_host): q / k / v pinned CPU bf16 tensors of the
+        chunk shape; O lands in `out` (pinned CPU).  Uploads, compute and downloads are pipelined
+        across calls (the upload of call i+1 overlaps the compute of call i); inputs must stay
+        unchanged and `out` unread until host_sync()."""
+        shape = (self.units, self.blocks_per_chunk * self.b, self.d)
+        for name, t in (("q", q), ("k", k), ("v", v)):
+            if t.device.type != "cpu" or t.dtype != torch.bfloat16 or not t.is_contiguous() or t.shape != shape:
+                raise PbsaError(f"attend_qkv_host: {name} must be a contiguous CPU bf16 tensor of shape {shape}")
+        # (pageable memory works too, but its copies cannot overlap the compute: pin for the pipeline)
+        o = torch.empty(shape, dtype=torch.bfloat16).pin_memory() if out is None else out
+        if o.device.type != "cpu" or not o.is_contiguous() or o.shape != shape or o.dtype != torch.bfloat16:
+            raise PbsaError(f"attend_qkv_host: out must be a contiguous CPU bf16 tensor of shape {shape}")
+        check(LIB.pbsa_attend_qkv_host(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), int(k_top),
+                                       0.0 if scale is None else float(scale), int(mode), o.data_ptr(),
+                                       _stream()))
+        return o
+
+    def host_sync(self) -> None:
+        """Wait for every upload / download issued by attend_qkv_host."""
+        check(LIB.pbsa_mem_host_sync(self._h))
+
     def attend_latent(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, block_shape, k_top: int,
                       mode: int = MODE_DENOISE, scale: float | None = None, out: torch.Tensor | None = None,
                       want_lse: bool = False):

@@ -482,3 +482,29 @@ def test_bsa_bwd_parity(pb, d, b):
 def test_bsa_bwd_dense_only_and_odd_pairs(pb):
     _bsa_bwd_case(pb, 2, 4, 60, 128, 7, 0, 0, seed=61)     # no local window, odd dense count
     _bsa_bwd_case(pb, 1, 3, 60, 128, 5, 9, 9, seed=62)     # k = N_l, odd local count
+
+
+def test_attend_qkv_host_pipelined_matches_device(pb):
+    """pbsa_attend_qkv_host (pinned host chunks, upload / compute / download pipelined over two
+    staging sets) gives bit-identical outputs to pbsa_attend_qkv on device copies of the same
+    chunks, across denoise and cache-update calls."""
+    U, C, W, bpc, b, d, k = 3, 12, 2, 6, 60, 128, 3
+    m1, m2 = pb.Memory(U, C, W, bpc, b, d), pb.Memory(U, C, W, bpc, b, d)
+    g = torch.Generator().manual_seed(31)
+    keep, got = [], []
+    for c in range(7):
+        for step in range(3):
+            mode = pb.MODE_CACHE_UPDATE if step == 2 else pb.MODE_DENOISE
+            q, kk, vv = (torch.randn(U, bpc * b, d, generator=g).bfloat16().pin_memory() for _ in range(3))
+            o1 = m1.attend_qkv(q.cuda(), kk.cuda(), vv.cuda(), k, mode).cpu()
+            o2 = m2.attend_qkv_host(q, kk, vv, k, mode)
+            keep.append((q, kk, vv))
+            got.append((o1, o2))
+    m2.host_sync()
+    torch.cuda.synchronize()
+    for i, (o1, o2) in enumerate(got):
+        assert torch.equal(o1.view(torch.int16), o2.view(torch.int16)), f"call {i}"
+    with pytest.raises(pb.PbsaError):
+        m2.attend_qkv_host(keep[0][0].cuda(), keep[0][1], keep[0][2], k)  # device tensor: rejected
+    m1.close()
+    m2.close()
