@@ -585,6 +585,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 tc_fence_before();
                 if (threadIdx.x == 64) stamp(p, 6, j);  // about to arrive P_j
                 __syncwarp();
+                if (lane == 0) stamp(p, 9 + warp, j);  // per-warp arrival (warps 2-5 -> stamps 11-14)
                 if (lane == 0) mbar_arrive(p_full + buf);
             }
             __syncwarp();

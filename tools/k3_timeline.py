@@ -54,3 +54,8 @@ for a, b, what in ((5, 7, "S seen -> S in regs (LDTM)"), (7, 8, "exps + packs + 
                    (11, 12, "warp3 - warp2 arrival"), (11, 13, "warp4 - warp2 arrival"),
                    (11, 14, "warp5 - warp2 arrival"), (11, 2, "warp2 arrival -> MMA sees P")):
     print(f"median {what}:", int(np.median(t[b, 10:200] - t[a, 10:200])))
+print("median (S_{j+1} issued) - (P_j arrival):", int(np.median(t[1, 10:200] - t[6, 10:200])))
+print("median (MMA sees P_j) - (S_{j+1} issued):", int(np.median(t[2, 10:200] - t[1, 10:200])))
+print("median (S_{j+1} issue start) - (P_j arrival):", int(np.median(t[0, 10:200] - t[6, 10:200])))
+print("median PV_j issued - MMA sees P_j:", int(np.median(t[3, 10:200] - t[2, 10:200])))
+print("median S_{j+1} issue duration (pre_S -> S_issued):", int(np.median(t[1, 10:200] - t[0, 10:200])))

@@ -5,6 +5,20 @@
 #include "../../paper_2604_21221_b200/csrc/ptx.cuh"
 using namespace pbsa;
 
+// A reused through the collector buffer: fill on the first of two MMAs, lastuse on the second
+__device__ __forceinline__ void mma_ss_col(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, int fill) {
+    if (fill)
+        asm volatile("{ .reg .pred p; setp.ne.b32 p, 1, 0;\n"
+                     "tcgen05.mma.cta_group::1.kind::f16.collector::a::fill [%0], %1, %2, %3, p; }" ::"r"(d_tmem),
+                     "l"(a_desc), "l"(b_desc), "r"(idesc) : "memory");
+    else
+        asm volatile("{ .reg .pred p; setp.ne.b32 p, 1, 0;\n"
+                     "tcgen05.mma.cta_group::1.kind::f16.collector::a::lastuse [%0], %1, %2, %3, p; }" ::"r"(d_tmem),
+                     "l"(a_desc), "l"(b_desc), "r"(idesc) : "memory");
+}
+
+// TS = 2: pairs of SS MMAs sharing A (different B, different D), A through the collector;
+// TS = 3: the same pairs without the collector
 template <int N, int TS>
 __global__ void k(long long* out, int iters) {
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -26,7 +40,12 @@ __global__ void k(long long* out, int iters) {
             for (int it = 0; it < iters; ++it) {
 #pragma unroll
                 for (int kk = 0; kk < 8; ++kk) {
-                    if (TS) mma_ts(tmem + 256, tmem + 448 + kk * 8 % 64, bdesc + (((kk & 3) * 32) >> 4), idesc, 1u);
+                    const uint64_t b2 = bdesc + (8192 >> 4);
+                    if (TS == 2) {
+                        mma_ss_col(tmem + 256 - 64 * (kk & 1), adesc + (((kk >> 1) * 32) >> 4), (kk & 1 ? b2 : bdesc) + (((kk >> 1) * 32) >> 4), idesc, !(kk & 1));
+                    } else if (TS == 3) {
+                        mma_ss(tmem + 256 - 64 * (kk & 1), adesc + (((kk >> 1) * 32) >> 4), (kk & 1 ? b2 : bdesc) + (((kk >> 1) * 32) >> 4), idesc, 1u);
+                    } else if (TS) mma_ts(tmem + 256, tmem + 448 + kk * 8 % 64, bdesc + (((kk & 3) * 32) >> 4), idesc, 1u);
                     else mma_ss(tmem + 256, adesc + (((kk & 3) * 32) >> 4), bdesc + (((kk & 3) * 32) >> 4), idesc, 1u);
                 }
             }
@@ -60,6 +79,9 @@ int main() {
     run<64, 0>("SS M128 K16");
     run<128, 0>("SS M128 K16");
     run<256, 0>("SS M128 K16");
+    run<64, 2>("SS pairs, A collector");
+    run<64, 3>("SS pairs, no collector");
+    run<128, 2>("SS pairs, A collector");
     run<64, 1>("TS M128 K16");
     run<128, 1>("TS M128 K16");
     run<256, 1>("TS M128 K16");
