@@ -508,3 +508,30 @@ def test_attend_qkv_host_pipelined_matches_device(pb):
         m2.attend_qkv_host(keep[0][0].cuda(), keep[0][1], keep[0][2], k)  # device tensor: rejected
     m1.close()
     m2.close()
+
+
+def test_score_select_certified_fuzz(pb):
+    """Certified denoise selection (default dispatch, windows >= 1024 keys) on randomised windows,
+    Top-K sizes, logit scales (flat to peaky), duplicated and near-duplicated keys: the indices must
+    be the oracle's exactly."""
+    g = np.random.default_rng(2024)
+    for trial in range(24):
+        d = int(g.choice([64, 128]))
+        n_l = int(g.integers(1024, 2600))
+        k = int(g.integers(1, n_l + 1)) if trial % 3 else int(g.integers(1, 40))
+        units, nqb, n_p = 1, int(g.integers(1, 6)), int(g.integers(0, 9))
+        n_slots = n_p + n_l + 2
+        scale_q = float(10.0 ** g.uniform(-2.5, 1.3))
+        qc = (g.standard_normal((units, nqb, d)) * scale_q).astype(np.float32)
+        krep = g.standard_normal((units, n_slots, d)).astype(np.float32)
+        if trial % 4 == 1:  # exact duplicates
+            krep[:, 1::5] = krep[:, 0:1]
+        if trial % 4 == 2:  # near duplicates (last-bit nudges)
+            krep[:, 1::7] = krep[:, 0:1] * (1.0 + np.float32(2.0 ** -23) * g.integers(-2, 3, size=(1, 1, d)))
+        keys = np.stack([g.permutation(n_slots)[:n_p + n_l] for _ in range(units)]).astype(np.int32)
+        sel = pb.score_select(dev(qc, torch.float32), dev(krep, torch.float32), dev(keys, torch.int32),
+                              n_p, n_l, k).cpu().numpy()
+        for u in range(units):
+            kc = krep[u][keys[u]]
+            want = orc.select_topk(orc.coarse_attention(qc[u], kc[n_p:n_p + n_l]), k)
+            assert np.array_equal(sel[u], want), f"trial {trial}: d={d} n={n_l} k={k} scale={scale_q:.3g}"
