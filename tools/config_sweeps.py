@@ -142,12 +142,21 @@ def config5(g):
     S = C + nl + bpc
     krep = torch.randn(U, S, d, device="cuda", generator=g)
     dense, local, sel = synth_tables(U, S, nd, nl, bpc, k, g)
-    ms2 = timeit(lambda: pb.score_select(qc, krep, local, 0, nl, k), reps=5, warm=1)
     dfma = U * bpc * nl * d
     byts2 = U * nl * d * 4 + U * bpc * d * 4 + U * bpc * k * 4
-    out["k2_score_select"] = {"ms": ms2, "dfma": dfma, "tdfma_per_s": dfma / ms2 / 1e9, "hbm_bytes": byts2,
-                              "gbs": byts2 / ms2 / 1e6, "note": "fp64 exact logits + row softmax: FP64-bound"}
-    print(json.dumps(out["k2_score_select"]))
+    for key, mode, note in (("k2_score_select", None, "certified fp32 ranking (default dispatch): fp32 logits "
+                             "with an error bound, exact fp64 logits only near the k-th boundary"),
+                            ("k2_score_select_exact", "0", "exact fp64 logits + row softmax on every row "
+                             "(PBSA_K2_CERT=0): FP64-bound")):
+        if mode is None:
+            os.environ.pop("PBSA_K2_CERT", None)
+        else:
+            os.environ["PBSA_K2_CERT"] = mode
+        ms2 = timeit(lambda: pb.score_select(qc, krep, local, 0, nl, k), reps=5, warm=1)
+        out[key] = {"ms": ms2, "mul_adds": dfma, "tmul_adds_per_s": dfma / ms2 / 1e9, "hbm_bytes": byts2,
+                    "gbs": byts2 / ms2 / 1e6, "note": note}
+        print(json.dumps(out[key]))
+    os.environ.pop("PBSA_K2_CERT", None)
     del krep
     torch.cuda.empty_cache()
     kp = torch.empty(U, S, 64, d, device="cuda", dtype=torch.bfloat16)
