@@ -157,6 +157,8 @@ int pbsa_attend_qkv_host(pbsa_mem* m, const void* q_host, const void* k_host, co
                          float scale, int mode, void* o_host, void* stream);
 /* Waits for every upload and download issued by pbsa_attend_qkv_host so far. */
 int pbsa_mem_host_sync(pbsa_mem* m);
+/* Number of kernels the library has launched since it was loaded (all entry points, all streams). */
+long long pbsa_launch_count(void);
 /* Chunk latents in the reference's Latent4D layout (proj/include/pbsa/tensor.hpp:30-47: (t, h, w, d)
  * row-major, d = heads * head_dim), one per batch element: [batch][T][H][W][heads*d]
  * bf16, blocked by blockify's (B_t, B_h, B_w) (proj/include/pbsa/blockify.hpp:11-67; block id

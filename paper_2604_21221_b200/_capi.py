@@ -60,6 +60,7 @@ _SIGS = {
     "pbsa_attend_qkv": (_i32, [_vp, _vp, _vp, _vp, _i32, _f32, _i32, _vp, _vp, _vp]),
     "pbsa_attend_qkv_host": (_i32, [_vp, _vp, _vp, _vp, _i32, _f32, _i32, _vp, _vp]),
     "pbsa_mem_host_sync": (_i32, [_vp]),
+    "pbsa_launch_count": (C.c_longlong, []),
     "pbsa_latent_blocks": (_i32, [C.POINTER(LatentGeom), C.POINTER(_i32), C.POINTER(_i32)]),
     "pbsa_attend_latent": (_i32, [_vp, _vp, _vp, _vp, C.POINTER(LatentGeom), _i32, _f32, _i32, _vp, _vp, _vp]),
     "pbsa_last_selection": (_i32, [_vp, C.POINTER(_vp), C.POINTER(_i32), C.POINTER(_vp),

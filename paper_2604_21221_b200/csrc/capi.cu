@@ -1,5 +1,6 @@
 // capi.cu -- the C ABI (include/pbsa_b200.h): argument checking, error reporting, TMA
 // descriptor encoding, the device-resident memory object and the per-call orchestration.
+#include <atomic>
 #include <cudaTypedefs.h>
 
 #include <cmath>
@@ -41,6 +42,11 @@ int ensure_smem(const void* kernel, size_t bytes, const char* what) {
     cur = bytes;
     return PBSA_OK;
 }
+
+namespace {
+std::atomic<long long> g_launches{0};
+}
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 int check_launch(const char* what) {
     const cudaError_t e = cudaGetLastError();
@@ -705,6 +711,8 @@ int pbsa_attend_qkv_host(pbsa_mem* m, const void* q_host, const void* k_host, co
     ++m->host_calls;
     return PBSA_OK;
 }
+
+long long pbsa_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 int pbsa_mem_host_sync(pbsa_mem* m) {
     PBSA_REQUIRE(m != nullptr, "mem_host_sync: null memory");

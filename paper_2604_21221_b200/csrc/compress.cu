@@ -273,6 +273,7 @@ int launch_compress(const bf16* x, int64_t xu, int64_t xb, const int32_t* map, i
     const int64_t warps = static_cast<int64_t>(nb) * units;
     if (warps == 0) return 0;
     const int grid = static_cast<int>((warps + 7) / 8);
+    count_launch();
     if (d == 128)
         compress_kernel<128><<<grid, 256, 0, s>>>(x, xu, xb, map, nb, units, b, reps, ru);
     else
@@ -304,6 +305,7 @@ int launch_write_chunk(const bf16* kc, const bf16* vc, const bf16* q, const int3
         return check_launch("write_chunk_bulk_kernel");
     }
     const int grid = static_cast<int>((warps + 7) / 8);
+    count_launch();
 #define PBSA_WC(DD, WQ) write_chunk_kernel<DD, WQ><<<grid, 256, 0, s>>>(kc, vc, q, stage, bpc, b, units, n_slots, kp, vp, krep, qrep)
     if (d == 128) {
         if (q) PBSA_WC(128, true); else PBSA_WC(128, false);

@@ -107,6 +107,7 @@ int launch_debug_impl(const bf16* q, const bf16* k, const bf16* v, float* s_out,
         return set_error(PBSA_ECUDA, "debug tensor map: " + err);
     const size_t smem = 1024 + (D / 64) * 32768 + 64;
     cudaFuncSetAttribute(debug_tile_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    count_launch();
     debug_tile_kernel<D><<<1, 128, smem, s>>>(tq, tk, tv, s_out, o_out);
     return check_launch("debug_tile_kernel");
 }

@@ -24,6 +24,9 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 // serialization and executes pdl_wait() (griddepcontrol.wait) before it touches data produced
 // upstream (measured effect at config 2: ~1 %, within run-to-run noise).  PBSA_PDL=0 disables it.
 bool pdl_enabled();
+// kernels launched by the library since it was loaded (pbsa_launch_count): every launch site goes
+// through launch_pdl or bumps the counter itself
+void count_launch();
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                        Args&&... args) {
@@ -37,6 +40,7 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    count_launch();
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 

@@ -191,6 +191,7 @@ __global__ void __launch_bounds__(256) mem_commit_kernel(const CommitParams p) {
 }  // namespace
 
 int launch_mem_init(const MemDev& m, int units, int C, int Lcap, int bpc, int S, cudaStream_t s) {
+    count_launch();
     mem_init_kernel<<<units, 256, 0, s>>>(m, C, Lcap, bpc, S);
     return check_launch("mem_init_kernel");
 }

@@ -176,6 +176,7 @@ int pbsa_pbt1_load_bf16(const char* path, void* dst, uint64_t capacity, void* st
             break;
         }
         const int64_t threads = (static_cast<int64_t>(cnt) + 3) / 4;
+        count_launch();
         f32_to_bf16_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, s>>>(
             dbuf, static_cast<bf16*>(dst) + off, static_cast<int64_t>(cnt));
         if (cudaGetLastError() != cudaSuccess || cudaEventRecord(done[bsel], s) != cudaSuccess) fail("convert launch failed");

@@ -535,3 +535,25 @@ def test_score_select_certified_fuzz(pb):
             kc = krep[u][keys[u]]
             want = orc.select_topk(orc.coarse_attention(qc[u], kc[n_p:n_p + n_l]), k)
             assert np.array_equal(sel[u], want), f"trial {trial}: d={d} n={n_l} k={k} scale={scale_q:.3g}"
+
+
+def test_launch_counter_per_call(pb):
+    """pbsa_launch_count: a denoise call at a short window launches ingest + K2 logits + K2 select
+    + K3 (4 kernels); a cache-update call adds the A_t aggregation and K4 (6) -- the bench reports
+    this counter's delta over its timed region as gpu_launches."""
+    from paper_2604_21221_b200._capi import LIB
+    U, C, W, bpc, b, d = 2, 12, 2, 6, 60, 128
+    mem = pb.Memory(U, C, W, bpc, b, d)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    for _ in range(W + 3):  # fill to steady state
+        q, kk, vv = (torch.randn(U, bpc * b, d, device="cuda", generator=g).bfloat16() for _ in range(3))
+        mem.attend_qkv(q, kk, vv, 3, pb.MODE_CACHE_UPDATE)
+    torch.cuda.synchronize()
+    n0 = LIB.pbsa_launch_count()
+    mem.attend_qkv(q, kk, vv, 3, pb.MODE_DENOISE)
+    n1 = LIB.pbsa_launch_count()
+    mem.attend_qkv(q, kk, vv, 3, pb.MODE_CACHE_UPDATE)
+    n2 = LIB.pbsa_launch_count()
+    torch.cuda.synchronize()
+    assert (n1 - n0, n2 - n1) == (4, 6)
+    mem.close()
