@@ -52,6 +52,10 @@ def test_argument_errors_need_no_gpu():
     rc = lib.pbsa_score_select(None, None, 0, None, 4, 4, 0, 4, 5, 1, 1, 128, 0.0, None, None,
                                None, 0, None)
     assert rc == _capi.PBSA_EINVAL and b"k exceeds" in lib.pbsa_last_error()
+    rc = lib.pbsa_attend_qkv_host(None, None, None, None, 4, 0.0, 0, None, None)
+    assert rc == _capi.PBSA_EINVAL and b"attend_qkv_host" in lib.pbsa_last_error()
+    assert lib.pbsa_mem_host_sync(None) == _capi.PBSA_EINVAL
+    assert lib.pbsa_launch_count() >= 0
 
 
 def test_product_package_does_not_import_the_oracle():
