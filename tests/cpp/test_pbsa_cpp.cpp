@@ -169,6 +169,40 @@ int main() {
         }
         EXPECT(threw);
     }
+    // host-resident chunks: attend_qkv_host (uploads / compute / downloads pipelined over two
+    // staging sets) == attend_qkv on device copies, denoise and cache-update calls
+    {
+        const int U = 2, C = 12, Wc = 2, bpc = 6, b = 60, d = 128, n = U * bpc * b * d, calls = 9;
+        pbsa::Memory mh(U, C, Wc, bpc, b, d), md(U, C, Wc, bpc, b, d);
+        std::vector<std::vector<uint16_t>> hin, hout, dref;  // inputs stay alive until host_sync
+        hin.reserve(3 * calls);
+        hout.reserve(calls);
+        dref.reserve(calls);
+        pbsa::detail::DevBuf<uint16_t> dq(n), dk(n), dv(n), dout(n);
+        for (int c = 0; c < calls; ++c) {
+            const int mode = (c % 3 == 2) ? PBSA_MODE_CACHE_UPDATE : PBSA_MODE_DENOISE;
+            for (int t = 0; t < 3; ++t) {
+                hin.emplace_back(n);
+                for (int i = 0; i < n; ++i)
+                    hin.back()[i] = pbsa::detail::to_bf16(static_cast<float>(std::sin(0.37 * i + 11.0 * c + 3.0 * t)));
+            }
+            const auto& q = hin[3 * c];
+            const auto& k = hin[3 * c + 1];
+            const auto& v = hin[3 * c + 2];
+            dq.upload(q.data(), n);
+            dk.upload(k.data(), n);
+            dv.upload(v.data(), n);
+            md.attend_qkv(dq.p, dk.p, dv.p, 3, mode, dout.p);
+            dref.emplace_back(n);
+            dout.download(dref.back().data(), n);
+            hout.emplace_back(n);
+            mh.attend_qkv_host(q.data(), k.data(), v.data(), 3, mode, hout.back().data());
+        }
+        mh.host_sync();
+        bool same = true;
+        for (int c = 0; c < calls; ++c) same &= hout[c] == dref[c];
+        EXPECT(same);
+    }
     std::printf("PASS %d\n", n_ok);
     return 0;
 }
