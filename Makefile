@@ -47,9 +47,10 @@ build/test_pbsa_cpp: tests/cpp/test_pbsa_cpp.cpp include/pbsa/pbsa_b200.hpp incl
 # K3 handshake-timeline build (tools/k3_timeline.py; perf experiments only)
 trace-lib: build/trace/libpbsa_b200.so
 
-build/trace/libpbsa_b200.so: $(PKG)/csrc/bsa_fwd.cu $(HDR) $(OBJ)
+build/trace/libpbsa_b200.so: $(PKG)/csrc/bsa_fwd.cu $(PKG)/csrc/bsa_bwd.cu $(HDR) $(OBJ)
 	@mkdir -p build/trace
-	$(NVCC) $(NVFLAGS) -DPBSA_K3_TRACE -ccbin $(HOSTCXX) -c $< -o build/trace/bsa_fwd.o 2> build/trace/ptxas.txt || (cat build/trace/ptxas.txt; false)
-	$(NVCC) $(ARCH) -ccbin $(HOSTCXX) -shared -o $@ build/trace/bsa_fwd.o $(filter-out build/obj/bsa_fwd.o,$(OBJ))
+	$(NVCC) $(NVFLAGS) -DPBSA_K3_TRACE -ccbin $(HOSTCXX) -c $(PKG)/csrc/bsa_fwd.cu -o build/trace/bsa_fwd.o 2> build/trace/ptxas.txt || (cat build/trace/ptxas.txt; false)
+	$(NVCC) $(NVFLAGS) -DPBSA_K3_TRACE -ccbin $(HOSTCXX) -c $(PKG)/csrc/bsa_bwd.cu -o build/trace/bsa_bwd.o 2>> build/trace/ptxas.txt || (cat build/trace/ptxas.txt; false)
+	$(NVCC) $(ARCH) -ccbin $(HOSTCXX) -shared -o $@ build/trace/bsa_fwd.o build/trace/bsa_bwd.o $(filter-out build/obj/bsa_fwd.o build/obj/bsa_bwd.o,$(OBJ))
 
 .PHONY: trace-lib

@@ -63,7 +63,16 @@ struct BwdParams {
     float* dv;
     int max_list, bm_words, tiles_per_unit, n_tiles;
     int dense_pairs, local_pairs, n_items;
+    long long* trace;    // handshake timeline (CTA 0), compiled in only with -DPBSA_K3_TRACE
 };
+
+__device__ __forceinline__ void bstamp(const BwdParams& p, int ev, int j) {
+#ifdef PBSA_K3_TRACE
+    if (p.trace != nullptr && blockIdx.x == 0 && j < 256) p.trace[ev * 256 + j] = clock64();
+#else
+    (void)p; (void)ev; (void)j;
+#endif
+}
 
 // ---------------------------------------------------------------------------------- prep
 __global__ void bwd_rows_kernel(const bf16* __restrict__ o, const bf16* __restrict__ d_o, const float* __restrict__ lse,
@@ -394,11 +403,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     for (int c = 0; c < 32; ++c) ov[c] = 0u;
                 }
                 if (valid) {
-                    float4* dst = reinterpret_cast<float4*>(p.dq + row * D + c0);
 #pragma unroll
-                    for (int c = 0; c < 8; ++c)
-                        dst[c] = make_float4(__uint_as_float(ov[4 * c]) * p.scale, __uint_as_float(ov[4 * c + 1]) * p.scale,
-                                             __uint_as_float(ov[4 * c + 2]) * p.scale, __uint_as_float(ov[4 * c + 3]) * p.scale);
+                    for (int c = 0; c < 4; ++c) st_global_v8_scaled(p.dq + row * D + c0 + 8 * c, ov + 8 * c, p.scale);
                 }
             }
             tc_fence_before();
@@ -587,6 +593,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             auto issue_acc = [&](int x, bool first) {
                 const int b = x & 1, sx = x % kNS;
                 mbar_wait(p_full + b, (x >> 1) & 1);
+                bstamp(p, 2, x);  // MMA: P_x seen
                 tc_fence_after();
                 const uint32_t pt = tmem + 256 + b * 128, dst = pt + 64;  // P^T, dS^T (bf16 pairs)
                 const uint64_t qd = qmn + ((sx * L::kBlk) >> 4), dd = domn + ((sx * L::kBlk) >> 4);
@@ -599,10 +606,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     mma_commit(q_empty + sx);
                 }
                 __syncwarp();
+                bstamp(p, 3, x);  // MMA: dV / dK of x issued
             };
             for (int idx = 0; idx < nf; ++idx) {
                 const int j = jg + idx, s = j % kNS, b = j & 1;
                 mbar_wait(q_full + s, (j / kNS) & 1);
+                bstamp(p, 0, j);  // MMA: Q_j / dO_j present, before S_j
                 tc_fence_after();
                 const uint32_t st = tmem + 256 + b * 128, dpt = st + 64;
                 const uint64_t qd = qdesc + ((s * L::kBlk) >> 4), dd = dodesc + ((s * L::kBlk) >> 4);
@@ -617,6 +626,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     mma_commit(s_full + b);
                 }
                 __syncwarp();
+                bstamp(p, 1, j);  // MMA: S_j, dP_j issued
                 if (idx > 0) issue_acc(j - 1, idx == 1);
             }
             if (nf > 0) issue_acc(jg + nf - 1, nf == 1);
@@ -642,7 +652,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             const bool kvalid = rr < p.b && slot >= 0;
             for (int idx = 0; idx < nf; ++idx) {
                 const int j = jg + idx, bb = j & 1, s = j % kNS;
+                if (threadIdx.x == 64) bstamp(p, 4, j);  // elementwise warp 2: waiting for S_j
                 mbar_wait(s_full + bb, (j >> 1) & 1);
+                if (threadIdx.x == 64) bstamp(p, 5, j);  // S_j seen
                 tc_fence_after();
                 const uint32_t ts = t_row + 256 + bb * 128 + ch * 32;  // this warp's 32 query columns
                 const bool vis = (list[idx] >> (24 + half)) & 1;
@@ -674,11 +686,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 tmem_wait_st();
                 tc_fence_before();
                 __syncwarp();
+                if (threadIdx.x == 64) bstamp(p, 6, j);  // P_j arrive
                 if (lane == 0) mbar_arrive(p_full + bb);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(list_empty + lb);
+            if (threadIdx.x == 64) bstamp(p, 7, f);  // fragment f: waiting for the accumulators
             mbar_wait(acc_done, f & 1);
+            if (threadIdx.x == 64) bstamp(p, 8, f);  // accumulators complete, epilogue starts
             tc_fence_after();
             // dK = scale * acc[0, D), dV = acc[128, 128 + D): this warp's column half of its rows
 #pragma unroll 1
@@ -696,16 +711,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                         for (int c = 0; c < 32; ++c) ov[c] = 0u;
                     }
                     if (kvalid) {
-                        float4* dst = reinterpret_cast<float4*>(outp + ((static_cast<int64_t>(u) * p.n_slots + slot) * 64 + rr) * D + c0);
+                        float* dst = outp + ((static_cast<int64_t>(u) * p.n_slots + slot) * 64 + rr) * D + c0;
 #pragma unroll
-                        for (int c = 0; c < 8; ++c)
-                            dst[c] = make_float4(__uint_as_float(ov[4 * c]) * mul, __uint_as_float(ov[4 * c + 1]) * mul,
-                                                 __uint_as_float(ov[4 * c + 2]) * mul, __uint_as_float(ov[4 * c + 3]) * mul);
+                        for (int c = 0; c < 4; ++c) st_global_v8_scaled(dst + 8 * c, ov + 8 * c, mul);
                     }
                 }
             }
             tc_fence_before();
             __syncwarp();
+            if (threadIdx.x == 64) bstamp(p, 9, f);  // epilogue done
             if (lane == 0) mbar_arrive(acc_free);
             jg += nf;
         }
@@ -767,6 +781,8 @@ size_t bsa_bwd_workspace(int units, int nqb, int b, int n_local) {
     return 2 * rows * 4 + static_cast<size_t>(units) * n_local * words * 4 + 256;
 }
 
+static long long* g_bwd_trace = nullptr;  // perf experiments: dK/dV handshake timeline (CTA 0)
+
 int launch_bsa_bwd(const bf16* q, const bf16* k_pool, const bf16* v_pool, int n_slots, const int32_t* dense,
                    int dense_stride, int n_dense, const int32_t* local, int local_stride, int n_local,
                    const int32_t* sel, int k, int nqb, int b, int d, int units, float scale, const bf16* o,
@@ -775,6 +791,7 @@ int launch_bsa_bwd(const bf16* q, const bf16* k_pool, const bf16* v_pool, int n_
     if (units == 0 || nqb == 0) return 0;
     if (ws_bytes < bsa_bwd_workspace(units, nqb, b, n_local)) return set_error(PBSA_EINVAL, "bsa_bwd: workspace too small");
     BwdParams p{};
+    p.trace = g_bwd_trace;
     p.units = units;
     p.nqb = nqb;
     p.b = b;
@@ -825,3 +842,5 @@ int launch_bsa_bwd(const bf16* q, const bf16* k_pool, const bf16* v_pool, int n_
 }
 
 }  // namespace pbsa
+
+extern "C" void pbsa_debug_bwd_trace_buffer(void* p) { pbsa::g_bwd_trace = static_cast<long long*>(p); }

@@ -75,6 +75,15 @@ __device__ __forceinline__ uint32_t ld_shared_u16(uint32_t addr) {
     asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr) : "memory");
     return v;
 }
+// 8 scaled fp32 values with one 256-bit store (dst 32-byte aligned): a warp of row-owning threads
+// then writes whole 32-byte sectors per instruction
+__device__ __forceinline__ void st_global_v8_scaled(float* dst, const uint32_t* v, float mul) {
+    asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst),
+                 "f"(__uint_as_float(v[0]) * mul), "f"(__uint_as_float(v[1]) * mul), "f"(__uint_as_float(v[2]) * mul),
+                 "f"(__uint_as_float(v[3]) * mul), "f"(__uint_as_float(v[4]) * mul), "f"(__uint_as_float(v[5]) * mul),
+                 "f"(__uint_as_float(v[6]) * mul), "f"(__uint_as_float(v[7]) * mul)
+                 : "memory");
+}
 __device__ __forceinline__ uint32_t ld_shared_u32(uint32_t addr) {
     uint32_t v;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
