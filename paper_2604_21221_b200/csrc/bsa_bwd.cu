@@ -458,6 +458,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < 2 + 2 * kNS + 10; ++i) mbar_init(bars + i, 1);
+        // a Q / dO / row stage is free once its MMAs completed (commit) AND the elementwise warps
+        // have read its lse2 / D rows
+        for (int s = 0; s < kNS; ++s) mbar_init(q_empty + s, 1 + kEw);
         for (int s = 0; s < 2; ++s) {
             mbar_init(p_full + s, kEw);
             mbar_init(list_empty + s, kEw + 1);
@@ -663,6 +666,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                     float sv[32], dp[32];
                     tmem_ld32(ts, *reinterpret_cast<uint32_t(*)[32]>(sv));
                     tmem_ld32(ts + 64, *reinterpret_cast<uint32_t(*)[32]>(dp));
+                    // the lse2 / D rows of stage s arrived with q_full[s] (bulk copy): acquire that
+                    // phase here too (already complete -- S_j was issued after it -- so this is
+                    // ordering, not waiting; the stage is reloaded only after q_empty[s], which
+                    // counts this warp's arrival below)
+                    mbar_wait(q_full + s, (j / kNS) & 1);
                     tmem_wait_ld();
                     const float* l2 = rows_s + s * 128 + ch * 32;
                     const float* dd = l2 + 64;
@@ -687,7 +695,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (threadIdx.x == 64) bstamp(p, 6, j);  // P_j arrive
-                if (lane == 0) mbar_arrive(p_full + bb);
+                if (lane == 0) {
+                    mbar_arrive(p_full + bb);
+                    mbar_arrive(q_empty + s);  // this warp is done with the stage's rows
+                }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(list_empty + lb);
