@@ -76,6 +76,16 @@ int pbsa_bsa_fwd(const void* q, const void* k_pool, const void* v_pool, int n_sl
                  int k, int nqb, int b, int d, int units, float scale, void* o, float* lse,
                  void* workspace, size_t workspace_bytes, void* stream);
 
+/* How the calling thread's last pbsa_bsa_fwd launch (direct or inside pbsa_attend*) was planned:
+ * visible-list entry width (2 = 16-bit entries, used for long lists over pools < 16384 slots so two
+ * CTAs still fit an SM), CTAs per SM, persistent grid, schedule and shared memory per CTA. */
+enum { PBSA_SCHED_WHOLE_TILES = 0, PBSA_SCHED_STREAM_K = 1, PBSA_SCHED_UNIT_GANGS = 2 };
+typedef struct pbsa_bsa_plan {
+    int list_entry_bytes, ctas_per_sm, grid, schedule, gangs, max_list, n_tiles;
+    size_t smem_bytes;
+} pbsa_bsa_plan;
+int pbsa_bsa_fwd_last_plan(pbsa_bsa_plan* out);
+
 /* (c') block-sparse attention backward -- the gradient of pbsa_bsa_fwd (the training path of
  * Alg. 2; the reference has no backward, the oracle is the derivative of
  * attention_sparse).  Inputs as pbsa_bsa_fwd plus the forward's o, its natural-log lse

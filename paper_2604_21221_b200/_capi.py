@@ -37,6 +37,14 @@ class LatentGeom(C.Structure):
                 ("head_dim", _i32), ("block_t", _i32), ("block_h", _i32), ("block_w", _i32)]
 
 
+class BsaPlan(C.Structure):
+    """pbsa_bsa_plan: how the last K3 launch of this thread was planned."""
+    _fields_ = [("list_entry_bytes", _i32), ("ctas_per_sm", _i32), ("grid", _i32), ("schedule", _i32),
+                ("gangs", _i32), ("max_list", _i32), ("n_tiles", _i32), ("smem_bytes", C.c_size_t)]
+
+
+SCHED_WHOLE_TILES, SCHED_STREAM_K, SCHED_UNIT_GANGS = 0, 1, 2
+
 _SIGS = {
     "pbsa_last_error": (C.c_char_p, []),
     "pbsa_version": (_i32, []),
@@ -47,6 +55,7 @@ _SIGS = {
     "pbsa_bsa_fwd_workspace": (C.c_size_t, [_i32, _i32, _i32]),
     "pbsa_bsa_fwd": (_i32, [_vp, _vp, _vp, _i32, _vp, _i32, _i32, _vp, _i32, _i32, _vp, _i32,
                             _i32, _i32, _i32, _i32, _f32, _vp, _vp, _vp, C.c_size_t, _vp]),
+    "pbsa_bsa_fwd_last_plan": (_i32, [C.POINTER(BsaPlan)]),
     "pbsa_bsa_bwd_workspace": (C.c_size_t, [_i32, _i32, _i32, _i32]),
     "pbsa_bsa_bwd": (_i32, [_vp, _vp, _vp, _i32, _vp, _i32, _i32, _vp, _i32, _i32, _vp, _i32,
                             _i32, _i32, _i32, _i32, _f32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, C.c_size_t, _vp]),

@@ -74,7 +74,14 @@ struct BsaParams {
     float* part_o;         // [kRing*grid][128][D] fp32 (null -> whole tiles only)
     float* part_ml;        // [kRing*grid][2][128]
     int* counters;         // [n_tiles], zero between launches
+    // unit-gang schedule (gangs > 0): CTA c = gang c / tiles_per_unit, member c % tiles_per_unit;
+    // gang g takes units g, g + gangs, ... one whole tile per member per unit, and the members'
+    // producers pass a barrier (gang_ctr[g]) between units so all tiles of a unit stream its pool
+    // together (the KV blocks they share are fetched from DRAM once and served from L2)
+    int gangs;
+    int* gang_ctr;         // [gangs] + done counter at [kMaxGangs], zero between launches
 };
+constexpr int kMaxGangs = 1024;
 
 struct FragMeta {
     int tile, u, qb0, has2;
@@ -123,6 +130,10 @@ __device__ __forceinline__ int64_t range_begin(int c, int64_t W, int G) { return
 
 // number of fragments this CTA processes
 __device__ __forceinline__ int num_fragments(const BsaParams& p, int c) {
+    if (p.gangs > 0) {
+        const int g = c / p.tiles_per_unit;
+        return g < p.units ? (p.units - 1 - g) / p.gangs + 1 : 0;
+    }
     if (p.part_o == nullptr) return c < p.n_tiles ? (p.n_tiles - 1 - c) / p.grid + 1 : 0;
     if (c >= p.tail_grid || p.vtotal == 0) return p.whole_waves;
     const int64_t a = range_begin(c, p.vtotal, p.tail_grid), b = range_begin(c + 1, p.vtotal, p.tail_grid);
@@ -237,8 +248,18 @@ __global__ void __launch_bounds__(kThreads, 2)
                 mbar_wait(list_empty + lb, ((f >> 1) & 1) ^ 1);
                 uint8_t* list = lists + static_cast<size_t>(lb) * p.max_list * esz;
                 // ---------------------------------------------------------- fragment schedule
-                const bool tail_frag = p.part_o != nullptr && f >= p.whole_waves;
-                const int tile = tail_frag ? my_first_tile + (f - p.whole_waves) : cta + f * p.grid;
+                const bool tail_frag = p.gangs == 0 && p.part_o != nullptr && f >= p.whole_waves;
+                int tile = tail_frag ? my_first_tile + (f - p.whole_waves) : cta + f * p.grid;
+                if (p.gangs > 0) {
+                    const int g = cta / p.tiles_per_unit;
+                    tile = (g + f * p.gangs) * p.tiles_per_unit + cta % p.tiles_per_unit;
+                    // every member of the gang has issued all loads of the previous unit
+                    if (f > 0 && lane == 0) {
+                        const int want = f * p.tiles_per_unit;
+                        while (ld_acquire_gpu(p.gang_ctr + g) < want) __nanosleep(64);
+                    }
+                    __syncwarp();
+                }
                 const int u = tile / p.tiles_per_unit;
                 const int qb0 = 2 * (tile % p.tiles_per_unit);
                 const bool has2 = qb0 + 1 < p.nqb;
@@ -367,6 +388,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                     load_v(nf - 1);
                     jg += nf;
                 }
+                if (p.gangs > 0 && lane == 0) red_release_gpu_add(p.gang_ctr + cta / p.tiles_per_unit, 1);
             }
         }
     } else if (warp == 1) {
@@ -724,6 +746,16 @@ __global__ void __launch_bounds__(kThreads, 2)
         tc_fence_after();
         tmem_dealloc<kTmemCols>(tmem);
     }
+    if (p.gangs > 0 && threadIdx.x == 0) {
+        // the last CTA out re-zeroes the gang counters for the next launch (every producer has
+        // passed its last barrier: a CTA only exits after its producer finished all units)
+        __threadfence();
+        if (atomicAdd(p.gang_ctr + kMaxGangs, 1) == static_cast<int>(gridDim.x) - 1) {
+            for (int g = 0; g < p.gangs; ++g) p.gang_ctr[g] = 0;
+            p.gang_ctr[kMaxGangs] = 0;
+            __threadfence();
+        }
+    }
 }
 
 int num_sms() {
@@ -783,6 +815,22 @@ int launch_impl(const bf16* q, const bf16* kp, const bf16* vp, BsaParams p, cuda
     p.tail_base = 0;
     p.tail_grid = 0;
     p.vtotal = 0;
+    p.gangs = 0;
+    if (p.gang_ctr != nullptr) {
+        // unit-gang schedule: many whole-tile waves over a slot pool far larger than L2 (config 5:
+        // 12480 tiles, 65 GB) -- tiles of one unit run together so the blocks they share come from
+        // DRAM once.  PBSA_K3_GANG=0/1 forces it off / on (experiments, tests).
+        const char* env = getenv("PBSA_K3_GANG");
+        const int force = env ? atoi(env) : -1;
+        const int gangs = slots / p.tiles_per_unit;
+        const double pool = static_cast<double>(p.units) * p.n_slots * 64 * D * 2 * 2;
+        const bool want = force >= 0 ? force > 0 : (p.n_tiles >= 4 * slots && pool > 4.0 * 126e6);
+        if (want && gangs >= 1 && gangs <= kMaxGangs) {
+            p.gangs = gangs < p.units ? gangs : p.units;
+            p.grid = p.gangs * p.tiles_per_unit;
+            p.part_o = nullptr;
+        }
+    }
     if (p.part_o != nullptr) {
         p.grid = slots;
         p.whole_waves = p.n_tiles / slots;
@@ -796,6 +844,17 @@ int launch_impl(const bf16* q, const bf16* kp, const bf16* vp, BsaParams p, cuda
         p.tail_grid = static_cast<int>(g);
         if (p.whole_waves == 0) p.grid = p.tail_grid;
     }
+    {
+        pbsa_bsa_plan& pl = last_bsa_plan();
+        pl.list_entry_bytes = L16 ? 2 : 4;
+        pl.ctas_per_sm = per_sm;
+        pl.grid = p.grid > 0 ? p.grid : 0;
+        pl.schedule = p.gangs > 0 ? PBSA_SCHED_UNIT_GANGS : (p.part_o != nullptr ? PBSA_SCHED_STREAM_K : PBSA_SCHED_WHOLE_TILES);
+        pl.gangs = p.gangs;
+        pl.max_list = p.max_list;
+        pl.n_tiles = p.n_tiles;
+        pl.smem_bytes = smem;
+    }
     if (p.grid <= 0) return 0;
     if (launch_pdl(bsa_fwd_kernel<D, NSK, NSV, B, POLY, L16>, dim3(p.grid), dim3(kThreads), smem, s, tq, tk, tv, p) !=
         cudaSuccess)
@@ -805,10 +864,15 @@ int launch_impl(const bf16* q, const bf16* kp, const bf16* vp, BsaParams p, cuda
 
 }  // namespace
 
+pbsa_bsa_plan& last_bsa_plan() {
+    static thread_local pbsa_bsa_plan plan{};
+    return plan;
+}
+
 size_t bsa_fwd_workspace(int units, int nqb, int d) {
     const size_t slots = kRing * static_cast<size_t>(2 * num_sms());
     const size_t tiles = static_cast<size_t>(units) * ((nqb + 1) / 2);
-    return slots * 128 * d * 4 + slots * 256 * 4 + tiles * 4 + 256;
+    return slots * 128 * d * 4 + slots * 256 * 4 + tiles * 4 + (kMaxGangs + 1) * 4 + 256;
 }
 
 static long long* g_trace = nullptr;
@@ -860,6 +924,7 @@ int launch_bsa_fwd(const bf16* q, const bf16* k_pool, const bf16* v_pool, int n_
         p.part_o = static_cast<float*>(ws);
         p.part_ml = p.part_o + slots * 128 * d;
         p.counters = reinterpret_cast<int*>(p.part_ml + slots * 256);
+        p.gang_ctr = p.counters + p.n_tiles;
     }
     // 16-bit visible-list entries only where 32-bit lists would cost the second CTA per SM (long
     // lists, e.g. config 5) and the pool is small enough to index with 14 bits

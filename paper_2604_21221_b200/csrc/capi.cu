@@ -284,6 +284,12 @@ int pbsa_score_select(const float* qc, const float* krep, int64_t krep_unit_stri
                                as_stream(stream));
 }
 
+int pbsa_bsa_fwd_last_plan(pbsa_bsa_plan* out) {
+    PBSA_REQUIRE(out != nullptr, "bsa_fwd_last_plan: null output");
+    *out = last_bsa_plan();
+    return PBSA_OK;
+}
+
 size_t pbsa_bsa_fwd_workspace(int units, int nqb, int d) {
     if (units < 0 || nqb < 0 || (d != 64 && d != 128)) return 0;
     return bsa_fwd_workspace(units, nqb, d);

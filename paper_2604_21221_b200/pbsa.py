@@ -23,7 +23,7 @@ from . import _capi
 from ._capi import LIB, PbsaCudaError, PbsaError, check  # noqa: F401
 
 __all__ = ["compress_blocks", "score_select", "attention_sparse", "Memory", "attention_scale",
-           "topk_count", "PbsaError", "PbsaCudaError", "debug_tile", "MODE_DENOISE",
+           "topk_count", "bsa_fwd_last_plan", "PbsaError", "PbsaCudaError", "debug_tile", "MODE_DENOISE",
            "MODE_CACHE_UPDATE"]
 
 MODE_DENOISE = _capi.MODE_DENOISE
@@ -145,12 +145,22 @@ def attention_sparse(q: torch.Tensor, k_pool: torch.Tensor, v_pool: torch.Tensor
     return (o, lse) if want_lse else o
 
 
+def bsa_fwd_last_plan() -> "_capi.BsaPlan":
+    """How this thread's last K3 launch was planned (list entry width, CTAs per SM, grid, schedule
+    0 whole tiles / 1 hybrid stream-K / 2 unit gangs) -- pbsa_bsa_fwd_last_plan."""
+    plan = _capi.BsaPlan()
+    check(LIB.pbsa_bsa_fwd_last_plan(C.byref(plan)))
+    return plan
+
+
 _WS: dict = {}
 
 
 def _workspace(nbytes: int, device) -> torch.Tensor:
-    """Zero-initialised K3 workspace, cached per device (the kernel leaves it zeroed)."""
-    key = str(device)
+    """Zero-initialised K3 workspace, cached per (device, stream): the stream-K merge counters and
+    partial slots in it are only safe for launches ordered on one stream, and a replaced (smaller)
+    buffer goes back to the caching allocator in that stream's order (the kernel leaves it zeroed)."""
+    key = (str(device), torch.cuda.current_stream(device).cuda_stream)
     t = _WS.get(key)
     if t is None or t.numel() < nbytes:
         t = torch.zeros(max(nbytes, 1), dtype=torch.uint8, device=device)

@@ -251,6 +251,37 @@ def test_bsa_fwd_wide_pool_32bit_lists(pb):
     _bsa_case(pb, 1, 4, 60, 128, 10, 16390, 8, seed=23)
 
 
+def test_bsa_fwd_16bit_lists_config5_lengths(pb):
+    """Config-5 list lengths (234 dense + the union of two 1502-of-6006 selections = ~2860-entry
+    lists) over a pool < 16384 slots: K3 takes the 16-bit visible-list variant (two CTAs per SM)."""
+    _bsa_case(pb, 1, 6, 60, 128, 234, 6006, 1502, seed=24)
+    plan = pb.bsa_fwd_last_plan()
+    assert plan.list_entry_bytes == 2 and plan.ctas_per_sm == 2, (plan.list_entry_bytes, plan.ctas_per_sm)
+    _bsa_case(pb, 2, 3, 64, 64, 100, 3000, 3000, seed=25, stream_k=False)  # k = n_local: list = all
+    plan = pb.bsa_fwd_last_plan()
+    assert plan.list_entry_bytes == 2, plan.list_entry_bytes
+
+
+def test_bsa_fwd_32bit_lists_selected(pb):
+    """The same long lists over >= 16384 slots keep 32-bit entries (and a short list never uses 16)."""
+    _bsa_case(pb, 1, 2, 60, 128, 234, 16200, 1502, seed=26)
+    assert pb.bsa_fwd_last_plan().list_entry_bytes == 4
+    _bsa_case(pb, 1, 4, 60, 128, 10, 30, 8, seed=27)
+    assert pb.bsa_fwd_last_plan().list_entry_bytes == 4
+
+
+@pytest.mark.parametrize("units,nqb", [(40, 17), (7, 78), (3, 5)])
+def test_bsa_fwd_unit_gang_schedule(pb, monkeypatch, units, nqb):
+    """Unit-gang schedule (PBSA_K3_GANG=1; the default for config-5-sized launches): gangs of
+    tiles_per_unit CTAs walk units in lockstep behind an inter-CTA barrier.  Several rounds per
+    gang, a partial last round, and back-to-back launches (the counters must re-zero)."""
+    monkeypatch.setenv("PBSA_K3_GANG", "1")
+    for rep in range(2):
+        _bsa_case(pb, units, nqb, 60, 128, 7, 40, 9, seed=70 + units + rep)
+        plan = pb.bsa_fwd_last_plan()
+        assert plan.schedule == 2 and plan.gangs >= 1, (plan.schedule, plan.gangs)
+
+
 def test_bsa_fwd_hybrid_two_waves_and_tail(pb):
     """Two full waves of whole tiles (2 x 296 CTA slots on a B200) then a stream-K tail."""
     _bsa_case(pb, 70, 17, 60, 128, 5, 12, 3, seed=22)
@@ -272,12 +303,17 @@ def test_bsa_fwd_long_list(pb):
 
 
 # ------------------------------------------------------------------ (d) memory + full calls
-def run_rollout(pb, units, d, b, bpc, C, W, n_chunks, k_top, seed, denoise_steps=1, check_qb=None):
-    """Alg. 1 over n_chunks chunks, every PBSA call checked against the oracle."""
+def run_rollout(pb, units, d, b, bpc, C, W, n_chunks, k_top, seed, denoise_steps=1, check_qb=None,
+                attn_from_chunk=0, expect_plan=None):
+    """Alg. 1 over n_chunks chunks, every PBSA call checked against the oracle: Top-K indices, s_t
+    and P / L ids bit-exact on every call; attention (sampled query blocks `check_qb`, from chunk
+    `attn_from_chunk` on) within the bf16 tolerance.  expect_plan: dict of pbsa_bsa_plan fields the
+    K3 launch of every checked call must have (e.g. {"list_entry_bytes": 2})."""
     mem = pb.Memory(units, C, W, bpc, b, d)
     oms = [orc.Memory(C, W) for _ in range(units)]
-    kst, vst = {}, {}  # (u, id) -> [b, d] f32 of committed blocks
+    kst, vst, rep = {}, {}, {}  # (u, id) -> [b, d] f32 K / V and [d] representative of committed blocks
     stats = []
+    empty = np.zeros((0, b, d), np.float32)
     for c in range(n_chunks):
         ids = np.arange(c * bpc, (c + 1) * bpc, dtype=np.int64)
         for step in range(denoise_steps + 1):
@@ -292,14 +328,18 @@ def run_rollout(pb, units, d, b, bpc, C, W, n_chunks, k_top, seed, denoise_steps
             else:
                 mem.write_chunk(dev(kc), dev(vc))
                 o = mem.attend(dev(q), k_top, mode)
+            check_attn = c >= attn_from_chunk
+            if check_attn and expect_plan:
+                plan = pb.bsa_fwd_last_plan()
+                for key, want in expect_plan.items():
+                    assert getattr(plan, key) == want, f"K3 plan {key} = {getattr(plan, key)}, expected {want}"
             sel_gpu, st_gpu = mem.last_selection()
             o = o.float().cpu().numpy()
             sel_gpu = None if sel_gpu is None else sel_gpu.cpu().numpy()
             st_gpu = None if st_gpu is None else st_gpu.cpu().numpy()
             for u in range(units):
-                p_ids, _, n_p, n_l = oms[u].assemble()
-                l_ids = p_ids[n_p:]
-                p_ids = p_ids[:n_p]
+                a_ids, _, n_p, n_l = oms[u].assemble()
+                p_ids, l_ids = a_ids[:n_p], a_ids[n_p:]
                 qb = q[u].reshape(bpc, b, d)
                 cur_k = kc[u].reshape(bpc, b, d)
                 cur_v = vc[u].reshape(bpc, b, d)
@@ -307,36 +347,40 @@ def run_rollout(pb, units, d, b, bpc, C, W, n_chunks, k_top, seed, denoise_steps
                 k = min(k_top, n_l)
                 sel = np.zeros((bpc, 0), np.int32)
                 if k > 0:
-                    kc_l = orc.compress_blocks(np.stack([kst[(u, i)] for i in l_ids]))
+                    kc_l = np.stack([rep[(u, i)] for i in l_ids])
                     sel = orc.select_topk(orc.coarse_attention(qc, kc_l), k)
                     assert np.array_equal(sel_gpu[u], sel), f"chunk {c} step {step} unit {u}: Top-K"
-                store_k = np.concatenate([np.stack([kst[(u, i)] for i in p_ids]) if n_p else
-                                          np.zeros((0, b, d), np.float32), cur_k,
-                                          np.stack([kst[(u, i)] for i in l_ids]) if n_l else
-                                          np.zeros((0, b, d), np.float32)])
-                store_v = np.concatenate([np.stack([vst[(u, i)] for i in p_ids]) if n_p else
-                                          np.zeros((0, b, d), np.float32), cur_v,
-                                          np.stack([vst[(u, i)] for i in l_ids]) if n_l else
-                                          np.zeros((0, b, d), np.float32)])
-                dense = np.arange(n_p + bpc)
-                vis = np.stack([np.concatenate([dense, n_p + bpc + sel[i]]) for i in range(bpc)]).astype(np.int32)
-                qmask = None
-                if check_qb is not None:
-                    qmask = np.zeros(bpc, np.uint8)
-                    qmask[check_qb] = 1
-                want = orc.attention_sparse(qb, store_k, store_v, vis, qmask=qmask)
-                rows = slice(None) if check_qb is None else check_qb
-                stats.append(check_attention(o[u].reshape(bpc, b, d)[rows], want[rows]))
+                if check_attn:
+                    store_k = np.concatenate([np.stack([kst[(u, i)] for i in p_ids]) if n_p else empty, cur_k,
+                                              np.stack([kst[(u, i)] for i in l_ids]) if n_l else empty])
+                    store_v = np.concatenate([np.stack([vst[(u, i)] for i in p_ids]) if n_p else empty, cur_v,
+                                              np.stack([vst[(u, i)] for i in l_ids]) if n_l else empty])
+                    dense = np.arange(n_p + bpc)
+                    vis = np.stack([np.concatenate([dense, n_p + bpc + sel[i]]) for i in range(bpc)]).astype(np.int32)
+                    qmask = None
+                    if check_qb is not None:
+                        qmask = np.zeros(bpc, np.uint8)
+                        qmask[check_qb] = 1
+                    want = orc.attention_sparse(qb, store_k, store_v, vis, qmask=qmask)
+                    rows = slice(None) if check_qb is None else check_qb
+                    stats.append(check_attention(o[u].reshape(bpc, b, d)[rows], want[rows]))
                 if update:
-                    keys_k = np.concatenate([store_k[:n_p], store_k[n_p + bpc:], cur_k])
+                    cur_rep = orc.compress_blocks(cur_k)
+                    keys_rep = np.concatenate([np.stack([rep[(u, i)] for i in p_ids]) if n_p else np.zeros((0, d), np.float32),
+                                               np.stack([rep[(u, i)] for i in l_ids]) if n_l else np.zeros((0, d), np.float32),
+                                               cur_rep])
                     key_ids = np.concatenate([p_ids, l_ids, ids])
-                    s_ref = orc.aggregate_scores(orc.coarse_attention(qc, orc.compress_blocks(keys_k)))
+                    s_ref = orc.aggregate_scores(orc.coarse_attention(qc, keys_rep))
                     assert np.array_equal(bits(st_gpu[u][:len(key_ids)]), bits(s_ref)), f"chunk {c} unit {u}: s_t"
                     ev = oms[u].push_chunk(ids)
                     oms[u].update_persistent(ev, key_ids, s_ref)
                     for i in range(bpc):
                         kst[(u, ids[i])] = cur_k[i]
                         vst[(u, ids[i])] = cur_v[i]
+                        rep[(u, ids[i])] = cur_rep[i]
+                    keep = set(oms[u].assemble()[0].tolist())
+                    for key in [key for key in kst if key[0] == u and key[1] not in keep]:
+                        del kst[key], vst[key], rep[key]
         # after the k=0 pass: P and L block ids bit-exact (SPEC.md:209-217 order)
         gp, gl = mem.assemble()
         gp, gl = gp.cpu().numpy(), gl.cpu().numpy()
@@ -368,6 +412,18 @@ def test_rollout_config2_full_size(pb):
     query blocks."""
     run_rollout(pb, units=12, d=128, b=60, bpc=78, C=156, W=4, n_chunks=7, k_top=78, seed=2,
                 denoise_steps=0, check_qb=np.array([0, 1, 40, 77]))
+
+
+def test_rollout_config5_window_steady_state(pb):
+    """Config-5 geometry per unit (BASELINE.json config 5: 240-frame cache = P 6 + L 231 + current 3
+    frames of 26 blocks, k = 25 % of the window = 1502) on 2 units, brought to steady state (81
+    chunks: the 6006-block window full, P full of sinks + dynamic blocks, evictions every chunk).
+    Every call: Top-K indices (exact long-window K2 on the k=0 pass, certified K2 on the denoise
+    pass), s_t over all 6396 keys and P / L ids bit-exact; over the last chunks K3 runs with 16-bit
+    visible-list entries (3238-entry lists) and its output is checked on sampled query blocks."""
+    run_rollout(pb, units=2, d=128, b=60, bpc=78, C=156, W=77, n_chunks=81, k_top=1502, seed=55,
+                denoise_steps=1, check_qb=np.array([0, 1, 77]), attn_from_chunk=79,
+                expect_plan={"list_entry_bytes": 2, "ctas_per_sm": 2})
 
 
 def test_errors_are_loud(pb):

@@ -10,13 +10,15 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2604_21221_b200 as pb  # noqa: E402
 from tools.config_sweeps import synth_tables  # noqa: E402
 
-U, d, b, bpc, C, Lw = 320, 128, 60, 78, 156, 77
+U, d, b, bpc, C, Lw = int(os.environ.get("UNITS", "320")), 128, 60, 78, 156, 77
 nl, nd = Lw * bpc, C + bpc
 k = pb.topk_count(nl, 0.25)
 S = C + nl + bpc
 g = torch.Generator(device="cuda").manual_seed(0)
 q = torch.randn(U, bpc * b, d, device="cuda", generator=g).bfloat16()
 dense, local, sel = synth_tables(U, S, nd, nl, bpc, k, g)
+if os.environ.get("SAMESEL"):  # experiment: both query blocks of a tile share one selection (no union)
+    sel[:, 1::2] = sel[:, 0::2]
 kp = torch.empty(U, S, 64, d, device="cuda", dtype=torch.bfloat16)
 kp.normal_(generator=g)
 kp[:, :, b:] = 0
