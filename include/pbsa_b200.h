@@ -216,12 +216,6 @@ int pbsa_pbt1_load_bf16(const char* path, void* dst, uint64_t capacity, void* st
 /* cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault) on `stream` (state export for tests) */
 int pbsa_copy(void* dst, const void* src, size_t bytes, void* stream);
 
-/* debug: one 128-row query tile against one 64-row KV slot through the tcgen05 path.
- * q [128][d], k/v [64][d] bf16 (device); s_out [128][64] f32 = q k^T; o_out [128][d] f32 =
- * bf16(s_out) v.  Validates descriptors / TMEM layouts. */
-int pbsa_debug_tile(const void* q, const void* k, const void* v, int d, float* s_out,
-                    float* o_out, void* stream);
-
 #ifdef __cplusplus
 }
 #endif

@@ -82,10 +82,18 @@ _SIGS = {
     "pbsa_pbt1_info": (_i32, [C.c_char_p, C.POINTER(_i32), C.POINTER(C.c_uint64), _i32]),
     "pbsa_pbt1_read": (_i32, [C.c_char_p, _vp, C.c_uint64]),
     "pbsa_pbt1_load_bf16": (_i32, [C.c_char_p, _vp, C.c_uint64, _vp]),
+}
+
+# test / experiment hooks (include/pbsa_b200_debug.h) -- not part of the drop-in boundary
+_DEBUG_SIGS = {
     "pbsa_debug_tile": (_i32, [_vp, _vp, _vp, _i32, _vp, _vp, _vp]),
+    "pbsa_debug_set_fault": (_i32, [C.c_char_p]),
+    "pbsa_debug_trace_buffer": (None, [_vp]),
+    "pbsa_debug_bwd_trace_buffer": (None, [_vp]),
 }
 
 EXPORTED = sorted(_SIGS)
+DEBUG_EXPORTED = sorted(_DEBUG_SIGS)
 
 
 def load(path: str = LIB_PATH) -> C.CDLL:
@@ -94,7 +102,7 @@ def load(path: str = LIB_PATH) -> C.CDLL:
             f"{path} is missing: build the CUDA library first (`make` or "
             f"`python -c 'import __graft_entry__ as g; g.build()'`). There is no CPU fallback.")
     lib = C.CDLL(path)
-    for name, (res, args) in _SIGS.items():
+    for name, (res, args) in list(_SIGS.items()) + list(_DEBUG_SIGS.items()):
         if path != os.path.join(HERE, "_lib", "libpbsa_b200.so") and not hasattr(lib, name):
             continue  # an older experiment build (PBSA_LIB_PATH) may predate some entry points
         fn = getattr(lib, name)

@@ -357,6 +357,18 @@ int pbsa_copy(void* dst, const void* src, size_t bytes, void* stream) {
     return PBSA_OK;
 }
 
+int pbsa_debug_set_fault(const char* name) {
+    if (name == nullptr || name[0] == '\0') {
+        g_fault.store(0);
+        return PBSA_OK;
+    }
+    if (std::string(name) == "drop-sink") {
+        g_fault.store(kFaultDropSink);
+        return PBSA_OK;
+    }
+    return set_error(PBSA_EINVAL, std::string("debug_set_fault: unknown fault '") + name + "'");
+}
+
 int pbsa_debug_tile(const void* q, const void* k, const void* v, int d, float* s_out, float* o_out,
                     void* stream) {
     if (int rc = check_d(d)) return rc;

@@ -7,7 +7,10 @@
 #include <string>
 #include <utility>
 
+#include <atomic>
+
 #include "../../include/pbsa_b200.h"
+#include "../../include/pbsa_b200_debug.h"
 
 namespace pbsa {
 
@@ -88,6 +91,9 @@ int launch_bsa_fwd(const bf16* q, const bf16* k_pool, const bf16* v_pool, int n_
                    const LatentGeom* lat = nullptr);
 size_t bsa_fwd_workspace(int units, int nqb, int d);
 pbsa_bsa_plan& last_bsa_plan();  // the calling thread's last K3 launch plan
+// injected fault (pbsa_debug_set_fault; negative controls only)
+constexpr int kFaultDropSink = 1;
+extern std::atomic<int> g_fault;
 // K3 backward: dq [units][n_q][d], dk / dv [units][n_slots][64][d] f32 (rows of visible slots written)
 size_t bsa_bwd_workspace(int units, int nqb, int b, int n_local);
 int launch_bsa_bwd(const bf16* q, const bf16* k_pool, const bf16* v_pool, int n_slots, const int32_t* dense,

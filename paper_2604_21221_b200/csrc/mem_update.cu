@@ -25,6 +25,7 @@ struct CommitParams {
     const float* s_t;
     int C, Lcap, bpc, S;
     MemCounts cur, next;
+    int fault;  // kFaultDropSink: sinks compete with the dynamic candidates (negative control)
 };
 
 __device__ __forceinline__ float nan_low(float x) { return x != x ? -INFINITY : x; }
@@ -100,6 +101,19 @@ __global__ void __launch_bounds__(256) mem_commit_kernel(const CommitParams p) {
     const int dyn_lo = sink_chunk ? n_p + bpc : n_s;  // first competing candidate
     // with sink_chunk, the dynamic set is empty (nothing was evicted before the first chunk)
     const int dyn_cap = C - n_sinks_new;
+    if (p.fault == kFaultDropSink && !sink_chunk) {
+        // injected fault: every candidate, sinks included, competes for all C slots -- the
+        // kept count (and so the slot accounting) is unchanged, only sink retention is broken
+        for (int i = tid; i < n_cand; i += nt) {
+            const float si = nan_low(c_score[i]);
+            int rank = 0;
+            for (int j = 0; j < n_cand; ++j) {
+                const float sj = nan_low(c_score[j]);
+                rank += (sj > si) || (sj == si && c_id[j] < c_id[i]);
+            }
+            c_keep[i] = rank < C;
+        }
+    } else
     for (int i = tid; i < n_cand; i += nt) {
         int keep = 1;
         if (i >= n_s && !(sink_chunk && i >= n_p)) {
@@ -190,6 +204,8 @@ __global__ void __launch_bounds__(256) mem_commit_kernel(const CommitParams p) {
 
 }  // namespace
 
+std::atomic<int> g_fault{0};
+
 int launch_mem_init(const MemDev& m, int units, int C, int Lcap, int bpc, int S, cudaStream_t s) {
     count_launch();
     mem_init_kernel<<<units, 256, 0, s>>>(m, C, Lcap, bpc, S);
@@ -198,7 +214,7 @@ int launch_mem_init(const MemDev& m, int units, int C, int Lcap, int bpc, int S,
 
 int launch_mem_commit(const MemDev& m, const float* s_t, int units, int C, int Lcap, int bpc, int S,
                       const MemCounts& cur, const MemCounts& next, cudaStream_t s) {
-    CommitParams p{m, s_t, C, Lcap, bpc, S, cur, next};
+    CommitParams p{m, s_t, C, Lcap, bpc, S, cur, next, g_fault.load()};
     const int max_cand = C + bpc;
     const size_t smem = static_cast<size_t>(max_cand) * (8 + 4 + 4 + 4) + static_cast<size_t>(Lcap) * 12 +
                         static_cast<size_t>(bpc) * 4 + static_cast<size_t>(S) * 4 + static_cast<size_t>(C) * 16 + 64;

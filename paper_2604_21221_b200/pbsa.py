@@ -200,6 +200,12 @@ def attention_sparse_backward(q: torch.Tensor, k_pool: torch.Tensor, v_pool: tor
     return dq, dk, dv
 
 
+def debug_set_fault(name: str | None) -> None:
+    """Test-only fault injection (pbsa_debug_set_fault): "drop-sink" breaks K4's sink retention
+    (the negative control of SPEC.md:625); None clears it."""
+    check(LIB.pbsa_debug_set_fault(None if not name else name.encode()))
+
+
 def debug_tile(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor):
     """One 128x64 tile through the tcgen05 path: returns (q k^T f32, bf16(q k^T) v f32)."""
     d = q.shape[1]

@@ -32,7 +32,7 @@ class RolloutConfig:
     timesteps: tuple = (1.0, 0.75, 0.5, 0.25)  # t_T .. t_1, strictly decreasing
     topk_ratio: float = 0.25
     capacity_frames: int = 6                 # C
-    window_frames: int = 12                  # L_local (frames; whole chunks)
+    window_frames: int = 6                   # L_local (frames; whole chunks; SPEC.md:493 default)
     chunk_frames: int = 3
     height: int = 30
     width: int = 52
@@ -157,9 +157,23 @@ class ToyDenoiser:
 # ---------------------------------------------------------------- Alg. 1
 
 
+def _per_head(x: torch.Tensor, cfg: RolloutConfig) -> torch.Tensor:
+    """Chunk tokens of one layer call -> [heads, bpc*b, head_dim] f32 in block-major token order (the
+    per-unit layout of the C ABI), from a (t, h, w, d) latent or an already block-major tensor."""
+    if cfg.latent:
+        x = blockify_tokens(x.reshape(cfg.chunk_frames, cfg.height, cfg.width, cfg.d_model), cfg.block_shape)
+        return x.reshape(-1, cfg.heads, cfg.head_dim).transpose(0, 1).float().cpu()
+    return x.float().cpu()
+
+
 def run_inference(cfg: RolloutConfig, denoiser: ToyDenoiser | None = None, trace_path: str | None = None,
-                  device="cuda", record_scores: bool = True):
-    """Returns (frames [list of (t,h,w,d) bf16 chunks], trace [list of dicts], timing dict)."""
+                  device="cuda", record_scores: bool = True, capture: list | None = None):
+    """Returns (frames [list of (t,h,w,d) bf16 chunks], trace [list of dicts], timing dict).
+
+    capture (a list): every layer-0 PBSA call appends {"mode", "k_top", "q", "k", "v", "o" (all
+    [heads, bpc*b, head_dim] f32, block-major), "sel" [heads, bpc, k] (or None), "s_t" [heads,
+    n_keys] (k=0 pass), "persistent" / "window" (ids after the call)} -- the record an oracle replay
+    (SPEC.md:487) consumes."""
     cfg.validate()
     den = denoiser or ToyDenoiser(cfg, device)
     bpc, b, U = cfg.blocks_per_chunk, cfg.b, cfg.heads
@@ -195,6 +209,14 @@ def run_inference(cfg: RolloutConfig, denoiser: ToyDenoiser | None = None, trace
                 if scores_rec is not None and layer == 0 and mode == pbsa.MODE_CACHE_UPDATE:
                     _, s_t = mem.last_selection()
                     scores_rec["scores"] = [[float(v_) for v_ in s_t[u].tolist()] for u in range(cfg.trace_units)]
+                if capture is not None and layer == 0:
+                    sel, s_t = mem.last_selection()
+                    p_ids, l_ids = mem.assemble()
+                    capture.append({"mode": mode, "k_top": k_top, "q": _per_head(q, cfg), "k": _per_head(k, cfg),
+                                    "v": _per_head(v, cfg), "o": _per_head(o, cfg),
+                                    "sel": None if sel is None else sel.cpu(),
+                                    "s_t": s_t.cpu() if mode == pbsa.MODE_CACHE_UPDATE and s_t is not None else None,
+                                    "persistent": p_ids.cpu(), "window": l_ids.cpu()})
                 calls += 1
             return h.view(dims) if cfg.latent else unblockify_tokens(h, dims, cfg.block_shape)
 
@@ -202,13 +224,15 @@ def run_inference(cfg: RolloutConfig, denoiser: ToyDenoiser | None = None, trace
             j = len(cfg.timesteps) - jj  # j = T .. 1
             x0_hat = layer_stack(x, t, pbsa.MODE_DENOISE)
             rec = {"chunk": i, "j": j, "t": t, "cache_updated": j == 1, "grad_enabled": False}
+            # every record carries the layer-0 memory it attended over
+            p_ids, l_ids = _ids(mems[0], cfg.trace_units)
+            rec["persistent"], rec["window"], rec["evicted"] = p_ids, l_ids, [[] for _ in range(cfg.trace_units)]
             if j == 1:
                 frames.append(x0_hat)
                 # k = 0 pass on the clean chunk: scores, push/evict, Top-C (Alg. 1 lines 9-10)
-                before = [_ids(m, cfg.trace_units) for m in mems[:1]]
                 layer_stack(x0_hat, 0.0, pbsa.MODE_CACHE_UPDATE, rec if record_scores else None)
+                prev_l = l_ids
                 p_ids, l_ids = _ids(mems[0], cfg.trace_units)
-                prev_l = before[0][1]
                 rec["evicted"] = [sorted(set(prev_l[u]) - set(l_ids[u])) for u in range(cfg.trace_units)]
                 rec["persistent"] = p_ids
                 rec["window"] = l_ids
@@ -237,25 +261,35 @@ def _ids(mem: pbsa.Memory, n_units: int):
 
 
 def check_trace(cfg: RolloutConfig, trace) -> None:
-    """SPEC.md:484-488 / acceptance 6: cache updates exactly once per chunk at j=1, |P| <= C,
-    |window| <= L_local, evicted ids strictly increasing, P and L disjoint."""
+    """SPEC.md:484-488 / acceptance 6: cache updates exactly once per chunk at j=1, |P| <= C and
+    |window| <= L_local at every record, P and L disjoint, evicted ids strictly increasing, and the
+    sinks (blocks of the first chunk) retained once they entered P -- for every traced
+    unit."""
     updates = [r for r in trace if r["cache_updated"]]
     if len(updates) != cfg.num_chunks or any(r["j"] != 1 for r in updates):
         raise AssertionError("cache updates must happen exactly once per chunk, at j = 1")
     if len(trace) != cfg.num_chunks * len(cfg.timesteps):
         raise AssertionError("one trace record per (chunk, denoise step)")
-    last = -1
-    for r in updates:
-        for u, (p, l_) in enumerate(zip(r["persistent"], r["window"])):
+    n_units = len(trace[0]["persistent"]) if trace else 0
+    for r in trace:
+        for p, l_ in zip(r["persistent"], r["window"]):
             if len(p) > cfg.capacity_blocks or len(l_) > cfg.window_chunks * cfg.blocks_per_chunk:
                 raise AssertionError("capacity exceeded")
             if set(p) & set(l_):
                 raise AssertionError("P and L overlap")
-        ev = r["evicted"][0]
-        if ev:
-            if min(ev) <= last:
-                raise AssertionError("eviction ids must strictly increase")
-            last = max(ev)
+    sinks = set(range(cfg.blocks_per_chunk))
+    for u in range(n_units):
+        last, sunk = -1, False
+        for r in updates:
+            ev = r["evicted"][u]
+            if ev:
+                if min(ev) <= last:
+                    raise AssertionError("eviction ids must strictly increase")
+                last = max(ev)
+            p = set(r["persistent"][u])
+            if sunk and not sinks <= p:
+                raise AssertionError(f"sink retention violated (unit {u}, chunk {r['chunk']})")
+            sunk = sunk or sinks <= p
 
 
 def main(argv=None):
@@ -264,7 +298,7 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=4, help="denoise steps T")
     ap.add_argument("--topk", type=float, default=0.25)
     ap.add_argument("--capacity-frames", type=int, default=6)
-    ap.add_argument("--window-frames", type=int, default=12)
+    ap.add_argument("--window-frames", type=int, default=6)
     ap.add_argument("--layers", type=int, default=30)
     ap.add_argument("--heads", type=int, default=12)
     ap.add_argument("--seed", type=int, default=7)
@@ -283,6 +317,9 @@ def main(argv=None):
     t0 = time.time()
     frames, trace, timing = run_inference(cfg, trace_path=trace_path)
     check_trace(cfg, trace)
+    if a.out:  # frames as PBT1 tensors, Latent4D (t, h, w, d) f32
+        for i, fr in enumerate(frames):
+            pbsa.write_tensor(os.path.join(a.out, f"frame_{i:04d}.pbt1"), fr.float().cpu().numpy())
     steady = timing["chunk_ms"][cfg.window_chunks + 2:] or timing["chunk_ms"]
     print(json.dumps({"chunks": cfg.num_chunks, "layers": cfg.layers, "heads": cfg.heads,
                       "pbsa_calls": timing["pbsa_calls"], "chunk_ms": timing["chunk_ms"],

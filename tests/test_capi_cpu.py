@@ -9,11 +9,12 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 HEADER = os.path.join(ROOT, "include", "pbsa_b200.h")
+DEBUG_HEADER = os.path.join(ROOT, "include", "pbsa_b200_debug.h")
 LIB = os.path.join(ROOT, "paper_2604_21221_b200", "_lib", "libpbsa_b200.so")
 
 
-def declared():
-    text = open(HEADER).read()
+def declared(header=HEADER):
+    text = open(header).read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
     return sorted(set(re.findall(r"\b(pbsa_[a-z0-9_]+)\s*\(", text)))
 
@@ -36,6 +37,20 @@ def test_library_exports_every_declared_symbol():
 def test_python_binding_matches_header():
     from paper_2604_21221_b200 import _capi
     assert sorted(_capi.EXPORTED) == declared()
+    # the test hooks live in their own header, outside the drop-in boundary
+    assert sorted(_capi.DEBUG_EXPORTED) == declared(DEBUG_HEADER)
+    assert not set(declared(DEBUG_HEADER)) & set(declared())
+    lib = C.CDLL(LIB)
+    assert all(hasattr(lib, n) for n in declared(DEBUG_HEADER))
+
+
+@pytest.mark.skipif(not os.path.exists(LIB), reason="library not built")
+def test_fault_injection_names():
+    from paper_2604_21221_b200 import _capi
+    assert _capi.LIB.pbsa_debug_set_fault(b"no-such-fault") == _capi.PBSA_EINVAL
+    assert b"unknown fault" in _capi.LIB.pbsa_last_error()
+    assert _capi.LIB.pbsa_debug_set_fault(b"drop-sink") == _capi.PBSA_OK
+    assert _capi.LIB.pbsa_debug_set_fault(None) == _capi.PBSA_OK
 
 
 @pytest.mark.skipif(not os.path.exists(LIB), reason="library not built")

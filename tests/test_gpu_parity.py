@@ -9,7 +9,7 @@ import pytest
 import torch
 
 from oracle import oracle as orc
-from tests.pbsa_oracle_compose import bf16_round, check_attention, normal_bf16
+from tests.pbsa_oracle_compose import OracleReplay, bf16_round, check_attention, normal_bf16
 
 pytestmark = pytest.mark.gpu
 
@@ -305,17 +305,14 @@ def test_bsa_fwd_long_list(pb):
 # ------------------------------------------------------------------ (d) memory + full calls
 def run_rollout(pb, units, d, b, bpc, C, W, n_chunks, k_top, seed, denoise_steps=1, check_qb=None,
                 attn_from_chunk=0, expect_plan=None):
-    """Alg. 1 over n_chunks chunks, every PBSA call checked against the oracle: Top-K indices, s_t
-    and P / L ids bit-exact on every call; attention (sampled query blocks `check_qb`, from chunk
-    `attn_from_chunk` on) within the bf16 tolerance.  expect_plan: dict of pbsa_bsa_plan fields the
-    K3 launch of every checked call must have (e.g. {"list_entry_bytes": 2})."""
+    """Alg. 1 over n_chunks chunks, every PBSA call checked against the oracle (OracleReplay):
+    Top-K indices, s_t and P / L ids bit-exact on every call; attention (sampled query blocks
+    `check_qb`, from chunk `attn_from_chunk` on) within the bf16 tolerance.  expect_plan: dict of
+    pbsa_bsa_plan fields the K3 launch of every attention-checked call must have."""
     mem = pb.Memory(units, C, W, bpc, b, d)
-    oms = [orc.Memory(C, W) for _ in range(units)]
-    kst, vst, rep = {}, {}, {}  # (u, id) -> [b, d] f32 K / V and [d] representative of committed blocks
+    rep = OracleReplay(units, C, W, bpc, b, d)
     stats = []
-    empty = np.zeros((0, b, d), np.float32)
     for c in range(n_chunks):
-        ids = np.arange(c * bpc, (c + 1) * bpc, dtype=np.int64)
         for step in range(denoise_steps + 1):
             update = step == denoise_steps
             base = seed * 1000003 + c * 17 + step
@@ -334,60 +331,13 @@ def run_rollout(pb, units, d, b, bpc, C, W, n_chunks, k_top, seed, denoise_steps
                 for key, want in expect_plan.items():
                     assert getattr(plan, key) == want, f"K3 plan {key} = {getattr(plan, key)}, expected {want}"
             sel_gpu, st_gpu = mem.last_selection()
-            o = o.float().cpu().numpy()
-            sel_gpu = None if sel_gpu is None else sel_gpu.cpu().numpy()
-            st_gpu = None if st_gpu is None else st_gpu.cpu().numpy()
-            for u in range(units):
-                a_ids, _, n_p, n_l = oms[u].assemble()
-                p_ids, l_ids = a_ids[:n_p], a_ids[n_p:]
-                qb = q[u].reshape(bpc, b, d)
-                cur_k = kc[u].reshape(bpc, b, d)
-                cur_v = vc[u].reshape(bpc, b, d)
-                qc = orc.compress_blocks(qb)
-                k = min(k_top, n_l)
-                sel = np.zeros((bpc, 0), np.int32)
-                if k > 0:
-                    kc_l = np.stack([rep[(u, i)] for i in l_ids])
-                    sel = orc.select_topk(orc.coarse_attention(qc, kc_l), k)
-                    assert np.array_equal(sel_gpu[u], sel), f"chunk {c} step {step} unit {u}: Top-K"
-                if check_attn:
-                    store_k = np.concatenate([np.stack([kst[(u, i)] for i in p_ids]) if n_p else empty, cur_k,
-                                              np.stack([kst[(u, i)] for i in l_ids]) if n_l else empty])
-                    store_v = np.concatenate([np.stack([vst[(u, i)] for i in p_ids]) if n_p else empty, cur_v,
-                                              np.stack([vst[(u, i)] for i in l_ids]) if n_l else empty])
-                    dense = np.arange(n_p + bpc)
-                    vis = np.stack([np.concatenate([dense, n_p + bpc + sel[i]]) for i in range(bpc)]).astype(np.int32)
-                    qmask = None
-                    if check_qb is not None:
-                        qmask = np.zeros(bpc, np.uint8)
-                        qmask[check_qb] = 1
-                    want = orc.attention_sparse(qb, store_k, store_v, vis, qmask=qmask)
-                    rows = slice(None) if check_qb is None else check_qb
-                    stats.append(check_attention(o[u].reshape(bpc, b, d)[rows], want[rows]))
-                if update:
-                    cur_rep = orc.compress_blocks(cur_k)
-                    keys_rep = np.concatenate([np.stack([rep[(u, i)] for i in p_ids]) if n_p else np.zeros((0, d), np.float32),
-                                               np.stack([rep[(u, i)] for i in l_ids]) if n_l else np.zeros((0, d), np.float32),
-                                               cur_rep])
-                    key_ids = np.concatenate([p_ids, l_ids, ids])
-                    s_ref = orc.aggregate_scores(orc.coarse_attention(qc, keys_rep))
-                    assert np.array_equal(bits(st_gpu[u][:len(key_ids)]), bits(s_ref)), f"chunk {c} unit {u}: s_t"
-                    ev = oms[u].push_chunk(ids)
-                    oms[u].update_persistent(ev, key_ids, s_ref)
-                    for i in range(bpc):
-                        kst[(u, ids[i])] = cur_k[i]
-                        vst[(u, ids[i])] = cur_v[i]
-                        rep[(u, ids[i])] = cur_rep[i]
-                    keep = set(oms[u].assemble()[0].tolist())
-                    for key in [key for key in kst if key[0] == u and key[1] not in keep]:
-                        del kst[key], vst[key], rep[key]
+            stats += rep.call(q, kc, vc, k_top, update, o=o.float().cpu().numpy() if check_attn else None,
+                              sel=None if sel_gpu is None else sel_gpu.cpu().numpy(),
+                              s_t=None if st_gpu is None else st_gpu.cpu().numpy(), check_qb=check_qb,
+                              where=f"chunk {c} step {step}")
         # after the k=0 pass: P and L block ids bit-exact (SPEC.md:209-217 order)
         gp, gl = mem.assemble()
-        gp, gl = gp.cpu().numpy(), gl.cpu().numpy()
-        for u in range(units):
-            a_ids, _, n_p, n_l = oms[u].assemble()
-            assert np.array_equal(gp[u], a_ids[:n_p]), f"chunk {c} unit {u}: persistent ids"
-            assert np.array_equal(gl[u], a_ids[n_p:]), f"chunk {c} unit {u}: local ids"
+        rep.check_ids(gp.cpu().numpy(), gl.cpu().numpy(), where=f"chunk {c}")
     assert mem.status() == 0  # no NaN rows, no certified-bound canary (bit 2)
     mem.close()
     return stats

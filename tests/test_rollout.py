@@ -6,6 +6,7 @@ import torch
 
 from oracle import oracle as orc
 from paper_2604_21221_b200 import rollout as ro
+from tests.pbsa_oracle_compose import OracleReplay
 
 
 def small_cfg(**kw):
@@ -77,3 +78,100 @@ def test_rollout_latent_path_equals_blocked_path():
     assert ta == tb
     for a, b in zip(fa, fb):
         assert torch.equal(a, b)
+
+
+def replay(cfg, capture, units=None, check_qb=None):
+    """Replay the layer-0 PBSA calls a rollout captured through the oracle: per call
+    Top-K indices, s_t and P / L ids bit-exact, attention output within the bf16 tolerance."""
+    units = cfg.heads if units is None else units
+    rep = OracleReplay(units, cfg.capacity_blocks, cfg.window_chunks, cfg.blocks_per_chunk, cfg.b, cfg.head_dim)
+    stats = []
+    for i, c in enumerate(capture):
+        upd = c["mode"] == 1
+        stats += rep.call(c["q"][:units].numpy(), c["k"][:units].numpy(), c["v"][:units].numpy(), c["k_top"], upd,
+                          o=c["o"][:units].numpy(), sel=None if c["sel"] is None else c["sel"][:units].numpy(),
+                          s_t=None if c["s_t"] is None else c["s_t"][:units].numpy(), check_qb=check_qb,
+                          where=f"call {i}")
+        rep.check_ids(c["persistent"][:units].numpy(), c["window"][:units].numpy(), where=f"call {i}")
+    return stats
+
+
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("latent", [True, False])
+def test_rollout_replays_through_oracle(latent):
+    """Every layer-0 PBSA call of a rollout (denoise and k=0 passes, 7 chunks: sinks, dynamic
+    blocks and evictions) replayed through the oracle on the captured inputs."""
+    _need_gpu()
+    cfg = small_cfg(num_chunks=7, latent=latent)
+    cap = []
+    ro.run_inference(cfg, capture=cap)
+    assert len(cap) == cfg.num_chunks * (len(cfg.timesteps) + 1)
+    stats = replay(cfg, cap)
+    assert stats and max(s[0] for s in stats) <= 2e-2
+
+
+@pytest.mark.gpu
+def test_rollout_wan_layout_replays_through_oracle():
+    """The Wan-1.3B layer layout (30x52 latent frames, (1,15,4) blocks, 12 heads, 3-frame chunks,
+    C = 6 frames, window 6 frames, Top-K 25 %) over 5 chunks: 3 heads replayed, attention on sampled
+    query blocks."""
+    _need_gpu()
+    cfg = ro.RolloutConfig(num_chunks=5, timesteps=(1.0, 0.5), layers=1, trace_units=12)
+    cap = []
+    _, trace, _ = ro.run_inference(cfg, capture=cap)
+    ro.check_trace(cfg, trace)
+    replay(cfg, cap, units=3, check_qb=np.array([0, 31, 77]))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("M", [1, 4, 12])
+@pytest.mark.parametrize("T", [1, 4])
+def test_acceptance6_trace_invariants(M, T, tmp_path):
+    """SPEC.md:664 acceptance 6: for M in {1,4,12}, T in {1,4}: M*T denoise records (plus the k=0
+    pass of each chunk on the device), M cache updates each at j=1, |P| <= C and |window| <= L_local
+    at every record, eviction ids strictly increasing, byte-identical reruns."""
+    _need_gpu()
+    ts = tuple(1.0 - i / T for i in range(T))
+    cfg = small_cfg(num_chunks=M, timesteps=ts, trace_units=2)
+    outs = []
+    for rep in range(2):
+        path = tmp_path / f"trace{rep}.jsonl"
+        frames, trace, timing = ro.run_inference(cfg, trace_path=str(path))
+        ro.check_trace(cfg, trace)
+        assert len(trace) == M * T
+        assert sum(r["cache_updated"] for r in trace) == M
+        assert all(r["j"] == 1 for r in trace if r["cache_updated"])
+        assert timing["pbsa_calls"] == M * (T + 1) * cfg.layers
+        outs.append((path.read_bytes(), frames))
+    assert outs[0][0] == outs[1][0]
+    for a, b in zip(outs[0][1], outs[1][1]):
+        assert torch.equal(a, b)
+
+
+@pytest.mark.gpu
+def test_fault_drop_sink_is_caught():
+    """Negative control (SPEC.md:625 `verify --fault drop-sink`): with K4's sink retention broken
+    the oracle replay's bit-exact P check and the trace's sink-retention invariant both fail."""
+    _need_gpu()
+    import paper_2604_21221_b200 as pb
+    cfg = small_cfg(num_chunks=7, trace_units=2)
+    cap = []
+    pb.debug_set_fault("drop-sink")
+    try:
+        _, trace, _ = ro.run_inference(cfg, capture=cap)
+    finally:
+        pb.debug_set_fault(None)
+    with pytest.raises(AssertionError, match="sink retention"):
+        ro.check_trace(cfg, trace)
+    with pytest.raises(AssertionError, match="persistent ids|Top-K|s_t"):
+        replay(cfg, cap)
+    # and without the fault the same rollout passes both
+    cap = []
+    _, trace, _ = ro.run_inference(cfg, capture=cap)
+    ro.check_trace(cfg, trace)
+    replay(cfg, cap)
