@@ -37,12 +37,28 @@ clean:
 # C++ drop-in API check (host code over the C ABI; runs on a GPU box via tests/test_cpp_api.py)
 cpp-test: build/test_pbsa_cpp
 
-build/test_pbsa_cpp: tests/cpp/test_pbsa_cpp.cpp include/pbsa/pbsa_b200.hpp include/pbsa/tensor.hpp $(LIB)
-	@mkdir -p build
-	$(NVCC) $(ARCH) -std=c++20 -O2 -ccbin $(HOSTCXX) -Iinclude tests/cpp/test_pbsa_cpp.cpp -o $@ \
-	  -L$(PKG)/_lib -lpbsa_b200 -Xlinker -rpath -Xlinker '$$ORIGIN/../$(PKG)/_lib'
+CPPHDR := $(wildcard include/pbsa/*.hpp) include/pbsa_b200.h tests/cpp/spec_kats.inc
 
-.PHONY: cpp-test
+# plain g++: the C++ API needs no CUDA toolchain (device memory goes through the C ABI)
+build/test_pbsa_cpp: tests/cpp/test_pbsa_cpp.cpp $(CPPHDR) $(LIB)
+	@mkdir -p build
+	$(HOSTCXX) -std=c++20 -O2 -Wall -Iinclude tests/cpp/test_pbsa_cpp.cpp -o $@ \
+	  -L$(PKG)/_lib -lpbsa_b200 -Wl,-rpath,'$$ORIGIN/../$(PKG)/_lib'
+
+# The same SPEC checks built the way a reference maintainer would: the reference's own headers FIRST
+# on the include path (its DenseMatrix / Latent4D / BlockedTensor and its CPU matmul, softmax, blockify,
+# PBT1 from its own tensor.cpp / blockify.cpp / tensor_io.cpp), this repo's include/ second for
+# pbsa/pbsa_b200.hpp.  Only where /root/reference exists; the binary (git-ignored) travels to the GPU box.
+REFPROJ ?= /root/reference/proj
+cpp-test-ref: build/ref/test_ref_headers
+
+build/ref/test_ref_headers: tests/cpp/test_ref_headers.cpp $(CPPHDR) $(LIB)
+	@mkdir -p build/ref
+	$(HOSTCXX) -std=c++20 -O2 -Wall -fopenmp -I$(REFPROJ)/include -Iinclude tests/cpp/test_ref_headers.cpp \
+	  $(REFPROJ)/src/tensor.cpp $(REFPROJ)/src/blockify.cpp $(REFPROJ)/src/tensor_io.cpp -o $@ \
+	  -L$(PKG)/_lib -lpbsa_b200 -Wl,-rpath,'$$ORIGIN/../../$(PKG)/_lib'
+
+.PHONY: cpp-test cpp-test-ref
 
 # K3 handshake-timeline build (tools/k3_timeline.py; perf experiments only)
 trace-lib: build/trace/libpbsa_b200.so

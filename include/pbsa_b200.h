@@ -86,6 +86,49 @@ typedef struct pbsa_bsa_plan {
 } pbsa_bsa_plan;
 int pbsa_bsa_fwd_last_plan(pbsa_bsa_plan* out);
 
+/* ---- the reference's tensor-module primitives and the SPEC router / memory ops on plain device
+ * f32 row-major matrices (the drop-in C++ free functions of include/pbsa/tensor.hpp, blockify.hpp and
+ * pbsa_b200.hpp run on these; the fused hot path above never does).  Bit-exact with the reference's
+ * CPU code on the same inputs (fp64 accumulation in the reference's order). */
+/* matmul (tensor.cpp:8-32, b_transposed = 0: b [k][m]) / matmul_nt (tensor.cpp:34-55, b_transposed = 1:
+ * b [m][k]): c [n][m] = float(sum over ascending k of double(a[i][k]) * double(b(k, j))) * scale
+ * (fp32 multiply; scale = 1 is the reference op, d^-1/2 the coarse logits of SPEC.md:281). */
+int pbsa_matmul(const float* a, const float* b, int n, int k_dim, int m, int b_transposed, float scale, float* c,
+                void* stream);
+/* masked_softmax_rows (tensor.cpp:57-108): out [rows][cols]; mask (nullable) of 0 / -inf entries.
+ * status (device int, nullable) gets bit 0 if scores hold a NaN and bit 1 if a mask entry is neither
+ * 0 nor -inf -- the inputs the reference rejects with std::invalid_argument. */
+int pbsa_masked_softmax_rows(const float* scores, const float* mask, int rows, int cols, float* out, int* status,
+                             void* stream);
+/* aggregate_scores: s[j] = float(sum over ascending i of double(a[i][j]) / rows). */
+int pbsa_aggregate_scores(const float* a, int rows, int cols, float* s, void* stream);
+/* compress_blocks on f32 blocks: x (n_blocks, b, d) -> reps (n_blocks, d), each the
+ * mean of its b tokens with the same fp64 ascending-token sum as aggregate_scores (the hot path's K1,
+ * pbsa_compress, is the bf16 form of the same op). */
+int pbsa_compress_f32(const float* x, int n_blocks, int b, int d, float* reps, void* stream);
+/* select_topk with an absolute k (1 <= k <= cols): sel [rows][k] = indices of the k
+ * largest entries of each row by (value desc, index asc), ascending.  workspace:
+ * pbsa_select_topk_workspace(rows, cols) bytes; status bit 0 = NaN in a. */
+size_t pbsa_select_topk_workspace(int rows, int cols);
+int pbsa_select_topk(const float* a, int rows, int cols, int k, int32_t* sel, void* workspace, size_t workspace_bytes,
+                     int* status, void* stream);
+/* blockify (blockify.cpp:38-65; inverse = 0): x (t, h, w, d) -> y (n_b, b, d) block-major; unblockify
+ * (blockify.cpp:67-96; inverse = 1): x (n_b, b, d) -> y (t, h, w, d).  PBSA_EINVAL naming the axis when
+ * (b_t, b_h, b_w) does not divide (t, h, w) (make_block_layout, blockify.cpp:7-36). */
+int pbsa_blockify(const float* x, int t, int h, int w, int d, int b_t, int b_h, int b_w, float* y, int inverse,
+                  void* stream);
+/* update_persistent's ranking (Eq. 9): keep[i] = 1 for the `slots` best candidates by
+ * (score desc, id asc), 0 otherwise (slots = C - |sinks|; sinks never compete).  status bit 0 = NaN score
+ * (ranked lowest, as K4 does). */
+int pbsa_topc_select(const int64_t* ids, const float* scores, int n, int slots, uint8_t* keep, int* status,
+                     void* stream);
+
+/* Device memory for callers that hold no CUDA runtime of their own (the header-only C++ API):
+ * cudaMalloc / cudaFree, cudaMemcpyAsync(cudaMemcpyDefault) and cudaStreamSynchronize. */
+int pbsa_dev_alloc(void** out, size_t bytes);
+int pbsa_dev_free(void* p);
+int pbsa_stream_sync(void* stream);
+
 /* (c') block-sparse attention backward -- the gradient of pbsa_bsa_fwd (the training path of
  * Alg. 2; the reference has no backward, the oracle is the derivative of
  * attention_sparse).  Inputs as pbsa_bsa_fwd plus the forward's o, its natural-log lse

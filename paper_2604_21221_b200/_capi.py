@@ -56,6 +56,17 @@ _SIGS = {
     "pbsa_bsa_fwd": (_i32, [_vp, _vp, _vp, _i32, _vp, _i32, _i32, _vp, _i32, _i32, _vp, _i32,
                             _i32, _i32, _i32, _i32, _f32, _vp, _vp, _vp, C.c_size_t, _vp]),
     "pbsa_bsa_fwd_last_plan": (_i32, [C.POINTER(BsaPlan)]),
+    "pbsa_matmul": (_i32, [_vp, _vp, _i32, _i32, _i32, _i32, _f32, _vp, _vp]),
+    "pbsa_masked_softmax_rows": (_i32, [_vp, _vp, _i32, _i32, _vp, _vp, _vp]),
+    "pbsa_aggregate_scores": (_i32, [_vp, _i32, _i32, _vp, _vp]),
+    "pbsa_compress_f32": (_i32, [_vp, _i32, _i32, _i32, _vp, _vp]),
+    "pbsa_select_topk_workspace": (C.c_size_t, [_i32, _i32]),
+    "pbsa_select_topk": (_i32, [_vp, _i32, _i32, _i32, _vp, _vp, C.c_size_t, _vp, _vp]),
+    "pbsa_blockify": (_i32, [_vp, _i32, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _i32, _vp]),
+    "pbsa_topc_select": (_i32, [_vp, _vp, _i32, _i32, _vp, _vp, _vp]),
+    "pbsa_dev_alloc": (_i32, [C.POINTER(_vp), C.c_size_t]),
+    "pbsa_dev_free": (_i32, [_vp]),
+    "pbsa_stream_sync": (_i32, [_vp]),
     "pbsa_bsa_bwd_workspace": (C.c_size_t, [_i32, _i32, _i32, _i32]),
     "pbsa_bsa_bwd": (_i32, [_vp, _vp, _vp, _i32, _vp, _i32, _i32, _vp, _i32, _i32, _vp, _i32,
                             _i32, _i32, _i32, _i32, _f32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, C.c_size_t, _vp]),

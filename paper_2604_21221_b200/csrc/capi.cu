@@ -284,6 +284,88 @@ int pbsa_score_select(const float* qc, const float* krep, int64_t krep_unit_stri
                                as_stream(stream));
 }
 
+int pbsa_matmul(const float* a, const float* b, int n, int k_dim, int m, int b_transposed, float scale, float* c,
+                void* stream) {
+    PBSA_REQUIRE(n >= 0 && k_dim >= 0 && m >= 0, "matmul: negative dims");
+    PBSA_REQUIRE((n == 0 || m == 0) || (c != nullptr && (k_dim == 0 || (a != nullptr && b != nullptr))),
+                 "matmul: null pointer");
+    return launch_matmul_f64acc(a, b, n, k_dim, m, b_transposed ? 1 : 0, scale, c, as_stream(stream));
+}
+
+int pbsa_masked_softmax_rows(const float* scores, const float* mask, int rows, int cols, float* out, int* status,
+                             void* stream) {
+    PBSA_REQUIRE(rows >= 0 && cols >= 0, "masked_softmax_rows: negative dims");
+    PBSA_REQUIRE(rows == 0 || cols == 0 || (scores != nullptr && out != nullptr), "masked_softmax_rows: null pointer");
+    if (cols == 0) return PBSA_OK;
+    return launch_softmax_rows(scores, mask, rows, cols, out, status, as_stream(stream));
+}
+
+int pbsa_aggregate_scores(const float* a, int rows, int cols, float* s, void* stream) {
+    PBSA_REQUIRE(rows >= 1, "aggregate_scores: no rows");
+    PBSA_REQUIRE(cols >= 0, "aggregate_scores: negative dims");
+    PBSA_REQUIRE(cols == 0 || (a != nullptr && s != nullptr), "aggregate_scores: null pointer");
+    return launch_aggregate_scores(a, rows, cols, 1, s, as_stream(stream));
+}
+
+int pbsa_compress_f32(const float* x, int n_blocks, int b, int d, float* reps, void* stream) {
+    PBSA_REQUIRE(n_blocks >= 0 && d >= 0, "compress_blocks: negative counts");
+    PBSA_REQUIRE(b >= 1, "compress_blocks: block size b must be >= 1");
+    PBSA_REQUIRE(n_blocks == 0 || d == 0 || (x != nullptr && reps != nullptr), "compress_blocks: null pointer");
+    if (n_blocks == 0 || d == 0) return PBSA_OK;
+    return launch_aggregate_scores(x, b, d, n_blocks, reps, as_stream(stream));
+}
+
+size_t pbsa_select_topk_workspace(int rows, int cols) {
+    if (rows < 0 || cols < 0) return 0;
+    return static_cast<size_t>(rows) * cols * 4 + 16;
+}
+
+int pbsa_select_topk(const float* a, int rows, int cols, int k, int32_t* sel, void* workspace, size_t workspace_bytes,
+                     int* status, void* stream) {
+    PBSA_REQUIRE(rows >= 0 && cols >= 1, "select_topk: empty local region");
+    PBSA_REQUIRE(k >= 1 && k <= cols, "select_topk: k must be in [1, cols]");
+    PBSA_REQUIRE(rows == 0 || (a != nullptr && sel != nullptr && workspace != nullptr), "select_topk: null pointer");
+    PBSA_REQUIRE(workspace_bytes >= pbsa_select_topk_workspace(rows, cols), "select_topk: workspace too small");
+    return launch_select_topk(a, rows, cols, k, sel, static_cast<uint32_t*>(workspace), status, as_stream(stream));
+}
+
+int pbsa_blockify(const float* x, int t, int h, int w, int d, int b_t, int b_h, int b_w, float* y, int inverse,
+                  void* stream) {
+    PBSA_REQUIRE(t >= 0 && h >= 0 && w >= 0 && d >= 0, "blockify: negative dims");
+    PBSA_REQUIRE(b_t >= 1 && b_h >= 1 && b_w >= 1, "block shape extents must be >= 1");
+    PBSA_REQUIRE(t % b_t == 0, "axis t (" + std::to_string(t) + ") not divisible by b_t (" + std::to_string(b_t) + ")");
+    PBSA_REQUIRE(h % b_h == 0, "axis h (" + std::to_string(h) + ") not divisible by b_h (" + std::to_string(b_h) + ")");
+    PBSA_REQUIRE(w % b_w == 0, "axis w (" + std::to_string(w) + ") not divisible by b_w (" + std::to_string(b_w) + ")");
+    const int64_t n = static_cast<int64_t>(t) * h * w * d;
+    PBSA_REQUIRE(n == 0 || (x != nullptr && y != nullptr), "blockify: null pointer");
+    PBSA_REQUIRE(static_cast<int64_t>(t) * h * w < (int64_t(1) << 31), "blockify: too many tokens");
+    return launch_blockify(x, t, h, w, d, b_t, b_h, b_w, y, inverse ? 1 : 0, as_stream(stream));
+}
+
+int pbsa_topc_select(const int64_t* ids, const float* scores, int n, int slots, uint8_t* keep, int* status,
+                     void* stream) {
+    PBSA_REQUIRE(n >= 0 && slots >= 0, "update_persistent: negative counts");
+    PBSA_REQUIRE(n == 0 || (ids != nullptr && scores != nullptr && keep != nullptr), "update_persistent: null pointer");
+    return launch_topc_keep(ids, scores, n, slots, keep, status, as_stream(stream));
+}
+
+int pbsa_dev_alloc(void** out, size_t bytes) {
+    PBSA_REQUIRE(out != nullptr, "dev_alloc: null output");
+    *out = nullptr;
+    PBSA_CUDA(cudaMalloc(out, bytes ? bytes : 1));
+    return PBSA_OK;
+}
+
+int pbsa_dev_free(void* p) {
+    if (p) PBSA_CUDA(cudaFree(p));
+    return PBSA_OK;
+}
+
+int pbsa_stream_sync(void* stream) {
+    PBSA_CUDA(cudaStreamSynchronize(as_stream(stream)));
+    return PBSA_OK;
+}
+
 int pbsa_bsa_fwd_last_plan(pbsa_bsa_plan* out) {
     PBSA_REQUIRE(out != nullptr, "bsa_fwd_last_plan: null output");
     *out = last_bsa_plan();

@@ -81,6 +81,19 @@ int launch_score_select(const float* qc, const float* krep, int64_t krep_unit_st
                         const int32_t* key_slots, int key_stride, int n_keys, int local_off,
                         int n_local, int k, int nqb, int units, int d, float scale, int32_t* sel,
                         float* s_t, void* ws, size_t ws_bytes, cudaStream_t s, int* status = nullptr);
+// aggregate_scores (Eq. 8): s[u][j] = float(sum_i double(a[u][i][j]) / rows), ascending i
+int launch_aggregate_scores(const float* a, int rows, int cols, int units, float* s, cudaStream_t st);
+// SPEC-op primitives on device f32 matrices (spec_ops.cu; the drop-in C++ API, not the hot path)
+int launch_matmul_f64acc(const float* a, const float* b, int n, int kd, int m, int bt, float scale, float* c,
+                         cudaStream_t s);
+int launch_softmax_rows(const float* scores, const float* mask, int rows, int cols, float* out, int* status,
+                        cudaStream_t s);
+int launch_select_topk(const float* a, int rows, int cols, int k, int32_t* sel, uint32_t* keys, int* status,
+                       cudaStream_t s);
+int launch_blockify(const float* x, int t, int h, int w, int d, int bt, int bh, int bw, float* y, int inverse,
+                    cudaStream_t s);
+int launch_topc_keep(const int64_t* ids, const float* scores, int n, int slots, uint8_t* keep, int* status,
+                     cudaStream_t s);
 // K3
 // lat != null: q and o are chunk latents (Q blocks gathered by a 5-D TMA box, O rows scattered back
 // to their latent positions in the epilogue -- unblockify fused); lse stays [units][n_q] block-major

@@ -16,6 +16,7 @@
 // Roofline: HBM (candidate scores + slot tables); launch-latency bound at Wan-1.3B shape.
 #include "internal.h"
 #include "ptx.cuh"
+#include "select_warp.cuh"
 
 namespace pbsa {
 namespace {
@@ -27,8 +28,6 @@ struct CommitParams {
     MemCounts cur, next;
     int fault;  // kFaultDropSink: sinks compete with the dynamic candidates (negative control)
 };
-
-__device__ __forceinline__ float nan_low(float x) { return x != x ? -INFINITY : x; }
 
 __global__ void mem_init_kernel(MemDev m, int C, int Lcap, int bpc, int S) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *m.status = 0;
@@ -105,12 +104,8 @@ __global__ void __launch_bounds__(256) mem_commit_kernel(const CommitParams p) {
         // injected fault: every candidate, sinks included, competes for all C slots -- the
         // kept count (and so the slot accounting) is unchanged, only sink retention is broken
         for (int i = tid; i < n_cand; i += nt) {
-            const float si = nan_low(c_score[i]);
             int rank = 0;
-            for (int j = 0; j < n_cand; ++j) {
-                const float sj = nan_low(c_score[j]);
-                rank += (sj > si) || (sj == si && c_id[j] < c_id[i]);
-            }
+            for (int j = 0; j < n_cand; ++j) rank += topc_before(c_score[j], c_id[j], c_score[i], c_id[i]);
             c_keep[i] = rank < C;
         }
     } else
@@ -120,13 +115,10 @@ __global__ void __launch_bounds__(256) mem_commit_kernel(const CommitParams p) {
             // (score desc, id asc) is a strict total order once NaN (invalid input, which the
             // reference rejects, tensor.cpp:61-64) ranks below every number: exactly dyn_cap
             // candidates survive whatever the scores are, so the slot accounting stays exact
-            const float si = nan_low(c_score[i]);
-            const int64_t ii = c_id[i];
             int rank = 0;
             for (int j = n_s; j < n_cand; ++j) {
                 if (sink_chunk && j >= n_p) break;
-                const float sj = nan_low(c_score[j]);
-                rank += (sj > si) || (sj == si && c_id[j] < ii);
+                rank += topc_before(c_score[j], c_id[j], c_score[i], c_id[i]);
             }
             keep = rank < dyn_cap;
             if (c_score[i] != c_score[i]) atomicOr(p.m.status, 2);

@@ -145,6 +145,107 @@ def attention_sparse(q: torch.Tensor, k_pool: torch.Tensor, v_pool: torch.Tensor
     return (o, lse) if want_lse else o
 
 
+# ---- the reference's tensor / blockify primitives and the SPEC router / memory ops on device f32
+# tensors (bit-exact with the reference's CPU code; the fused hot path never uses them) ------------
+def _f32(t: torch.Tensor, name: str) -> None:
+    _need(t, torch.float32, name)
+
+
+def _status_check(st: torch.Tensor, msgs: dict) -> None:
+    flags = int(st.item())
+    for bit, msg in msgs.items():
+        if flags & bit:
+            raise PbsaError(msg)
+
+
+def matmul(a: torch.Tensor, b: torch.Tensor, transpose_b: bool = False, scale: float = 1.0) -> torch.Tensor:
+    """matmul (tensor.cpp:8-32) / matmul_nt (transpose_b, tensor.cpp:34-55): fp64 accumulation in
+    ascending k, one fp32 rounding, then an fp32 multiply by `scale`."""
+    _f32(a, "a")
+    _f32(b, "b")
+    n, kd = a.shape
+    m = b.shape[0] if transpose_b else b.shape[1]
+    if (b.shape[1] if transpose_b else b.shape[0]) != kd:
+        op = "matmul_nt: a.cols" if transpose_b else "matmul: a.cols"
+        raise PbsaError(f"{op} ({kd}) != b.{'cols' if transpose_b else 'rows'} ({b.shape[1] if transpose_b else b.shape[0]})")
+    c = torch.empty(n, m, device=a.device, dtype=torch.float32)
+    check(LIB.pbsa_matmul(a.data_ptr(), b.data_ptr(), n, kd, m, int(transpose_b), float(scale), c.data_ptr(), _stream()))
+    return c
+
+
+def masked_softmax_rows(scores: torch.Tensor, mask: torch.Tensor | None = None) -> torch.Tensor:
+    """masked_softmax_rows (tensor.cpp:57-108); raises PbsaError on NaN scores / non 0/-inf mask."""
+    _f32(scores, "scores")
+    if mask is not None:
+        _f32(mask, "mask")
+        if mask.shape != scores.shape:
+            raise PbsaError("masked_softmax_rows: mask shape mismatch")
+    out = torch.empty_like(scores)
+    st = torch.zeros(1, dtype=torch.int32, device=scores.device)
+    check(LIB.pbsa_masked_softmax_rows(scores.data_ptr(), _ptr(mask), scores.shape[0], scores.shape[1],
+                                       out.data_ptr(), st.data_ptr(), _stream()))
+    _status_check(st, {1: "masked_softmax_rows: NaN in scores",
+                       2: "masked_softmax_rows: mask entries must be 0 or -inf"})
+    return out
+
+
+def aggregate_scores(a: torch.Tensor) -> torch.Tensor:
+    """aggregate_scores: ascending-row fp64 column means."""
+    _f32(a, "a")
+    s = torch.empty(a.shape[1], device=a.device, dtype=torch.float32)
+    check(LIB.pbsa_aggregate_scores(a.data_ptr(), a.shape[0], a.shape[1], s.data_ptr(), _stream()))
+    return s
+
+
+def select_topk(a_local: torch.Tensor, k: int) -> torch.Tensor:
+    """select_topk with absolute k: [rows, k] int32 ascending indices of the k largest
+    entries per row, ties toward the lower index (use topk_count(n, ratio) for a ratio)."""
+    _f32(a_local, "a_local")
+    rows, cols = a_local.shape
+    sel = torch.empty(rows, max(k, 1), device=a_local.device, dtype=torch.int32)
+    ws_bytes = LIB.pbsa_select_topk_workspace(rows, cols)
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=a_local.device)
+    st = torch.zeros(1, dtype=torch.int32, device=a_local.device)
+    check(LIB.pbsa_select_topk(a_local.data_ptr(), rows, cols, int(k), sel.data_ptr(), ws.data_ptr(), ws_bytes,
+                               st.data_ptr(), _stream()))
+    _status_check(st, {1: "select_topk: NaN in scores"})
+    return sel[:, :k]
+
+
+def blockify(x: torch.Tensor, shape) -> torch.Tensor:
+    """blockify (blockify.cpp:38-65): (t, h, w, d) f32 -> block-major (n_b, b, d)."""
+    _f32(x, "x")
+    t, h, w, d = x.shape
+    bt, bh, bw = (int(v) for v in shape)
+    y = torch.empty((t * h * w) // max(bt * bh * bw, 1) if bt * bh * bw else 0, bt * bh * bw, d,
+                    device=x.device, dtype=torch.float32)
+    check(LIB.pbsa_blockify(x.data_ptr(), t, h, w, d, bt, bh, bw, y.data_ptr(), 0, _stream()))
+    return y
+
+
+def unblockify(xb: torch.Tensor, dims, shape) -> torch.Tensor:
+    """unblockify (blockify.cpp:67-96): block-major (n_b, b, d) -> (t, h, w, d)."""
+    _f32(xb, "xb")
+    t, h, w, d = (int(v) for v in dims)
+    bt, bh, bw = (int(v) for v in shape)
+    if xb.numel() != t * h * w * d:
+        raise PbsaError("blocked data length does not match layout")
+    y = torch.empty(t, h, w, d, device=xb.device, dtype=torch.float32)
+    check(LIB.pbsa_blockify(xb.data_ptr(), t, h, w, d, bt, bh, bw, y.data_ptr(), 1, _stream()))
+    return y
+
+
+def topc_select(ids: torch.Tensor, scores: torch.Tensor, slots: int) -> torch.Tensor:
+    """update_persistent's ranking: bool mask of the `slots` best candidates by
+    (score desc, id asc)."""
+    _need(ids, torch.int64, "ids")
+    _f32(scores, "scores")
+    keep = torch.empty(ids.shape[0], dtype=torch.uint8, device=ids.device)
+    check(LIB.pbsa_topc_select(ids.data_ptr(), scores.data_ptr(), ids.shape[0], int(slots), keep.data_ptr(), None,
+                               _stream()))
+    return keep.bool()
+
+
 def bsa_fwd_last_plan() -> "_capi.BsaPlan":
     """How this thread's last K3 launch was planned (list entry width, CTAs per SM, grid, schedule
     0 whole tiles / 1 hybrid stream-K / 2 unit gangs) -- pbsa_bsa_fwd_last_plan."""

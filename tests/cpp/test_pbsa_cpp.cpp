@@ -27,7 +27,13 @@ static pbsa::BlockedTensor blocks(std::size_t nb, std::size_t b, std::size_t d, 
     return t;
 }
 
+// SPEC known-answer examples of the tensor / blockify / router / memory / attention modules through
+// the GPU-backed drop-in free functions (shared with test_ref_headers.cpp, where the same checks run
+// on the reference's own types and primitives)
+#include "spec_kats.inc"
+
 int main() {
+    spec_kats();
     // compress_blocks: block {[0,2],[2,0]} -> [1,1] (d padded to 64 with zeros)
     {
         std::vector<float> v(2 * 64, 0.0f);
@@ -106,7 +112,7 @@ int main() {
             mem.write_chunk(kv.p, kv.p);
             mem.attend(q.p, 2, PBSA_MODE_CACHE_UPDATE, o.p);
         }
-        pbsa::detail::cuda(cudaDeviceSynchronize(), "sync");
+        pbsa::detail::check(pbsa_stream_sync(nullptr));
         std::vector<int64_t> P, L;
         mem.assemble(1, &P, &L);
         EXPECT(static_cast<int>(L.size()) == W * bpc);
@@ -155,8 +161,7 @@ int main() {
             dk.upload(hk.data(), hk.size());
             dv.upload(hv.data(), hv.size());
             mq.attend_qkv(dq.p, dk.p, dv.p, 2, mode, dout.p);
-            std::vector<uint16_t> ob(dq.n);
-            pbsa::detail::cuda(cudaMemcpy(ob.data(), dout.p, ob.size() * 2, cudaMemcpyDeviceToHost), "D2H");
+            const std::vector<uint16_t> ob = dout.to_host();
             const auto ol_blocked = blocked(ol);
             for (std::size_t i = 0; i < ob.size(); ++i) same &= ob[i] == ol_blocked[i];
         }
