@@ -19,7 +19,9 @@
  * Status codes: 0 ok, 1 invalid argument, 2 CUDA / launch error, 3 unsupported shape.  The
  * message of the last failure on the calling thread is returned by pbsa_last_error() (mirrors
  * the std::invalid_argument messages of tensor.cpp / blockify.cpp).  No entry point synchronizes
- * the stream; nothing allocates device memory except pbsa_mem_create.
+ * the stream.  Device memory is allocated only by pbsa_mem_create, pbsa_mem_host_reserve (the
+ * host-chunk staging of one memory; pbsa_attend_qkv_host calls it on its first use) and
+ * pbsa_dev_alloc; everything else takes caller-owned buffers and workspaces.
  */
 #ifndef PBSA_B200_H
 #define PBSA_B200_H
@@ -208,6 +210,9 @@ int pbsa_attend_qkv(pbsa_mem* m, const void* q, const void* k_chunk, const void*
  * call's compute, not after its download). */
 int pbsa_attend_qkv_host(pbsa_mem* m, const void* q_host, const void* k_host, const void* v_host, int k_top,
                          float scale, int mode, void* o_host, void* stream);
+/* Allocates the host-chunk path of m up front (two device staging sets of 4 x units x n_q x d bf16,
+ * two copy streams, events; freed by pbsa_mem_destroy).  Idempotent. */
+int pbsa_mem_host_reserve(pbsa_mem* m);
 /* Waits for every upload and download issued by pbsa_attend_qkv_host so far. */
 int pbsa_mem_host_sync(pbsa_mem* m);
 /* Number of kernels the library has launched since it was loaded (all entry points, all streams). */
@@ -233,7 +238,27 @@ int pbsa_attend_latent(pbsa_mem* m, const void* q, const void* k_lat, const void
                        const pbsa_latent_geom* g, int k_top, float scale, int mode, void* o, float* lse,
                        void* stream);
 
-/* last selection of pbsa_attend (device): [units][blocks_per_chunk][k] ascending, and last s_t */
+/* Query-split form of pbsa_attend_qkv for multi-GPU layouts whose units are fewer than the ranks
+ * (batch-1 Wan shapes: 12 heads on 8 GPUs): every rank sharing a head holds a
+ * replica of the head's memory and attends for the query blocks [q_begin, q_begin + q_count) of each
+ * unit.  q_part / o_part: [units][q_count*b][d] bf16; k_chunk / v_chunk: the WHOLE chunk
+ * [units][blocks_per_chunk*b][d] (the KV write is replicated); qc_full: caller-owned device
+ * [units][blocks_per_chunk][d] f32.
+ *   1. pbsa_attend_part_ingest: KV write + K compression, and this rank's query representatives into
+ *      rows [q_begin, q_begin + q_count) of qc_full.
+ *   2. in PBSA_MODE_CACHE_UPDATE the caller all-gathers qc_full across the replicas (s_t averages A_t
+ *      over ALL query blocks; 40 KB per head at d = 128); denoise calls need only the own rows.
+ *   3. pbsa_attend_part: Top-K of the own rows (the k=0 pass scores all rows, so every replica computes
+ *      the same s_t and commits the identical P / L update), K3 for the own query blocks, K4.
+ * Results are bit-identical to pbsa_attend_qkv on the whole chunk restricted to the part. */
+int pbsa_attend_part_ingest(pbsa_mem* m, const void* q_part, int q_begin, int q_count, const void* k_chunk,
+                            const void* v_chunk, float* qc_full, void* stream);
+int pbsa_attend_part(pbsa_mem* m, const void* q_part, int q_begin, int q_count, const float* qc_full, int k_top,
+                     float scale, int mode, void* o_part, float* lse, void* stream);
+
+/* last selection of pbsa_attend (device): [units][rows][k] ascending (rows = blocks_per_chunk, or
+ * q_count after a denoise pbsa_attend_part: see pbsa_last_selection_rows), and last s_t */
+int pbsa_last_selection_rows(const pbsa_mem* m, int* rows);
 int pbsa_last_selection(const pbsa_mem* m, const int32_t** sel, int* k, const float** s_t,
                         int* n_keys);
 

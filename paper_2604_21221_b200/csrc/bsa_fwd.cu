@@ -58,6 +58,7 @@ struct BsaParams {
     int local_stride, n_local;
     const int32_t* sel;
     int k;
+    int sel_rows, sel_row0;  // sel is [units][sel_rows][k]; query block i of the launch reads row sel_row0 + i
     bf16* o;
     float* lse;
     float scale_log2;
@@ -281,7 +282,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                     const int sel_rows = has2 ? 2 : 1;
                     for (int e = lane; e < sel_rows * p.k; e += 32) {
                         const int rw = e / p.k, c = e % p.k;
-                        const int idx = __ldg(p.sel + (static_cast<int64_t>(u) * p.nqb + qb0 + rw) * p.k + c);
+                        const int idx = __ldg(p.sel + (static_cast<int64_t>(u) * p.sel_rows + p.sel_row0 + qb0 + rw) * p.k + c);
                         atomicOr(&bm[rw * p.bm_words + (idx >> 5)], 1u << (idx & 31));
                     }
                 }
@@ -887,7 +888,7 @@ int launch_bsa_fwd(const bf16* q, const bf16* k_pool, const bf16* v_pool, int n_
                    const int32_t* dense, int dense_stride, int n_dense, const int32_t* local,
                    int local_stride, int n_local, const int32_t* sel, int k, int nqb, int b, int d,
                    int units, float scale, bf16* o, float* lse, void* ws, size_t ws_bytes, cudaStream_t s,
-                   const LatentGeom* lat) {
+                   const LatentGeom* lat, int sel_rows, int sel_row0) {
     BsaParams p{};
     p.lat = lat != nullptr;
     if (lat) p.lg = *lat;
@@ -902,6 +903,8 @@ int launch_bsa_fwd(const bf16* q, const bf16* k_pool, const bf16* v_pool, int n_
     p.local_stride = local_stride;
     p.n_local = n_local;
     p.sel = sel;
+    p.sel_rows = sel_rows > 0 ? sel_rows : nqb;
+    p.sel_row0 = sel_row0;
     p.k = (n_local > 0) ? k : 0;
     p.o = o;
     p.lse = lse;

@@ -142,7 +142,7 @@ struct pbsa_mem {
     int32_t* sel = nullptr;
     void* k3ws = nullptr;
     size_t k3ws_bytes = 0;
-    int last_k = 0, last_n_keys = 0;
+    int last_k = 0, last_n_keys = 0, last_sel_rows = 0;
     // stage profiling: 5 events per attend call, 2 per KV write
     std::vector<cudaEvent_t> ev_attend, ev_write;
     int prof_max = 0, prof_attend = 0, prof_write = 0;
@@ -639,8 +639,16 @@ int pbsa_mem_commit(pbsa_mem* m, const float* s_t, void* stream) {
 
 namespace {
 
+// The query blocks a call attends for: all of the chunk (begin 0, count bpc), or -- the query-split
+// multi-GPU layout -- the range [begin, begin + count) with `qc_full` holding the caller-gathered
+// representatives of ALL bpc query blocks (needed by the k=0 pass's s_t).
+struct QueryPart {
+    int begin = 0, count = -1;
+    const float* qc_full = nullptr;
+};
+
 int attend_impl(pbsa_mem* m, const void* q, int k_top, float scale, int mode, void* o, float* lse, void* stream,
-                bool q_compressed, const LatentGeom* lat) {
+                bool q_compressed, const LatentGeom* lat, QueryPart part = QueryPart{}) {
     PBSA_REQUIRE(m != nullptr && q != nullptr && o != nullptr, "attend: null pointer");
     PBSA_REQUIRE(mode == PBSA_MODE_DENOISE || mode == PBSA_MODE_CACHE_UPDATE, "attend: unknown mode");
     PBSA_REQUIRE(k_top >= 0, "attend: k_top must be >= 0");
@@ -650,8 +658,11 @@ int attend_impl(pbsa_mem* m, const void* q, int k_top, float scale, int mode, vo
     const int U = m->units, bpc = m->bpc, b = m->b, d = m->d;
     const int n_p = m->counts.n_p, n_l = m->counts.n_l;
     const int k = n_l == 0 ? 0 : (k_top < n_l ? k_top : n_l);
+    const bool split = part.count >= 0;
+    const int nq = split ? part.count : bpc;  // query blocks of this call
     prof_mark(m, 0, s);
-    // (a) query-block representatives (already produced by the fused ingest in pbsa_attend_qkv)
+    // (a) query-block representatives (already produced by the fused ingest in pbsa_attend_qkv; in
+    //     the split form the caller's qc_full, whose own rows pbsa_attend_part_ingest wrote)
     if (!q_compressed) {
         if (int rc = launch_compress(static_cast<const bf16*>(q), static_cast<int64_t>(bpc) * b * d,
                                      static_cast<int64_t>(b) * d, nullptr, bpc, U, b, d, m->qc,
@@ -661,26 +672,37 @@ int attend_impl(pbsa_mem* m, const void* q, int k_top, float scale, int mode, vo
     prof_mark(m, 1, s);
     // (b) coarse scoring + Top-K (+ s_t over P ++ L ++ current at the k=0 pass)
     const bool update = mode == PBSA_MODE_CACHE_UPDATE;
+    int sel_rows = bpc, sel_row0 = 0;
     if (update) {
+        // the k=0 pass always scores every query block of the chunk (s_t is their mean), so the
+        // replicas of a query-split head all commit the same update
         const int n_keys = n_p + n_l + bpc;
-        if (int rc = launch_score_select(m->qc, m->krep, static_cast<int64_t>(m->S) * d, m->dev.keys, m->S,
-                                         n_keys, n_p, n_l, k, bpc, U, d, scale, m->sel, m->s_t, m->ws,
-                                         m->ws_bytes, s, m->dev.status))
+        if (int rc = launch_score_select(split ? part.qc_full : m->qc, m->krep, static_cast<int64_t>(m->S) * d,
+                                         m->dev.keys, m->S, n_keys, n_p, n_l, k, bpc, U, d, scale, m->sel, m->s_t,
+                                         m->ws, m->ws_bytes, s, m->dev.status))
             return rc;
         m->last_n_keys = n_keys;
+        sel_row0 = split ? part.begin : 0;
     } else if (k > 0) {
+        if (split) {  // this rank's rows of qc_full, compacted into m->qc
+            PBSA_CUDA(cudaMemcpy2DAsync(m->qc, static_cast<size_t>(nq) * d * 4, part.qc_full + static_cast<size_t>(part.begin) * d,
+                                        static_cast<size_t>(bpc) * d * 4, static_cast<size_t>(nq) * d * 4, U,
+                                        cudaMemcpyDeviceToDevice, s));
+        }
         if (int rc = launch_score_select(m->qc, m->krep, static_cast<int64_t>(m->S) * d, m->dev.l_slot, m->Lcap,
-                                         n_l, 0, n_l, k, bpc, U, d, scale, m->sel, nullptr, m->ws,
+                                         n_l, 0, n_l, k, nq, U, d, scale, m->sel, nullptr, m->ws,
                                          m->ws_bytes, s, m->dev.status))
             return rc;
+        sel_rows = nq;
     }
     m->last_k = k;
+    m->last_sel_rows = sel_rows;
     prof_mark(m, 2, s);
     // (c) block-sparse attention over P ++ current (dense) and the selected local blocks
     if (int rc = launch_bsa_fwd(static_cast<const bf16*>(q), m->k_pool, m->v_pool, m->S, m->dev.dense,
-                                m->C + bpc, n_p + bpc, m->dev.l_slot, m->Lcap, n_l, m->sel, k, bpc, b, d, U,
+                                m->C + bpc, n_p + bpc, m->dev.l_slot, m->Lcap, n_l, m->sel, k, nq, b, d, U,
                                 scale, static_cast<bf16*>(o), lse, use_stream_k() ? m->k3ws : nullptr,
-                                m->k3ws_bytes, s, lat))
+                                m->k3ws_bytes, s, lat, sel_rows, sel_row0))
         return rc;
     prof_mark(m, 3, s);
     // (d) persistent-memory update after the k=0 pass
@@ -771,13 +793,58 @@ int pbsa_attend_qkv(pbsa_mem* m, const void* q, const void* k_chunk, const void*
     return attend_impl(m, q, k_top, scale, mode, o, lse, stream, true, nullptr);
 }
 
-int pbsa_attend_qkv_host(pbsa_mem* m, const void* q_host, const void* k_host, const void* v_host, int k_top,
-                         float scale, int mode, void* o_host, void* stream) {
-    PBSA_REQUIRE(m != nullptr && q_host != nullptr && k_host != nullptr && v_host != nullptr && o_host != nullptr,
-                 "attend_qkv_host: null pointer");
+int pbsa_attend_part_ingest(pbsa_mem* m, const void* q_part, int q_begin, int q_count, const void* k_chunk,
+                            const void* v_chunk, float* qc_full, void* stream) {
+    PBSA_REQUIRE(m != nullptr && q_part != nullptr && k_chunk != nullptr && v_chunk != nullptr && qc_full != nullptr,
+                 "attend_part_ingest: null pointer");
+    PBSA_REQUIRE(q_begin >= 0 && q_count >= 1 && q_begin + q_count <= m->bpc,
+                 "attend_part_ingest: query range outside the chunk's blocks");
+    PBSA_REQUIRE(aligned16(q_part) && aligned16(k_chunk) && aligned16(v_chunk) && aligned16(qc_full),
+                 "attend_part_ingest: tensors must be 16-byte aligned");
     cudaStream_t s = as_stream(stream);
+    const bool prof = m->prof_on && m->prof_write < m->prof_max;
+    if (prof) cudaEventRecord(m->ev_write[static_cast<size_t>(m->prof_write) * 2], s);
+    // the whole chunk's K/V into the stage slots + K compression (replicated on every rank holding the
+    // head), then the representatives of this rank's query blocks into their rows of qc_full
+    if (int rc = launch_write_chunk(static_cast<const bf16*>(k_chunk), static_cast<const bf16*>(v_chunk), nullptr,
+                                    m->dev.stage, m->bpc, m->b, m->d, m->units, m->S, m->k_pool, m->v_pool, m->krep,
+                                    nullptr, s))
+        return rc;
+    const int b = m->b, d = m->d;
+    if (int rc = launch_compress(static_cast<const bf16*>(q_part), static_cast<int64_t>(q_count) * b * d,
+                                 static_cast<int64_t>(b) * d, nullptr, q_count, m->units, b, d,
+                                 qc_full + static_cast<size_t>(q_begin) * d, static_cast<int64_t>(m->bpc) * d, s))
+        return rc;
+    if (prof) {
+        cudaEventRecord(m->ev_write[static_cast<size_t>(m->prof_write) * 2 + 1], s);
+        ++m->prof_write;
+    }
+    return PBSA_OK;
+}
+
+int pbsa_attend_part(pbsa_mem* m, const void* q_part, int q_begin, int q_count, const float* qc_full, int k_top,
+                     float scale, int mode, void* o_part, float* lse, void* stream) {
+    PBSA_REQUIRE(m != nullptr && qc_full != nullptr, "attend_part: null pointer");
+    PBSA_REQUIRE(q_begin >= 0 && q_count >= 1 && q_begin + q_count <= m->bpc,
+                 "attend_part: query range outside the chunk's blocks");
+    QueryPart part;
+    part.begin = q_begin;
+    part.count = q_count;
+    part.qc_full = qc_full;
+    return attend_impl(m, q_part, k_top, scale, mode, o_part, lse, stream, true, nullptr, part);
+}
+
+int pbsa_last_selection_rows(const pbsa_mem* m, int* rows) {
+    PBSA_REQUIRE(m != nullptr && rows != nullptr, "last_selection_rows: null pointer");
+    *rows = m->last_sel_rows;
+    return PBSA_OK;
+}
+
+int pbsa_mem_host_reserve(pbsa_mem* m) {
+    PBSA_REQUIRE(m != nullptr, "mem_host_reserve: null memory");
+    if (m->up != nullptr) return PBSA_OK;
     const size_t bytes = static_cast<size_t>(m->units) * m->bpc * m->b * m->d * sizeof(bf16);
-    if (m->up == nullptr) {  // first call: staging sets, copy streams, events
+    {  // two staging sets {q, k, v, o}, the copy streams and their events
         bool ok = cudaStreamCreateWithFlags(&m->up, cudaStreamNonBlocking) == cudaSuccess &&
                   cudaStreamCreateWithFlags(&m->down, cudaStreamNonBlocking) == cudaSuccess;
         for (int i = 0; ok && i < 2; ++i) {
@@ -789,9 +856,19 @@ int pbsa_attend_qkv_host(pbsa_mem* m, const void* q_host, const void* k_host, co
         if (!ok) {
             free_host_path(m);
             cudaGetLastError();
-            return set_error(PBSA_ECUDA, "attend_qkv_host: staging allocation failed");
+            return set_error(PBSA_ECUDA, "mem_host_reserve: staging allocation failed");
         }
     }
+    return PBSA_OK;
+}
+
+int pbsa_attend_qkv_host(pbsa_mem* m, const void* q_host, const void* k_host, const void* v_host, int k_top,
+                         float scale, int mode, void* o_host, void* stream) {
+    PBSA_REQUIRE(m != nullptr && q_host != nullptr && k_host != nullptr && v_host != nullptr && o_host != nullptr,
+                 "attend_qkv_host: null pointer");
+    cudaStream_t s = as_stream(stream);
+    const size_t bytes = static_cast<size_t>(m->units) * m->bpc * m->b * m->d * sizeof(bf16);
+    if (int rc = pbsa_mem_host_reserve(m)) return rc;  // no-op once reserved
     const int b = static_cast<int>(m->host_calls & 1);
     bf16* const* st = m->hstage[b];
     if (m->host_calls >= 2) {  // set b was last used two calls ago

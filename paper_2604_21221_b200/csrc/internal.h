@@ -101,7 +101,7 @@ int launch_bsa_fwd(const bf16* q, const bf16* k_pool, const bf16* v_pool, int n_
                    const int32_t* dense, int dense_stride, int n_dense, const int32_t* local,
                    int local_stride, int n_local, const int32_t* sel, int k, int nqb, int b, int d,
                    int units, float scale, bf16* o, float* lse, void* ws, size_t ws_bytes, cudaStream_t s,
-                   const LatentGeom* lat = nullptr);
+                   const LatentGeom* lat = nullptr, int sel_rows = 0, int sel_row0 = 0);
 size_t bsa_fwd_workspace(int units, int nqb, int d);
 pbsa_bsa_plan& last_bsa_plan();  // the calling thread's last K3 launch plan
 // injected fault (pbsa_debug_set_fault; negative controls only)

@@ -189,9 +189,10 @@ __global__ void __launch_bounds__(256) row_select_kernel(const ScoreParams p, co
 // float(dot64) * scale); cert_select_kernel radix-selects the k-th largest z~ (T), takes every key
 // above T + 2 eps_max + tau, drops every key below T - 2 eps_max - tau, recomputes the oracle's exact
 // logit (ascending-c fp64 dot, same roundings) for the few keys in between and ranks those exactly.
-// tau = 2^-20: two logits further apart than tau give probabilities more than 7 fp32 ulps apart
-// (exp(tau) - 1 > 2^-20.01 vs ulp <= 2^-23 for normal fp32), so no probability tie can cross the
-// boundary.  A row reruns the oracle's exact softmax + Top-K (warp_softmax / warp_topk, fp64
+// tau = 2^-22: two logits further apart than tau give probabilities whose ratio exceeds
+// exp(2^-22) > 1 + 2^-22, i.e. at least 2 fp32 ulps apart for normal fp32 (relative ulp <= 2^-23;
+// the fp64 quotient e / denom adds only 2^-53), so they cannot round to one fp32 value and no
+// probability tie can cross the boundary.  A row reruns the oracle's exact softmax + Top-K (warp_softmax / warp_topk, fp64
 // scratch in global memory) when (a) the exact gap at the boundary is <= tau, (b) boundary
 // probabilities could be subnormal (T - max z < -60), (c) more than kCertAmb keys are ambiguous,
 // (d) a logit is NaN, or (e) an exact logit falls outside its certified interval (status bit 2 --

@@ -133,3 +133,103 @@ class HeadLayout:
         if async_op:
             return work, finish
         return finish()
+
+
+class QuerySplitLayout:
+    """Batch-1 layout for any world size (config 2/3: 12 heads of one batch element on 1/2/4/8
+    GPUs).
+
+    The heads are cut into G = gcd(world, heads) groups of heads/G contiguous heads; every group is
+    replicated on R = world / G ranks and replica r attends the contiguous range r of the chunk's
+    query blocks (balanced split).  A replica holds the group's whole KV memory (the KV write is
+    replicated) and its own query blocks, so the only exchanges are
+      * at the k=0 pass, an all-gather of the query-block representatives Q^c inside the group
+        (s_t averages the coarse attention over ALL query blocks; 40 KB per head at
+        d = 128): every replica then scores all rows, so K2's s_t and K4's update are computed
+        redundantly and deterministically -- no reduction whose order could break bit-exactness;
+      * after every call, the output gather of O (the consumer needs all heads of every token).
+    12 heads: N = 2 -> 2 groups of 6 heads, R = 1; N = 4 -> 4 x 3, R = 1; N = 8 -> 4 x 3, R = 2
+    (24 half-head units, 3 per GPU)."""
+
+    def __init__(self, heads: int, bpc: int, world: int, rank: int):
+        if world < 1 or not (0 <= rank < world):
+            raise ValueError("QuerySplitLayout: bad world/rank")
+        import math
+        self.heads, self.bpc, self.world, self.rank = heads, bpc, world, rank
+        self.groups = math.gcd(world, heads)
+        self.replicas = world // self.groups
+        if bpc < self.replicas:
+            raise ValueError(f"QuerySplitLayout: {bpc} query blocks cannot be split {self.replicas} ways")
+        self.group, self.replica = divmod(rank, self.replicas)
+        self.heads_per_group = heads // self.groups
+        self.head0 = self.group * self.heads_per_group
+        self.q_ranges = [partition_units(bpc, self.replicas, r) for r in range(self.replicas)]
+        self.q_begin, self.q_count = self.q_ranges[self.replica]
+        self.max_q = max(c for _, c in self.q_ranges)
+        self._group_pg = None
+
+    @property
+    def n_local(self) -> int:
+        return self.heads_per_group
+
+    def group_ranks(self, group: int | None = None) -> list[int]:
+        g = self.group if group is None else group
+        return [g * self.replicas + r for r in range(self.replicas)]
+
+    def setup(self) -> None:
+        """Create the per-group process groups (collective: every rank calls it, same order)."""
+        if not is_dist() or self.world == 1 or self.replicas == 1:
+            return
+        for g in range(self.groups):
+            pg = dist.new_group(self.group_ranks(g))
+            if g == self.group:
+                self._group_pg = pg
+
+    def gather_qc(self, qc_full: torch.Tensor) -> torch.Tensor:
+        """qc_full [heads_per_group, bpc, d]: this replica's rows are filled; after the call every
+        row is (all replicas of the group end with identical tensors)."""
+        if self.replicas == 1:
+            return qc_full
+        units, _, d = qc_full.shape
+        send = torch.zeros(units, self.max_q, d, dtype=qc_full.dtype, device=qc_full.device)
+        send[:, : self.q_count] = qc_full[:, self.q_begin: self.q_begin + self.q_count]
+        recv = torch.empty((self.replicas * units,) + tuple(send.shape[1:]), dtype=send.dtype, device=send.device)
+        if is_dist():
+            dist.all_gather_into_tensor(recv, send, group=self._group_pg)
+        else:
+            recv[:] = send
+        recv = recv.view((self.replicas,) + tuple(send.shape))
+        for r, (b, c) in enumerate(self.q_ranges):
+            qc_full[:, b: b + c] = recv[r, :, :c]
+        return qc_full
+
+    def gather_output(self, o_part: torch.Tensor, block_rows: int, out: torch.Tensor | None = None,
+                      async_op: bool = False):
+        """o_part [heads_per_group, q_count * block_rows, d] -> [heads, bpc * block_rows, d] on every
+        rank (all-gather of the padded shards).  async_op=True returns (work, finish)."""
+        units, _, d = o_part.shape
+        mrows = self.max_q * block_rows
+        send = o_part
+        if o_part.shape[1] != mrows:
+            send = torch.zeros(units, mrows, d, dtype=o_part.dtype, device=o_part.device)
+            send[:, : o_part.shape[1]] = o_part
+        flat = torch.empty((self.world * units, mrows, d), dtype=o_part.dtype, device=o_part.device)
+        recv = flat.view(self.world, units, mrows, d)
+        if out is None:
+            out = torch.empty(self.heads, self.bpc * block_rows, d, dtype=o_part.dtype, device=o_part.device)
+
+        def finish():
+            for src in range(self.world):
+                g, r = divmod(src, self.replicas)
+                b, c = self.q_ranges[r]
+                h0 = g * self.heads_per_group
+                out[h0: h0 + units, b * block_rows: (b + c) * block_rows] = recv[src, :, : c * block_rows]
+            return out
+
+        if not is_dist() or self.world == 1:
+            recv[0] = send
+            return finish() if not async_op else (_Done(), finish)
+        work = dist.all_gather_into_tensor(flat, send.contiguous(), async_op=async_op)
+        if async_op:
+            return work, finish
+        return finish()

@@ -47,6 +47,16 @@ def _need(t: torch.Tensor, dtype, name: str) -> None:
         raise PbsaError(f"{name} must be contiguous")
 
 
+def _out(out: torch.Tensor | None, like: torch.Tensor, name: str = "out") -> torch.Tensor:
+    """A caller-supplied output must match the input it stands for exactly (the kernels write it
+    unchecked)."""
+    if out is None:
+        return torch.empty_like(like)
+    if out.device != like.device or out.dtype != like.dtype or out.shape != like.shape or not out.is_contiguous():
+        raise PbsaError(f"{name} must be a contiguous {like.dtype} tensor of shape {tuple(like.shape)} on {like.device}")
+    return out
+
+
 def attention_scale(d: int) -> float:
     """AttentionConfig.scale = d^-1/2, rounded to fp32 like the oracle."""
     return float(torch.tensor(1.0 / math.sqrt(d), dtype=torch.float32))
@@ -109,13 +119,14 @@ def attention_sparse(q: torch.Tensor, k_pool: torch.Tensor, v_pool: torch.Tensor
                      dense_slots: torch.Tensor | None, local_slots: torch.Tensor | None,
                      sel: torch.Tensor | None, b: int, scale: float | None = None,
                      n_dense: int | None = None, n_local: int | None = None,
-                     want_lse: bool = False, stream_k: bool = True):
+                     want_lse: bool = False, stream_k: bool = True, validate: bool = True):
     """Block-sparse attention forward.
 
     q [units, nqb*b, d] bf16 (query tokens block-major); k_pool / v_pool [units, n_slots, 64, d]
     bf16 with rows >= b zero; dense_slots [units, >=n_dense] int32 (persistent + current chunk,
     visible to every query block); local_slots [units, >=n_local] int32; sel [units, nqb, k]
-    int32 ascending local indices.  Returns o [units, nqb*b, d] bf16 (and lse [units, nqb*b])."""
+    int32 ascending local indices.  Returns o [units, nqb*b, d] bf16 (and lse [units, nqb*b]).
+    validate: check every slot / selection index is in range first (one host sync)."""
     _need(q, torch.bfloat16, "q")
     _need(k_pool, torch.bfloat16, "k_pool")
     _need(v_pool, torch.bfloat16, "v_pool")
@@ -132,6 +143,21 @@ def attention_sparse(q: torch.Tensor, k_pool: torch.Tensor, v_pool: torch.Tensor
     for name, t in (("dense_slots", dense_slots), ("local_slots", local_slots), ("sel", sel)):
         if t is not None:
             _need(t, torch.int32, name)
+    if sel is not None and (sel.dim() != 3 or sel.shape[:2] != (units, nqb)):
+        raise PbsaError(f"attention_sparse: sel must be [units, nqb, k] = [{units}, {nqb}, k]")
+    for name, t, n in (("dense_slots", dense_slots, nd), ("local_slots", local_slots, nl)):
+        if t is not None and (t.dim() != 2 or t.shape[0] != units or t.shape[1] < n):
+            raise PbsaError(f"attention_sparse: {name} must be [units, >= {n}]")
+    if validate:  # one host sync: every index in range (the kernel reads them unchecked)
+        bad = []
+        if dense_slots is not None and nd and ((dense_slots[:, :nd] < 0) | (dense_slots[:, :nd] >= n_slots)).any():
+            bad.append("dense_slots out of [0, n_slots)")
+        if local_slots is not None and nl and ((local_slots[:, :nl] < 0) | (local_slots[:, :nl] >= n_slots)).any():
+            bad.append("local_slots out of [0, n_slots)")
+        if sel is not None and k and ((sel < 0) | (sel >= nl)).any():
+            bad.append("sel out of [0, n_local)")
+        if bad:
+            raise PbsaError("attention_sparse: " + "; ".join(bad))
     o = torch.empty_like(q)
     lse = torch.empty(units, nq, device=q.device, dtype=torch.float32) if want_lse else None
     scale = attention_scale(d) if scale is None else scale
@@ -405,11 +431,15 @@ class Memory:
         check(LIB.pbsa_mem_create(C.byref(h), units, capacity_c, window_chunks, blocks_per_chunk,
                                   b, d))
         self._h = h
+        self._host_refs = []  # host tensors of attend_qkv_host calls not yet waited for
         self.units, self.capacity_c, self.window_chunks = units, capacity_c, window_chunks
         self.blocks_per_chunk, self.b, self.d = blocks_per_chunk, b, d
 
     def close(self) -> None:
         if getattr(self, "_h", None) is not None and self._h.value:
+            if self._host_refs:
+                LIB.pbsa_mem_host_sync(self._h)
+                self._host_refs.clear()
             LIB.pbsa_mem_destroy(self._h)
             self._h = None
 
@@ -479,7 +509,7 @@ class Memory:
         _need(q, torch.bfloat16, "q")
         if q.shape != (self.units, self.blocks_per_chunk * self.b, self.d):
             raise PbsaError("attend: q must be [units, blocks_per_chunk*b, d]")
-        o = torch.empty_like(q) if out is None else out
+        o = _out(out, q)
         lse = torch.empty(q.shape[:2], device=q.device, dtype=torch.float32) if want_lse else None
         check(LIB.pbsa_attend(self._h, q.data_ptr(), int(k_top), 0.0 if scale is None else float(scale),
                               int(mode), o.data_ptr(), _ptr(lse), _stream()))
@@ -494,7 +524,7 @@ class Memory:
             _need(t, torch.bfloat16, name)
             if t.shape != shape:
                 raise PbsaError(f"attend_qkv: {name} must be {shape}")
-        o = torch.empty_like(q) if out is None else out
+        o = _out(out, q)
         lse = torch.empty(q.shape[:2], device=q.device, dtype=torch.float32) if want_lse else None
         check(LIB.pbsa_attend_qkv(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), int(k_top),
                                   0.0 if scale is None else float(scale), int(mode), o.data_ptr(),
@@ -519,11 +549,52 @@ class Memory:
         check(LIB.pbsa_attend_qkv_host(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), int(k_top),
                                        0.0 if scale is None else float(scale), int(mode), o.data_ptr(),
                                        _stream()))
+        # the library's copies read q/k/v and write o asynchronously: keep the host blocks alive (and
+        # out of torch's pinned-memory cache) until host_sync() has waited for them
+        self._host_refs.append((q, k, v, o))
         return o
+
+    def attend_part_ingest(self, q_part: torch.Tensor, q_begin: int, k: torch.Tensor, v: torch.Tensor,
+                           qc_full: torch.Tensor) -> None:
+        """Query-split call, step 1 (pbsa_attend_part_ingest): the whole chunk's K/V into the memory
+        (replicated across the ranks sharing these heads) and this rank's query blocks
+        [q_begin, q_begin + q_count) compressed into their rows of qc_full [units, bpc, d] f32."""
+        self._part_check(q_part, q_begin, qc_full)
+        shape = (self.units, self.blocks_per_chunk * self.b, self.d)
+        for name, t in (("k", k), ("v", v)):
+            _need(t, torch.bfloat16, name)
+            if t.shape != shape:
+                raise PbsaError(f"attend_part_ingest: {name} must be the whole chunk {shape}")
+        check(LIB.pbsa_attend_part_ingest(self._h, q_part.data_ptr(), int(q_begin), q_part.shape[1] // self.b,
+                                          k.data_ptr(), v.data_ptr(), qc_full.data_ptr(), _stream()))
+
+    def attend_part(self, q_part: torch.Tensor, q_begin: int, qc_full: torch.Tensor, k_top: int,
+                    mode: int = MODE_DENOISE, scale: float | None = None, out: torch.Tensor | None = None,
+                    want_lse: bool = False):
+        """Query-split call, step 2 (pbsa_attend_part): K2 / K3 (/ K4) for this rank's query blocks.
+        In MODE_CACHE_UPDATE every row of qc_full must hold the gathered representatives."""
+        self._part_check(q_part, q_begin, qc_full)
+        o = _out(out, q_part)
+        lse = torch.empty(q_part.shape[:2], device=q_part.device, dtype=torch.float32) if want_lse else None
+        check(LIB.pbsa_attend_part(self._h, q_part.data_ptr(), int(q_begin), q_part.shape[1] // self.b,
+                                   qc_full.data_ptr(), int(k_top), 0.0 if scale is None else float(scale), int(mode),
+                                   o.data_ptr(), _ptr(lse), _stream()))
+        return (o, lse) if want_lse else o
+
+    def _part_check(self, q_part, q_begin, qc_full):
+        _need(q_part, torch.bfloat16, "q_part")
+        _need(qc_full, torch.float32, "qc_full")
+        if q_part.dim() != 3 or q_part.shape[0] != self.units or q_part.shape[2] != self.d or q_part.shape[1] % self.b:
+            raise PbsaError("attend_part: q_part must be [units, q_count*b, d]")
+        if qc_full.shape != (self.units, self.blocks_per_chunk, self.d):
+            raise PbsaError(f"attend_part: qc_full must be {(self.units, self.blocks_per_chunk, self.d)}")
+        if q_begin < 0 or q_begin + q_part.shape[1] // self.b > self.blocks_per_chunk:
+            raise PbsaError("attend_part: query range outside the chunk")
 
     def host_sync(self) -> None:
         """Wait for every upload / download issued by attend_qkv_host."""
         check(LIB.pbsa_mem_host_sync(self._h))
+        self._host_refs.clear()
 
     def attend_latent(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, block_shape, k_top: int,
                       mode: int = MODE_DENOISE, scale: float | None = None, out: torch.Tensor | None = None,
@@ -538,7 +609,7 @@ class Memory:
             _need(t, torch.bfloat16, name)
             if t.shape != q.shape:
                 raise PbsaError(f"attend_latent: {name} must have q's shape {tuple(q.shape)}")
-        o = torch.empty_like(q) if out is None else out
+        o = _out(out, q)
         lse = torch.empty(self.units, self.blocks_per_chunk * self.b, device=q.device,
                           dtype=torch.float32) if want_lse else None
         check(LIB.pbsa_attend_latent(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), C.byref(geom),
@@ -570,7 +641,9 @@ class Memory:
     def last_selection(self):
         sel, k, st, nk = C.c_void_p(), C.c_int(), C.c_void_p(), C.c_int()
         check(LIB.pbsa_last_selection(self._h, C.byref(sel), C.byref(k), C.byref(st), C.byref(nk)))
-        selt = self._view(sel.value, (self.units, self.blocks_per_chunk, max(k.value, 0)), torch.int32) \
+        rows = C.c_int()
+        check(LIB.pbsa_last_selection_rows(self._h, C.byref(rows)))
+        selt = self._view(sel.value, (self.units, rows.value or self.blocks_per_chunk, max(k.value, 0)), torch.int32) \
             if k.value else None
         stt = self._view(st.value, (self.units, nk.value), torch.float32) if nk.value else None
         return selt, stt

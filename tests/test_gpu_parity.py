@@ -563,3 +563,66 @@ def test_launch_counter_per_call(pb):
     torch.cuda.synchronize()
     assert (n1 - n0, n2 - n1) == (4, 6)
     mem.close()
+
+
+# ------------------------------------------------------------------ query-split multi-GPU layout
+@pytest.mark.parametrize("replicas", [2, 3])
+def test_query_split_replicas_commit_identical_memory(pb, replicas):
+    """SURVEY 8(e) batch-1 layout simulated on one GPU: R replicas of the same heads, each attending
+    its range of query blocks (pbsa_attend_part_ingest / pbsa_attend_part), Q^c gathered between
+    them at the k=0 pass.  Every replica must commit the identical P / L ids and s_t, its Top-K rows
+    must equal the full-chunk call's, and the stitched outputs must pass the oracle replay."""
+    from paper_2604_21221_b200.parallel import QuerySplitLayout
+    U, C, W, bpc, b, d, k_top = 3, 12, 2, 7, 60, 128, 3
+    ranges = [partition_units_(bpc, replicas, r) for r in range(replicas)]
+    lay = QuerySplitLayout(12, bpc, 8, 1)  # the config-2 N=8 layout: 4 groups of 3 heads, 2 replicas
+    assert (lay.groups, lay.replicas, lay.n_local) == (4, 2, 3)
+    full = pb.Memory(U, C, W, bpc, b, d)
+    parts = [pb.Memory(U, C, W, bpc, b, d) for _ in range(replicas)]
+    rep = OracleReplay(U, C, W, bpc, b, d)
+    for c in range(7):
+        for step in range(3):
+            update = step == 2
+            mode = pb.MODE_CACHE_UPDATE if update else pb.MODE_DENOISE
+            base = 900 + c * 17 + step
+            q = normal_bf16(base, (U, bpc * b, d))
+            kc = normal_bf16(base + 7, (U, bpc * b, d))
+            vc = normal_bf16(base + 13, (U, bpc * b, d))
+            o_full = full.attend_qkv(dev(q), dev(kc), dev(vc), k_top, mode)
+            sel_full, st_full = full.last_selection()
+            qcs = [torch.zeros(U, bpc, d, device="cuda") for _ in range(replicas)]
+            q_parts = [dev(q.reshape(U, bpc, b, d)[:, qb:qb + qn].reshape(U, qn * b, d)) for qb, qn in ranges]
+            for r, (qb, qn) in enumerate(ranges):
+                parts[r].attend_part_ingest(q_parts[r], qb, dev(kc), dev(vc), qcs[r])
+            if update:  # the group all-gather of Q^c, by hand
+                for r, (qb, qn) in enumerate(ranges):
+                    for r2 in range(replicas):
+                        qcs[r2][:, qb:qb + qn] = qcs[r][:, qb:qb + qn]
+            o = torch.empty(U, bpc * b, d, dtype=torch.bfloat16, device="cuda")
+            for r, (qb, qn) in enumerate(ranges):
+                o[:, qb * b:(qb + qn) * b] = parts[r].attend_part(q_parts[r], qb, qcs[r], k_top, mode)
+                sel_r, st_r = parts[r].last_selection()
+                if sel_full is not None:
+                    want = sel_full[:, qb:qb + qn] if not update else sel_full
+                    assert torch.equal(sel_r, want), f"chunk {c} step {step} replica {r}: Top-K rows"
+                if update:
+                    assert torch.equal(st_r, st_full), f"chunk {c} replica {r}: s_t"
+            torch.cuda.synchronize()
+            rep.call(q, kc, vc, k_top, update, o=o.float().cpu().numpy(),
+                     sel=None if sel_full is None else sel_full.cpu().numpy(),
+                     s_t=None if st_full is None else st_full.cpu().numpy(), where=f"chunk {c} step {step}")
+            # the stitched query-split output against the full-chunk call (same kernel, different
+            # stream-K splits: bf16-rounding-level differences at most)
+            assert (o.float() - o_full.float()).abs().max().item() <= 1e-2
+        gp, gl = full.assemble()
+        rep.check_ids(gp.cpu().numpy(), gl.cpu().numpy(), where=f"chunk {c}")
+        for r in range(replicas):
+            pp, pl = parts[r].assemble()
+            assert torch.equal(pp, gp) and torch.equal(pl, gl), f"chunk {c} replica {r}: P / L ids"
+    for m in [full] + parts:
+        m.close()
+
+
+def partition_units_(total, world, rank):
+    from paper_2604_21221_b200.parallel import partition_units
+    return partition_units(total, world, rank)

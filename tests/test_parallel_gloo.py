@@ -114,3 +114,100 @@ def test_gloo_head_exchange(world, batch, heads):
     for rank, my_batch, full, full2 in out:
         want = [float(e * heads + h) for e in my_batch for h in range(heads)]
         assert full == want and full2 == want
+
+
+# ------------------------------------------------------------------ batch-1 query-split layout
+def test_query_split_layout_partition():
+    from paper_2604_21221_b200.parallel import QuerySplitLayout
+    for world, groups, replicas in [(1, 1, 1), (2, 2, 1), (4, 4, 1), (8, 4, 2), (3, 3, 1), (5, 1, 5), (16, 4, 4)]:
+        lays = [QuerySplitLayout(12, 78, world, r) for r in range(world)]
+        assert (lays[0].groups, lays[0].replicas) == (groups, replicas)
+        # every (head, query block) pair is attended exactly once
+        seen = {}
+        for lay in lays:
+            for h in range(lay.head0, lay.head0 + lay.n_local):
+                for qb in range(lay.q_begin, lay.q_begin + lay.q_count):
+                    seen[(h, qb)] = seen.get((h, qb), 0) + 1
+        assert len(seen) == 12 * 78 and set(seen.values()) == {1}
+        # replicas of a group hold the same heads
+        for lay in lays:
+            assert all(lays[r].head0 == lay.head0 for r in lay.group_ranks())
+    with pytest.raises(ValueError):
+        QuerySplitLayout(12, 1, 8, 0)  # 1 query block cannot be split over 2 replicas
+
+
+def _qs_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2604_21221_b200.parallel import QuerySplitLayout
+        heads, bpc, b, d = 12, 7, 2, 4
+        lay = QuerySplitLayout(heads, bpc, world, rank)
+        lay.setup()
+        # Q^c: this replica fills only its rows; after the gather every replica of the group holds
+        # the group's full, identical Q^c (value = 1000 * head + block)
+        qc = torch.full((lay.n_local, bpc, d), -1.0)
+        for i in range(lay.n_local):
+            for qb in range(lay.q_begin, lay.q_begin + lay.q_count):
+                qc[i, qb] = 1000.0 * (lay.head0 + i) + qb
+        lay.gather_qc(qc)
+        want_qc = torch.tensor([[1000.0 * (lay.head0 + i) + qb for qb in range(bpc)] for i in range(lay.n_local)])
+        ok_qc = torch.equal(qc[:, :, 0], want_qc) and bool((qc == qc[:, :, :1]).all())
+        # O: every rank ends with all heads x all query rows
+        o_part = torch.zeros(lay.n_local, lay.q_count * b, d)
+        for i in range(lay.n_local):
+            for r in range(lay.q_count * b):
+                o_part[i, r] = 1000.0 * (lay.head0 + i) + lay.q_begin * b + r
+        full = lay.gather_output(o_part, b)
+        want = torch.tensor([[1000.0 * h + r for r in range(bpc * b)] for h in range(heads)])
+        q.put((rank, ok_qc, torch.equal(full[:, :, 0], want)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_gloo_query_split_gathers(world):
+    """world 2 (R = 1: two groups of 6 heads) and world 4 (gcd(4, 12) = 4 groups, R = 1) run the
+    output all-gather; a world-8-like replica split is exercised with world 2 over 1 head group
+    below."""
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_qs_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok_qc and ok_o for _, ok_qc, ok_o in res), res
+
+
+def _qs_replica_worker(rank, world, port, q):
+    """heads = 1: one group replicated on every rank (R = world), query blocks split 7 -> 4 + 3."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2604_21221_b200.parallel import QuerySplitLayout
+        lay = QuerySplitLayout(1, 7, world, rank)
+        lay.setup()
+        qc = torch.full((1, 7, 3), -1.0)
+        qc[:, lay.q_begin:lay.q_begin + lay.q_count] = torch.arange(lay.q_begin, lay.q_begin + lay.q_count,
+                                                                   dtype=torch.float32).view(1, -1, 1)
+        lay.gather_qc(qc)
+        q.put((rank, lay.replicas, qc[0, :, 0].tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_query_split_replicas_gather_identical_qc():
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_qs_replica_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert [r[1] for r in res] == [2, 2]
+    assert res[0][2] == res[1][2] == [float(i) for i in range(7)]
