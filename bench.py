@@ -170,7 +170,7 @@ def run_reference(args, rank, world):
     line = {"metric": METRIC, "value": val, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": chunk_s * 1e3, "chunk_latency_ms": chunk_s * 1e3,
             "chunk_latency_kind": "extrapolated from the timed per-head chunk sample to 12 heads x 78 query blocks",
-            "sample_ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+            "sample_ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f32 (fp64 accumulation)", "data": "synthetic N(0,1)",
             "config": cfg, "impl": "reference",
             "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": cores, "kind": "port", "sample": desc,
