@@ -63,10 +63,11 @@ build/ref/test_ref_headers: tests/cpp/test_ref_headers.cpp $(CPPHDR) $(LIB)
 # K3 handshake-timeline build (tools/k3_timeline.py; perf experiments only)
 trace-lib: build/trace/libpbsa_b200.so
 
-build/trace/libpbsa_b200.so: $(PKG)/csrc/bsa_fwd.cu $(PKG)/csrc/bsa_bwd.cu $(HDR) $(OBJ)
+TRACED := bsa_fwd bsa_bwd
+build/trace/libpbsa_b200.so: $(foreach f,$(TRACED),$(PKG)/csrc/$(f).cu) $(HDR) $(OBJ)
 	@mkdir -p build/trace
-	$(NVCC) $(NVFLAGS) -DPBSA_K3_TRACE -ccbin $(HOSTCXX) -c $(PKG)/csrc/bsa_fwd.cu -o build/trace/bsa_fwd.o 2> build/trace/ptxas.txt || (cat build/trace/ptxas.txt; false)
-	$(NVCC) $(NVFLAGS) -DPBSA_K3_TRACE -ccbin $(HOSTCXX) -c $(PKG)/csrc/bsa_bwd.cu -o build/trace/bsa_bwd.o 2>> build/trace/ptxas.txt || (cat build/trace/ptxas.txt; false)
-	$(NVCC) $(ARCH) -ccbin $(HOSTCXX) -shared -o $@ build/trace/bsa_fwd.o build/trace/bsa_bwd.o $(filter-out build/obj/bsa_fwd.o build/obj/bsa_bwd.o,$(OBJ))
+	@rm -f build/trace/ptxas.txt
+	for f in $(TRACED); do $(NVCC) $(NVFLAGS) -DPBSA_K3_TRACE -ccbin $(HOSTCXX) -c $(PKG)/csrc/$$f.cu -o build/trace/$$f.o 2>> build/trace/ptxas.txt || exit 1; done
+	$(NVCC) $(ARCH) -ccbin $(HOSTCXX) -shared -o $@ $(foreach f,$(TRACED),build/trace/$(f).o) $(filter-out $(foreach f,$(TRACED),build/obj/$(f).o),$(OBJ))
 
 .PHONY: trace-lib

@@ -36,6 +36,7 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include "bsa_common.cuh"
 #include "internal.h"
 #include "ptx.cuh"
 
@@ -43,55 +44,6 @@ namespace pbsa {
 namespace {
 
 constexpr int kThreads = 192;
-constexpr int kRing = 2;  // partial-output slots per CTA (stream-K tail: first and last fragment)
-constexpr uint32_t kTmemCols = 256;
-// a block whose row sum (against the running max) exceeds this takes the exact rescale path
-constexpr float kOverflowSum = 65536.0f;
-// column pairs whose exp2 runs as a polynomial on the FMA pipe instead of MUFU (bit c2 = pair c2)
-constexpr uint32_t kPolyMask = 0u;  // MUFU-only: the softmax is issue/latency-bound, not MUFU-bound
-
-struct BsaParams {
-    int units, nqb, b, n_slots;
-    const int32_t* dense;
-    int dense_stride, n_dense;
-    const int32_t* local;
-    int local_stride, n_local;
-    const int32_t* sel;
-    int k;
-    int sel_rows, sel_row0;  // sel is [units][sel_rows][k]; query block i of the launch reads row sel_row0 + i
-    bf16* o;
-    float* lse;
-    float scale_log2;
-    int max_list, bm_words;
-    int lat;        // q / o are chunk latents (LatentGeom lg), not block-major [units][n_q][d]
-    LatentGeom lg;
-    long long* trace;  // perf experiments only: per-event clock64 stamps of CTA 0 (null = off)
-    int ablate;  // perf experiments only (PBSA_ABLATE): 1 no softmax math, 2 no K/V loads, 3 no MMAs
-    // schedule: `whole_waves` rounds of one whole tile per CTA (tile = cta + w * grid), then the
-    // remaining tiles [tail_base, n_tiles) split stream-K over the first tail_grid CTAs
-    int tiles_per_unit, n_tiles, grid;
-    int whole_waves, tail_base, tail_grid;
-    int64_t vlen, vtotal;  // virtual length of one tile (upper bound of its list) and of the tail
-    float* part_o;         // [kRing*grid][128][D] fp32 (null -> whole tiles only)
-    float* part_ml;        // [kRing*grid][2][128]
-    int* counters;         // [n_tiles], zero between launches
-    // unit-gang schedule (gangs > 0): CTA c = gang c / tiles_per_unit, member c % tiles_per_unit;
-    // gang g takes units g, g + gangs, ... one whole tile per member per unit, and the members'
-    // producers pass a barrier (gang_ctr[g]) between units so all tiles of a unit stream its pool
-    // together (the KV blocks they share are fetched from DRAM once and served from L2)
-    int gangs;
-    int* gang_ctr;         // [gangs] + done counter at [kMaxGangs], zero between launches
-};
-constexpr int kMaxGangs = 1024;
-
-struct FragMeta {
-    int tile, u, qb0, has2;
-    int n, e0, e1;   // list length and the entry range of this fragment
-    int whole, nf, slot;
-    int first_cta;   // first CTA holding a fragment of this tile (for the merge)
-    int pad;
-};
-
 template <int D, int NSK, int NSV>
 struct Layout {
     static constexpr int kHalves = D / 64;
@@ -121,25 +73,6 @@ __device__ __forceinline__ void stamp(const BsaParams& p, int ev, int j) {
 #else
     (void)p; (void)ev; (void)j;
 #endif
-}
-
-// CTA holding virtual position x (stream-K ranges B_c = floor(c * W / G))
-__device__ __forceinline__ int cta_of(int64_t x, int64_t W, int G) {
-    return static_cast<int>(((x + 1) * G - 1) / W);
-}
-__device__ __forceinline__ int64_t range_begin(int c, int64_t W, int G) { return (static_cast<int64_t>(c) * W) / G; }
-
-// number of fragments this CTA processes
-__device__ __forceinline__ int num_fragments(const BsaParams& p, int c) {
-    if (p.gangs > 0) {
-        const int g = c / p.tiles_per_unit;
-        return g < p.units ? (p.units - 1 - g) / p.gangs + 1 : 0;
-    }
-    if (p.part_o == nullptr) return c < p.n_tiles ? (p.n_tiles - 1 - c) / p.grid + 1 : 0;
-    if (c >= p.tail_grid || p.vtotal == 0) return p.whole_waves;
-    const int64_t a = range_begin(c, p.vtotal, p.tail_grid), b = range_begin(c + 1, p.vtotal, p.tail_grid);
-    if (b <= a) return p.whole_waves;
-    return p.whole_waves + static_cast<int>((b - 1) / p.vlen - a / p.vlen) + 1;
 }
 
 template <int D, int NSK, int NSV, int B, uint32_t POLY, bool L16>
@@ -174,15 +107,6 @@ __global__ void __launch_bounds__(kThreads, 2)
     constexpr int esz = L16 ? 2 : 4;
     constexpr int mshift = L16 ? 14 : 24;
     uint32_t* bm = reinterpret_cast<uint32_t*>(lists + ((2 * static_cast<size_t>(p.max_list) * esz + 15) & ~size_t(15)));
-    auto list_put = [&](uint8_t* base, int i, int slot, int mask) {
-        if (L16) reinterpret_cast<uint16_t*>(base)[i] = static_cast<uint16_t>(slot | (mask << 14));
-        else reinterpret_cast<int32_t*>(base)[i] = slot | (mask << 24);
-    };
-    auto list_slot = [&](const uint8_t* base, int i) {
-        return L16 ? static_cast<int>(reinterpret_cast<const uint16_t*>(base)[i] & 0x3FFF)
-                        : (reinterpret_cast<const int32_t*>(base)[i] & 0xFFFFFF);
-    };
-
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int cta = blockIdx.x;
     const int n_frag = num_fragments(p, cta);
@@ -239,95 +163,17 @@ __global__ void __launch_bounds__(kThreads, 2)
         {
             // The producer also builds each fragment's visible list (double-buffered): list f+1 is
             // built while the MMA / softmax warps still work on the last blocks of fragment f.
-            const bool in_tail = p.part_o != nullptr && cta < p.tail_grid;
-            const int64_t my_begin = in_tail ? range_begin(cta, p.vtotal, p.tail_grid) : 0;
-            const int64_t my_end = in_tail ? range_begin(cta + 1, p.vtotal, p.tail_grid) : 0;
-            const int my_first_tile = p.tail_base + static_cast<int>(my_begin / p.vlen);  // first tail tile
             int jg = 0, q_uses = 0;
             for (int f = 0; f < n_frag; ++f) {
                 const int lb = f & 1;
                 mbar_wait(list_empty + lb, ((f >> 1) & 1) ^ 1);
                 uint8_t* list = lists + static_cast<size_t>(lb) * p.max_list * esz;
                 // ---------------------------------------------------------- fragment schedule
-                const bool tail_frag = p.gangs == 0 && p.part_o != nullptr && f >= p.whole_waves;
-                int tile = tail_frag ? my_first_tile + (f - p.whole_waves) : cta + f * p.grid;
-                if (p.gangs > 0) {
-                    const int g = cta / p.tiles_per_unit;
-                    tile = (g + f * p.gangs) * p.tiles_per_unit + cta % p.tiles_per_unit;
-                    // every member of the gang has issued all loads of the previous unit
-                    if (f > 0 && lane == 0) {
-                        const int want = f * p.tiles_per_unit;
-                        while (ld_acquire_gpu(p.gang_ctr + g) < want) __nanosleep(64);
-                    }
-                    __syncwarp();
-                }
-                const int u = tile / p.tiles_per_unit;
-                const int qb0 = 2 * (tile % p.tiles_per_unit);
-                const bool has2 = qb0 + 1 < p.nqb;
-                int64_t va = 0, vb = p.vlen;
-                int nfr = 1, first_cta = cta;
-                if (tail_frag) {
-                    const int64_t t0 = static_cast<int64_t>(tile - p.tail_base) * p.vlen;
-                    va = (my_begin > t0 ? my_begin : t0) - t0;
-                    vb = (my_end < t0 + p.vlen ? my_end : t0 + p.vlen) - t0;
-                    first_cta = cta_of(t0, p.vtotal, p.tail_grid);
-                    nfr = cta_of(t0 + p.vlen - 1, p.vtotal, p.tail_grid) - first_cta + 1;
-                }
+                const FragPlan fp = plan_fragment(p, cta, f);
+                gang_wait(p, cta, f);  // unit gangs: every member has issued the previous unit's loads
                 // ---------------------------------------------------------- visible list of the tile
-                // dense blocks first (both halves), then the union of the two Top-K selections in
-                // ascending local order with a 2-bit visibility mask in bits 24-25
-                for (int w = lane; w < 2 * p.bm_words; w += 32) bm[w] = 0u;
-                __syncwarp();
-                if (p.k > 0 && p.n_local > 0) {
-                    const int sel_rows = has2 ? 2 : 1;
-                    for (int e = lane; e < sel_rows * p.k; e += 32) {
-                        const int rw = e / p.k, c = e % p.k;
-                        const int idx = __ldg(p.sel + (static_cast<int64_t>(u) * p.sel_rows + p.sel_row0 + qb0 + rw) * p.k + c);
-                        atomicOr(&bm[rw * p.bm_words + (idx >> 5)], 1u << (idx & 31));
-                    }
-                }
-                for (int e = lane; e < p.n_dense; e += 32)
-                    list_put(list, e, __ldg(p.dense + static_cast<int64_t>(u) * p.dense_stride + e), 3);
-                __syncwarp();
-                int run = p.n_dense;
-                {
-                    const int32_t* loc = p.local + static_cast<int64_t>(u) * p.local_stride;
-                    for (int w0 = 0; w0 < p.bm_words; w0 += 32) {
-                        const int w = w0 + lane;
-                        const uint32_t a = w < p.bm_words ? bm[w] : 0u;
-                        const uint32_t c = w < p.bm_words ? bm[p.bm_words + w] : 0u;
-                        uint32_t un = a | c;
-                        const int cnt = __popc(un);
-                        int incl = cnt;
-#pragma unroll
-                        for (int o = 1; o < 32; o <<= 1) {
-                            const int y = __shfl_up_sync(0xffffffffu, incl, o);
-                            if (lane >= o) incl += y;
-                        }
-                        int pos = run + incl - cnt;
-                        while (un) {
-                            const int bit = __ffs(un) - 1;
-                            un &= un - 1;
-                            const int idx = w * 32 + bit;
-                            const int mask = static_cast<int>((a >> bit) & 1u) | (static_cast<int>((c >> bit) & 1u) << 1);
-                            list_put(list, pos++, __ldg(loc + idx), mask);
-                        }
-                        run += __shfl_sync(0xffffffffu, incl, 31);
-                    }
-                }
-                FragMeta fm;
-                fm.tile = tile;
-                fm.u = u;
-                fm.qb0 = qb0;
-                fm.has2 = has2;
-                fm.n = run;
-                fm.e0 = static_cast<int>((va * run) / p.vlen);
-                fm.e1 = static_cast<int>((vb * run) / p.vlen);
-                fm.whole = (nfr == 1);
-                fm.nf = nfr;
-                fm.slot = 2 * cta + (tile == my_first_tile ? 0 : 1);
-                fm.first_cta = first_cta;
-                fm.pad = 0;
+                const int run = build_visible_list<L16>(p, fp, list, bm);
+                const FragMeta fm = make_meta(p, fp, run);
                 if (lane == 0) meta[lb] = fm;
                 __syncwarp();
                 if (lane == 0) mbar_arrive(list_full + lb);
@@ -357,7 +203,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                         const int j = jg + idx;
                         const int s = j % NSV;
                         mbar_wait(v_empty + s, ((j / NSV) & 1) ^ 1);
-                        const int row0 = (fm.u * p.n_slots + list_slot(list, fm.e0 + idx)) * 64;
+                        const int row0 = (fm.u * p.n_slots + list_slot<L16>(list, fm.e0 + idx)) * 64;
                         if (elect_one()) {
                             if (p.ablate == 2) {  // experiment: no K/V traffic
                                 mbar_arrive(v_full + s);
@@ -373,7 +219,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                         const int j = jg + idx;
                         const int s = j % NSK;
                         mbar_wait(k_empty + s, ((j / NSK) & 1) ^ 1);
-                        const int row0 = (fm.u * p.n_slots + list_slot(list, fm.e0 + idx)) * 64;
+                        const int row0 = (fm.u * p.n_slots + list_slot<L16>(list, fm.e0 + idx)) * 64;
                         if (elect_one()) {
                             if (p.ablate == 2) {
                                 mbar_arrive(k_full + s);
@@ -389,7 +235,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                     load_v(nf - 1);
                     jg += nf;
                 }
-                if (p.gangs > 0 && lane == 0) red_release_gpu_add(p.gang_ctr + cta / p.tiles_per_unit, 1);
+                gang_arrive(p, cta);
             }
         }
     } else if (warp == 1) {
@@ -759,42 +605,11 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
 }
 
-int num_sms() {
-    static int n = 0;
-    if (n == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
-    }
-    return n;
-}
-
 template <int D, int NSK, int NSV, int B, uint32_t POLY, bool L16>
 int launch_impl(const bf16* q, const bf16* kp, const bf16* vp, BsaParams p, cudaStream_t s) {
     using L = Layout<D, NSK, NSV>;
     alignas(64) CUtensorMap tq, tk, tv;
-    std::string err;
-    if (p.lat) {
-        if (!encode_latent_tmap(&tq, q, p.lg, 64, true, &err))
-            return set_error(PBSA_ECUDA, "tensor map Q (latent): " + err);
-    } else {
-        const uint64_t dims[3] = {static_cast<uint64_t>(D), static_cast<uint64_t>(p.b),
-                                  static_cast<uint64_t>(p.units) * p.nqb};
-        const uint64_t strides[2] = {static_cast<uint64_t>(D) * 2, static_cast<uint64_t>(p.b) * D * 2};
-        const uint32_t box[3] = {64, static_cast<uint32_t>(p.b), 1};
-        if (!encode_tmap_bf16(&tq, q, 3, dims, strides, box, &err))
-            return set_error(PBSA_ECUDA, "tensor map Q: " + err);
-    }
-    {
-        const uint64_t dims[2] = {static_cast<uint64_t>(D), static_cast<uint64_t>(p.units) * p.n_slots * 64};
-        const uint64_t strides[1] = {static_cast<uint64_t>(D) * 2};
-        const uint32_t box[2] = {64, 64};
-        if (!encode_tmap_bf16(&tk, kp, 2, dims, strides, box, &err))
-            return set_error(PBSA_ECUDA, "tensor map K: " + err);
-        if (!encode_tmap_bf16(&tv, vp, 2, dims, strides, box, &err))
-            return set_error(PBSA_ECUDA, "tensor map V: " + err);
-    }
+    if (int rc = encode_k3_maps(q, kp, vp, p, D, &tq, &tk, &tv)) return rc;
     const size_t smem = L::bytes(p.max_list, p.bm_words, L16 ? 2 : 4);
     if (smem > 227 * 1024)
         return set_error(PBSA_EUNSUPPORTED, "bsa_fwd: visible list too long for shared memory");
@@ -811,51 +626,8 @@ int launch_impl(const bf16* q, const bf16* kp, const bf16* vp, BsaParams p, cuda
         if (sm_smem > 0 && 2 * (smem + static_cast<size_t>(reserved)) > static_cast<size_t>(sm_smem)) per_sm = 1;
     }
     const int slots = per_sm * num_sms();
-    p.grid = p.n_tiles < slots ? p.n_tiles : slots;
-    p.whole_waves = 0;
-    p.tail_base = 0;
-    p.tail_grid = 0;
-    p.vtotal = 0;
-    p.gangs = 0;
-    if (p.gang_ctr != nullptr) {
-        // unit-gang schedule: many whole-tile waves over a slot pool far larger than L2 (config 5:
-        // 12480 tiles, 65 GB) -- tiles of one unit run together so the blocks they share come from
-        // DRAM once.  PBSA_K3_GANG=0/1 forces it off / on (experiments, tests).
-        const char* env = getenv("PBSA_K3_GANG");
-        const int force = env ? atoi(env) : -1;
-        const int gangs = slots / p.tiles_per_unit;
-        const double pool = static_cast<double>(p.units) * p.n_slots * 64 * D * 2 * 2;
-        const bool want = force >= 0 ? force > 0 : (p.n_tiles >= 4 * slots && pool > 4.0 * 126e6);
-        if (want && gangs >= 1 && gangs <= kMaxGangs) {
-            p.gangs = gangs < p.units ? gangs : p.units;
-            p.grid = p.gangs * p.tiles_per_unit;
-            p.part_o = nullptr;
-        }
-    }
-    if (p.part_o != nullptr) {
-        p.grid = slots;
-        p.whole_waves = p.n_tiles / slots;
-        p.tail_base = p.whole_waves * slots;
-        const int64_t tail = p.n_tiles - p.tail_base;
-        p.vtotal = tail * p.vlen;
-        // at most ~4 CTAs share a tail tile (the merge handles up to 8 fragments)
-        int64_t g = slots;
-        if (g > p.vtotal) g = p.vtotal;
-        if (g > 4 * tail) g = 4 * tail;
-        p.tail_grid = static_cast<int>(g);
-        if (p.whole_waves == 0) p.grid = p.tail_grid;
-    }
-    {
-        pbsa_bsa_plan& pl = last_bsa_plan();
-        pl.list_entry_bytes = L16 ? 2 : 4;
-        pl.ctas_per_sm = per_sm;
-        pl.grid = p.grid > 0 ? p.grid : 0;
-        pl.schedule = p.gangs > 0 ? PBSA_SCHED_UNIT_GANGS : (p.part_o != nullptr ? PBSA_SCHED_STREAM_K : PBSA_SCHED_WHOLE_TILES);
-        pl.gangs = p.gangs;
-        pl.max_list = p.max_list;
-        pl.n_tiles = p.n_tiles;
-        pl.smem_bytes = smem;
-    }
+    plan_schedule(p, slots, D);
+    record_plan(p, L16, per_sm, smem);
     if (p.grid <= 0) return 0;
     if (launch_pdl(bsa_fwd_kernel<D, NSK, NSV, B, POLY, L16>, dim3(p.grid), dim3(kThreads), smem, s, tq, tk, tv, p) !=
         cudaSuccess)

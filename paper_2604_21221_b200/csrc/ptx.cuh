@@ -292,11 +292,11 @@ __device__ __forceinline__ float exp2_approx(float x) {
 // softmax's binding unit at d = 128): Cody-Waite split x = i + f, f in [-1/2, 1/2] by the
 // 1.5*2^23 rounding trick, 2^f by a degree-3 minimax polynomial (max rel. error 7.5e-5, far
 // below the bf16 rounding of P), 2^i added into the exponent field.  x is clamped at -120 so the
-// exponent never underflows (2^-120 is zero against any row sum >= 1).
+// exponent never underflows (2^-120 is zero against any row sum >= 1), and at 64 so it never wraps.
 __device__ __forceinline__ float2 exp2_poly2(float2 x) {
     constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
-    x.x = fmaxf(x.x, -120.0f);
-    x.y = fmaxf(x.y, -120.0f);
+    x.x = fmaxf(fminf(x.x, 64.0f), -120.0f);  // above 2^64 the caller's overflow check fires anyway
+    x.y = fmaxf(fminf(x.y, 64.0f), -120.0f);
     const float2 t = __fadd2_rn(x, make_float2(kMagic, kMagic));
     const float2 fi = __fadd2_rn(t, make_float2(-kMagic, -kMagic));
     const float2 f = __ffma2_rn(fi, make_float2(-1.0f, -1.0f), x);

@@ -231,6 +231,14 @@ def test_bsa_fwd_parity(pb, d, b, stream_k):
     _bsa_case(pb, 2, 5, b, d, 6, 16, 4, seed=d + b, stream_k=stream_k)
 
 
+@pytest.mark.parametrize("units,nqb,n_dense,n_local,k", [(3, 7, 0, 9, 3), (2, 1, 5, 0, 0), (5, 9, 3, 40, 17),
+                                                         (4, 6, 1, 7, 7), (1, 2, 0, 1, 1)])
+def test_bsa_fwd_odd_lists(pb, units, nqb, n_dense, n_local, k):
+    """Odd list lengths, single query blocks, no dense part, k = n_local, n_local = 1."""
+    _bsa_case(pb, units, nqb, 60, 128, n_dense, n_local, k, seed=80 + units + nqb + n_local)
+    _bsa_case(pb, units, nqb, 60, 128, n_dense, n_local, k, seed=90 + units, stream_k=False)
+
+
 def test_bsa_fwd_stream_k_many_tiles(pb):
     """More tiles than CTA slots: whole tiles, split tiles and the partial merge all exercised;
     stream-K and whole-tile schedules must agree."""
