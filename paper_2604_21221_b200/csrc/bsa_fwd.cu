@@ -456,6 +456,9 @@ __global__ void __launch_bounds__(kThreads, 2)
                 __syncwarp();
                 if (lane == 0) stamp(p, 9 + warp, j);  // per-warp arrival (warps 2-5 -> stamps 11-14)
                 if (lane == 0) mbar_arrive(p_full + buf);
+                // every o_done phase gets a waiter (compute-sanitizer synccheck): PV_{j-1} was issued
+                // before S_{j+1}, which this warp waits for next, so this costs nothing
+                pv_done(j - 1);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(list_empty + lb);  // this warp is done with the list

@@ -33,6 +33,41 @@ sel = torch.stack([torch.stack([torch.randperm(nl, device="cuda", generator=g)[:
                                 for _ in range(nqb)]) for _ in range(U)]).int().contiguous()
 o, lse = pb.attention_sparse(q, kp, vp, dense, local, sel, b, want_lse=True)
 grads = pb.attention_sparse_backward(q, kp, vp, dense, local, sel, b, o, lse, do)
+# unit-gang K3 schedule (forced) and a 16-bit-list launch
+os.environ["PBSA_K3_GANG"] = "1"
+pb.attention_sparse(q, kp, vp, dense, local, sel, b)
+del os.environ["PBSA_K3_GANG"]
+# query-split calls (2 replicas of the same heads) and the drop-sink fault path of K4
+parts = [pb.Memory(U, C, W, bpc, b, d) for _ in range(2)]
+qc = [torch.zeros(U, bpc, d, device="cuda") for _ in range(2)]
+for c in range(5):
+    q6, k6, v6 = (torch.randn(U, bpc * b, d, device="cuda", generator=g).bfloat16() for _ in range(3))
+    for mode in (pb.MODE_DENOISE, pb.MODE_CACHE_UPDATE):
+        for r, (qb, qn) in enumerate(((0, 3), (3, 3))):
+            qp = q6.view(U, bpc, b, d)[:, qb:qb + qn].reshape(U, qn * b, d).contiguous()
+            parts[r].attend_part_ingest(qp, qb, k6, v6, qc[r])
+        qc[0][:, 3:] = qc[1][:, 3:]
+        qc[1][:, :3] = qc[0][:, :3]
+        for r, (qb, qn) in enumerate(((0, 3), (3, 3))):
+            qp = q6.view(U, bpc, b, d)[:, qb:qb + qn].reshape(U, qn * b, d).contiguous()
+            parts[r].attend_part(qp, qb, qc[r], 3, mode)
+pb.debug_set_fault("drop-sink")
+for c in range(4):
+    q6, k6, v6 = (torch.randn(U, bpc * b, d, device="cuda", generator=g).bfloat16() for _ in range(3))
+    parts[0].attend_qkv(q6, k6, v6, 3, pb.MODE_CACHE_UPDATE)
+pb.debug_set_fault(None)
+# SPEC-op primitives
+a = torch.randn(37, 129, device="cuda", generator=g)
+bm = torch.randn(129, 41, device="cuda", generator=g)
+pb.matmul(a, bm)
+pb.matmul(a, bm.t().contiguous(), transpose_b=True)
+sm = pb.masked_softmax_rows(a)
+pb.aggregate_scores(sm)
+pb.select_topk(sm, 17)
+lat = torch.randn(3, 30, 52, 8, device="cuda", generator=g)
+pb.unblockify(pb.blockify(lat, (1, 15, 4)), lat.shape, (1, 15, 4))
+pb.topc_select(torch.arange(40, device="cuda"), torch.rand(40, device="cuda", generator=g), 13)
 torch.cuda.synchronize()
 print("sanitize paths ok", mem.status(), [t.shape for t in grads])
-mem.close()
+for m in [mem] + parts:
+    m.close()
