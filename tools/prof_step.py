@@ -37,7 +37,9 @@ while True:  # fill (cheap k = 1 cache updates) until P and L are full
     inf = mem.info()
     if inf.n_p == C and inf.n_l == W * bpc and inf.chunks_committed > W + 2:
         break
-    q, kk, vv = sets[i % 3]
+    # fresh K/V for every filled chunk: a window built from a few repeated chunks would hold
+    # identical key blocks, whose exactly tied scores pull every Top-K towards the oldest copies
+    q, kk, vv = (torch.randn(U, bpc * b, d, device="cuda", generator=g).bfloat16() for _ in range(3))
     mem.attend_qkv(q, kk, vv, 1, pb.MODE_CACHE_UPDATE, out=out)
     i += 1
 for j in range(T + 1):  # one warm chunk step
