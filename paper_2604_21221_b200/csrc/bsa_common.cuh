@@ -171,23 +171,48 @@ __device__ __forceinline__ int list_mask(uint32_t ent) {
 
 template <bool L16>
 __device__ int build_visible_list(const BsaParams& p, const FragPlan& fp, uint8_t* list, uint32_t* bm) {
+    // Global loads are issued 8 per lane ahead of their consumers (the list is built before the
+    // fragment's first TMA can be issued, so a serial load -> store chain here is launch latency).
+    constexpr int kB = 8;
     const int lane = threadIdx.x & 31;
     const int u = fp.u, qb0 = fp.qb0;
     for (int w = lane; w < 2 * p.bm_words; w += 32) bm[w] = 0u;
     __syncwarp();
     if (p.k > 0 && p.n_local > 0) {
-        const int sel_rows = fp.has2 ? 2 : 1;
-        for (int e = lane; e < sel_rows * p.k; e += 32) {
-            const int rw = e / p.k, c = e % p.k;
-            const int idx = __ldg(p.sel + (static_cast<int64_t>(u) * p.sel_rows + p.sel_row0 + qb0 + rw) * p.k + c);
-            atomicOr(&bm[rw * p.bm_words + (idx >> 5)], 1u << (idx & 31));
+        const int sel_rows = fp.has2 ? 2 : 1, total = sel_rows * p.k;
+        const int32_t* srow = p.sel + (static_cast<int64_t>(u) * p.sel_rows + p.sel_row0 + qb0) * p.k;
+        for (int e0 = 0; e0 < total; e0 += 32 * kB) {
+            int idx[kB];
+#pragma unroll
+            for (int i = 0; i < kB; ++i) {
+                const int e = e0 + i * 32 + lane;
+                idx[i] = e < total ? __ldg(srow + e) : -1;  // rows qb0, qb0 + 1 are contiguous in sel
+            }
+#pragma unroll
+            for (int i = 0; i < kB; ++i) {
+                const int e = e0 + i * 32 + lane;
+                if (e < total) atomicOr(&bm[(e >= p.k ? p.bm_words : 0) + (idx[i] >> 5)], 1u << (idx[i] & 31));
+            }
         }
     }
-    for (int e = lane; e < p.n_dense; e += 32)
-        list_put<L16>(list, e, __ldg(p.dense + static_cast<int64_t>(u) * p.dense_stride + e), 3);
+    const int32_t* drow = p.dense + static_cast<int64_t>(u) * p.dense_stride;
+    for (int e0 = 0; e0 < p.n_dense; e0 += 32 * kB) {
+        int v[kB];
+#pragma unroll
+        for (int i = 0; i < kB; ++i) {
+            const int e = e0 + i * 32 + lane;
+            v[i] = e < p.n_dense ? __ldg(drow + e) : 0;
+        }
+#pragma unroll
+        for (int i = 0; i < kB; ++i) {
+            const int e = e0 + i * 32 + lane;
+            if (e < p.n_dense) list_put<L16>(list, e, v[i], 3);
+        }
+    }
     __syncwarp();
+    // union of the two bitmaps in ascending local order: first the local INDICES (a pure
+    // shared-memory pass), then one batched gather of their pool slots
     int run = p.n_dense;
-    const int32_t* loc = p.local + static_cast<int64_t>(u) * p.local_stride;
     for (int w0 = 0; w0 < p.bm_words; w0 += 32) {
         const int w = w0 + lane;
         const uint32_t a = w < p.bm_words ? bm[w] : 0u;
@@ -204,11 +229,31 @@ __device__ int build_visible_list(const BsaParams& p, const FragPlan& fp, uint8_
         while (un) {
             const int bit = __ffs(un) - 1;
             un &= un - 1;
-            const int idx = w * 32 + bit;
             const int mask = static_cast<int>((a >> bit) & 1u) | (static_cast<int>((c >> bit) & 1u) << 1);
-            list_put<L16>(list, pos++, __ldg(loc + idx), mask);
+            list_put<L16>(list, pos++, w * 32 + bit, mask);
         }
         run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    __syncwarp();
+    const int32_t* loc = p.local + static_cast<int64_t>(u) * p.local_stride;
+    for (int e0 = p.n_dense; e0 < run; e0 += 32 * kB) {
+        int v[kB], mk[kB];
+#pragma unroll
+        for (int i = 0; i < kB; ++i) {
+            const int e = e0 + i * 32 + lane;
+            v[i] = 0;
+            mk[i] = 0;
+            if (e < run) {
+                const uint32_t ent = L16 ? reinterpret_cast<const uint16_t*>(list)[e] : reinterpret_cast<const uint32_t*>(list)[e];
+                mk[i] = list_mask<L16>(ent);
+                v[i] = __ldg(loc + static_cast<int>(L16 ? (ent & 0x3FFFu) : (ent & 0xFFFFFFu)));
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < kB; ++i) {
+            const int e = e0 + i * 32 + lane;
+            if (e < run) list_put<L16>(list, e, v[i], mk[i]);
+        }
     }
     __syncwarp();
     return run;
@@ -279,10 +324,11 @@ inline void plan_schedule(BsaParams& p, int slots, int D) {
         p.tail_base = p.whole_waves * slots;
         const int64_t tail = p.n_tiles - p.tail_base;
         p.vtotal = tail * p.vlen;
-        // at most ~4 slots share a tail tile (the merge handles up to 8 fragments)
+        // at most ~cap slots share a tail tile (the merge handles up to 8 fragments)
+        static const int cap = getenv("PBSA_K3_TAILCAP") ? atoi(getenv("PBSA_K3_TAILCAP")) : 4;
         int64_t g = slots;
         if (g > p.vtotal) g = p.vtotal;
-        if (g > 4 * tail) g = 4 * tail;
+        if (g > cap * tail) g = cap * tail;
         p.tail_grid = static_cast<int>(g);
         if (p.whole_waves == 0) p.grid = p.tail_grid;
     }

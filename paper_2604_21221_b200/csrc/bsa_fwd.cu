@@ -17,9 +17,11 @@
 // visible-block index, every tile counted with the upper-bound length V) is cut into equal
 // contiguous ranges, one per tail CTA, so a CTA processes at most two tile FRAGMENTS of the
 // tail.  A fragment writes fp32 partials (unnormalised O, running max m, sum l) to a workspace;
-// the last CTA to finish a split tile (per-tile arrival counter) merges all fragments of that
-// tile in fragment order (deterministic) and writes O.  This removes the 1.58-wave quantisation
-// of one-tile-per-CTA launches at the Wan-1.3B shape (468 tiles on 296 CTA slots).
+// once a CTA has finished all its fragments it waits for the other fragments of each split tile
+// it holds (per-tile arrival counter) and merges ITS SLICE of the tile's rows, in fragment order
+// (deterministic) -- the nf CTAs of a tile merge it in parallel (a single last-arriving merger was
+// a 20-38 us serial tail per launch).  This removes the 1.58-wave quantisation of one-tile-per-CTA
+// launches at the Wan-1.3B shape (468 tiles on 296 CTA slots).
 //
 // Warp roles (192 threads):
 //   warp 0  TMA producer: Q (3-D map over [unit*nqb][b][d], one box per query block and d-half),
@@ -74,6 +76,20 @@ __device__ __forceinline__ void stamp(const BsaParams& p, int ev, int j) {
     (void)p; (void)ev; (void)j;
 #endif
 }
+// per-CTA milestones on the global timer (tools/k3_cta_timeline.py), same build flag:
+// trace[15 * 256 + cta * 8 + ev], ev 0 start / 1 first list built / 2 first S seen / 3 last P
+// arrived / 4 partial written / 5 merge start / 6 merge end / 7 exit (slot 7 also gets the SM id)
+__device__ __forceinline__ void stamp_cta(const BsaParams& p, int ev) {
+#ifdef PBSA_K3_TRACE
+    if (p.trace != nullptr) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.trace[15 * 256 + blockIdx.x * 8 + ev] = static_cast<long long>(t);
+    }
+#else
+    (void)p; (void)ev;
+#endif
+}
 
 template <int D, int NSK, int NSV, int B, uint32_t POLY, bool L16>
 __global__ void __launch_bounds__(kThreads, 2)
@@ -99,7 +115,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     uint64_t* list_full = o_free + 1;
     uint64_t* list_empty = list_full + 2;
     FragMeta* meta = reinterpret_cast<FragMeta*>(smem + L::kOffMeta);
-    uint32_t* misc = reinterpret_cast<uint32_t*>(smem + L::kOffMisc);  // [0] tmem base, [1] merge flag
+    uint32_t* misc = reinterpret_cast<uint32_t*>(smem + L::kOffMisc);  // [0] tmem base
     // visible lists, double-buffered: [2][max_list] entries of 4 bytes (slot | mask << 24) or, when
     // the pool has < 16384 slots, 2 bytes (slot | mask << 14) -- halves the footprint of long lists
     // (config 5: 3238 entries) so two CTAs still fit an SM
@@ -156,6 +172,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     // programmatic dependent launch: everything above (barriers, TMEM, tensor-map prefetch, Q
     // padding) overlapped the previous kernel; its outputs (selections, Q) are visible from here
     pdl_wait();
+    if (threadIdx.x == 0) stamp_cta(p, 0);
 
     if (warp == 0) {
         // ============================================================== TMA producer
@@ -175,6 +192,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 const int run = build_visible_list<L16>(p, fp, list, bm);
                 const FragMeta fm = make_meta(p, fp, run);
                 if (lane == 0) meta[lb] = fm;
+                if (lane == 0 && f == 0) stamp_cta(p, 1);
                 __syncwarp();
                 if (lane == 0) mbar_arrive(list_full + lb);
                 const int nf = fm.e1 - fm.e0;
@@ -330,6 +348,20 @@ __global__ void __launch_bounds__(kThreads, 2)
         constexpr int BB = B > 0 ? B : 64;
         const int bcols = B > 0 ? B : p.b;
         const float2 scl2 = make_float2(p.scale_log2, p.scale_log2);
+        // output row of query block qb, token rr: block-major, or (unblockify fused) the token's
+        // position in the latent
+        auto orow_offset = [&](int u, int qb, int rr_) -> int64_t {
+            const int64_t idx = (static_cast<int64_t>(u) * p.nqb + qb) * p.b + rr_;
+            if (!p.lat) return idx * D;
+            const int e = u / p.lg.heads, hd = u % p.lg.heads;
+            const int nw = qb % p.lg.nw(), nh = (qb / p.lg.nw()) % p.lg.nh(), nt = qb / (p.lg.nw() * p.lg.nh());
+            const int dw = rr_ % p.lg.bw, dh = (rr_ / p.lg.bw) % p.lg.bh, dt = rr_ / (p.lg.bw * p.lg.bh);
+            const int64_t tok = ((static_cast<int64_t>(e) * p.lg.T + nt * p.lg.bt + dt) * p.lg.H + nh * p.lg.bh + dh) *
+                                    p.lg.W + nw * p.lg.bw + dw;
+            return (tok * p.lg.heads + hd) * D;
+        };
+        FragMeta pend[2];  // split-tile fragments of this CTA (stream-K tail: at most two)
+        int npend = 0;
         int jg = 0;
         for (int f = 0; f < n_frag; ++f) {
             const int lb = f & 1;
@@ -350,6 +382,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 if (threadIdx.x == 64) stamp(p, 4, j);  // softmax warp 2 lane 0: waiting for S_j
                 mbar_wait(s_full + buf, (j >> 1) & 1);
                 if (threadIdx.x == 64) stamp(p, 5, j);  // S_j seen
+                if (threadIdx.x == 64 && j == 0) stamp_cta(p, 2);
                 tc_fence_after();
                 const uint32_t t_s = t_o + L::kSColBase + buf * 64;
                 // rows of one warp all lie in one half -> visibility is warp-uniform
@@ -465,20 +498,12 @@ __global__ void __launch_bounds__(kThreads, 2)
             pv_done(jg + nf - 2);
             pv_done(jg + nf - 1);
             tc_fence_after();
+            if (threadIdx.x == 64) stamp_cta(p, 3);
 
             // ---------------------------------------------------------- epilogue
             const int64_t orow_idx = (static_cast<int64_t>(u) * p.nqb + qb) * p.b + rr;
-            // output row: block-major, or (unblockify fused) the token's position in the latent
-            int64_t orow_off = orow_idx * D;
-            if (p.lat) {
-                const int e = u / p.lg.heads, hd = u % p.lg.heads;
-                const int nw = qb % p.lg.nw(), nh = (qb / p.lg.nw()) % p.lg.nh(), nt = qb / (p.lg.nw() * p.lg.nh());
-                const int dw = rr % p.lg.bw, dh = (rr / p.lg.bw) % p.lg.bh, dt = rr / (p.lg.bw * p.lg.bh);
-                const int64_t tok = ((static_cast<int64_t>(e) * p.lg.T + nt * p.lg.bt + dt) * p.lg.H + nh * p.lg.bh + dh) *
-                                        p.lg.W + nw * p.lg.bw + dw;
-                orow_off = (tok * p.lg.heads + hd) * D;
-            }
             if (fm.whole) {
+                const int64_t orow_off = orow_offset(u, qb, rr);
                 const float inv = l > 0.0f ? 1.0f / l : 0.0f;
                 bf16* orow = p.o + orow_off;
 #pragma unroll 1
@@ -533,61 +558,113 @@ __global__ void __launch_bounds__(kThreads, 2)
                 __syncwarp();
                 if (lane == 0) mbar_arrive(o_free);
                 __threadfence();
+                if (t == 0) stamp_cta(p, 4);
                 named_bar_sync(1, 128);
-                if (t == 0) misc[1] = (atomicAdd(p.counters + tile, 1) == fm.nf - 1) ? 1u : 0u;
-                named_bar_sync(1, 128);
-                if (misc[1]) {
-                    // last fragment to finish: merge all fragments of the tile in fragment order
-                    __threadfence();
-                    float mf[8], lf[8];
-                    int sl[8];
-                    float M = -INFINITY;
-                    const int nfr2 = fm.nf < 8 ? fm.nf : 8;
-                    for (int q2 = 0; q2 < nfr2; ++q2) {
-                        const int c2 = fm.first_cta + q2;
-                        const int first2 =
-                            p.tail_base + static_cast<int>(range_begin(c2, p.vtotal, p.tail_grid) / p.vlen);
-                        sl[q2] = 2 * c2 + (tile == first2 ? 0 : 1);
-                        mf[q2] = __ldcg(p.part_ml + static_cast<int64_t>(sl[q2]) * 256 + r);
-                        lf[q2] = __ldcg(p.part_ml + static_cast<int64_t>(sl[q2]) * 256 + 128 + r);
-                        M = fmaxf(M, mf[q2]);
-                    }
-                    float Ls = 0.0f;
-                    for (int q2 = 0; q2 < nfr2; ++q2) {
-                        mf[q2] = mf[q2] == -INFINITY ? 0.0f : exp2_approx(mf[q2] - M);
-                        Ls += mf[q2] * lf[q2];
-                    }
-                    const float inv = Ls > 0.0f ? 1.0f / Ls : 0.0f;
-                    if (valid) {
-                        bf16* orow = p.o + orow_off;
-#pragma unroll 1
-                        for (int c0 = 0; c0 < D; c0 += 8) {
-                            float acc8[8];
-#pragma unroll
-                            for (int c = 0; c < 8; ++c) acc8[c] = 0.0f;
-                            for (int q2 = 0; q2 < nfr2; ++q2) {
-                                const float4* src = reinterpret_cast<const float4*>(
-                                    p.part_o + (static_cast<int64_t>(sl[q2]) * 128 + r) * D + c0);
-                                const float4 x0 = __ldcg(src), x1 = __ldcg(src + 1);
-                                acc8[0] += mf[q2] * x0.x; acc8[1] += mf[q2] * x0.y;
-                                acc8[2] += mf[q2] * x0.z; acc8[3] += mf[q2] * x0.w;
-                                acc8[4] += mf[q2] * x1.x; acc8[5] += mf[q2] * x1.y;
-                                acc8[6] += mf[q2] * x1.z; acc8[7] += mf[q2] * x1.w;
-                            }
-                            uint4 w;
-                            w.x = pack_bf16x2(acc8[0] * inv, acc8[1] * inv);
-                            w.y = pack_bf16x2(acc8[2] * inv, acc8[3] * inv);
-                            w.z = pack_bf16x2(acc8[4] * inv, acc8[5] * inv);
-                            w.w = pack_bf16x2(acc8[6] * inv, acc8[7] * inv);
-                            *reinterpret_cast<uint4*>(orow + c0) = w;
-                        }
-                        if (p.lse != nullptr)
-                            p.lse[orow_idx] = Ls > 0.0f ? (M + __log2f(Ls)) * 0.69314718055994531f : -INFINITY;
-                    }
-                    if (t == 0) p.counters[tile] = 0;  // ready for the next launch
-                }
+                if (t == 0) atomicAdd(p.counters + tile, 1);  // this fragment's partial is written
+                pend[npend++] = fm;
             }
             jg += nf;
+        }
+
+        // ---------------------------------------------------------- split-tile merge
+        // Every CTA holding a fragment of a split tile merges a slice of its 128 rows (fragment q of
+        // nf takes rows [128 q / nf, 128 (q + 1) / nf)), in fragment order (deterministic), once it
+        // has finished ALL its own fragments -- so no CTA waits while a partial of its own is
+        // unwritten, and the co-resident grid cannot deadlock.  The K ring is idle by now (every
+        // fragment's MMAs completed) and holds the per-row merge weights.  The tile counter counts
+        // nf partial arrivals, then nf merge completions; the last merger re-zeroes it.
+        float* wsm = reinterpret_cast<float*>(k_smem);  // [8][128] weights, [8 * 128 + r] 1 / sum, [9 * 128 + q] slots
+        for (int i = 0; i < npend; ++i) {
+            const FragMeta pm = pend[i];
+            const int nfr = pm.nf < 8 ? pm.nf : 8;
+            const int q = cta - pm.first_cta;
+            const int r0 = q * 128 / nfr, nrows = (q + 1) * 128 / nfr - r0;
+            if (t == 0) {
+                while (ld_acquire_gpu(p.counters + pm.tile) < nfr) __nanosleep(32);
+                stamp_cta(p, 5);
+            }
+            int* sl = reinterpret_cast<int*>(wsm + 9 * 128);  // partial slot of fragment q2
+            if (t < nfr) {
+                const int c2 = pm.first_cta + t;
+                const int first2 = p.tail_base + static_cast<int>(range_begin(c2, p.vtotal, p.tail_grid) / p.vlen);
+                sl[t] = 2 * c2 + (pm.tile == first2 ? 0 : 1);
+            }
+            named_bar_sync(1, 128);
+            if (t < nrows) {
+                const int row = r0 + t;
+                float mf[8], lf[8];
+                float M = -INFINITY;
+                for (int q2 = 0; q2 < nfr; ++q2) {
+                    mf[q2] = __ldcg(p.part_ml + static_cast<int64_t>(sl[q2]) * 256 + row);
+                    lf[q2] = __ldcg(p.part_ml + static_cast<int64_t>(sl[q2]) * 256 + 128 + row);
+                    M = fmaxf(M, mf[q2]);
+                }
+                float Ls = 0.0f;
+                for (int q2 = 0; q2 < nfr; ++q2) {
+                    mf[q2] = mf[q2] == -INFINITY ? 0.0f : exp2_approx(mf[q2] - M);
+                    Ls += mf[q2] * lf[q2];
+                }
+                for (int q2 = 0; q2 < nfr; ++q2) wsm[q2 * 128 + t] = mf[q2];
+                wsm[8 * 128 + t] = Ls > 0.0f ? 1.0f / Ls : 0.0f;
+                const int qb2 = pm.qb0 + (row >> 6), rr2 = row & 63;
+                if (rr2 < p.b && qb2 < p.nqb && p.lse != nullptr)
+                    p.lse[(static_cast<int64_t>(pm.u) * p.nqb + qb2) * p.b + rr2] =
+                        Ls > 0.0f ? (M + __log2f(Ls)) * 0.69314718055994531f : -INFINITY;
+            }
+            named_bar_sync(1, 128);
+            // the slice as (row, float4 column) items, 8 per thread in flight per fragment: a warp
+            // reads one 512-byte partial row per load instruction
+            constexpr int C4 = D / 4;
+            const int items = nrows * C4;
+            for (int base = 0; base < items; base += 128 * 8) {
+                float4 acc[8];
+#pragma unroll
+                for (int k8 = 0; k8 < 8; ++k8) acc[k8] = make_float4(0.f, 0.f, 0.f, 0.f);
+                // two fragments per round: 16 loads in flight per thread
+                for (int q2 = 0; q2 < nfr; q2 += 2) {
+                    float4 x[2][8];
+#pragma unroll
+                    for (int h2 = 0; h2 < 2; ++h2)
+#pragma unroll
+                        for (int k8 = 0; k8 < 8; ++k8) {
+                            const int it = base + k8 * 128 + t;
+                            x[h2][k8] = (it < items && q2 + h2 < nfr)
+                                            ? __ldcg(reinterpret_cast<const float4*>(
+                                                         p.part_o + (static_cast<int64_t>(sl[q2 + h2]) * 128 + r0 + it / C4) * D) +
+                                                     it % C4)
+                                            : make_float4(0.f, 0.f, 0.f, 0.f);
+                        }
+#pragma unroll
+                    for (int h2 = 0; h2 < 2; ++h2)
+#pragma unroll
+                        for (int k8 = 0; k8 < 8; ++k8) {  // fragment order: q2, then q2 + 1
+                            const int it = base + k8 * 128 + t;
+                            const float w = (it < items && q2 + h2 < nfr) ? wsm[(q2 + h2) * 128 + it / C4] : 0.0f;
+                            acc[k8].x += w * x[h2][k8].x;
+                            acc[k8].y += w * x[h2][k8].y;
+                            acc[k8].z += w * x[h2][k8].z;
+                            acc[k8].w += w * x[h2][k8].w;
+                        }
+                }
+#pragma unroll
+                for (int k8 = 0; k8 < 8; ++k8) {
+                    const int it = base + k8 * 128 + t;
+                    if (it >= items) continue;
+                    const int rl = it / C4, row = r0 + rl;
+                    const int qb2 = pm.qb0 + (row >> 6), rr2 = row & 63;
+                    if (rr2 >= p.b || qb2 >= p.nqb) continue;
+                    const float inv = wsm[8 * 128 + rl];
+                    uint2 w2;
+                    w2.x = pack_bf16x2(acc[k8].x * inv, acc[k8].y * inv);
+                    w2.y = pack_bf16x2(acc[k8].z * inv, acc[k8].w * inv);
+                    *reinterpret_cast<uint2*>(p.o + orow_offset(pm.u, qb2, rr2) + (it % C4) * 4) = w2;
+                }
+            }
+            named_bar_sync(1, 128);  // wsm is rewritten by the next merge
+            if (t == 0) {
+                if (atomicAdd(p.counters + pm.tile, 1) == 2 * nfr - 1) p.counters[pm.tile] = 0;  // next launch
+                stamp_cta(p, 6);
+            }
         }
     }
     tc_fence_before();
@@ -596,6 +673,14 @@ __global__ void __launch_bounds__(kThreads, 2)
         tc_fence_after();
         tmem_dealloc<kTmemCols>(tmem);
     }
+#ifdef PBSA_K3_TRACE
+    if (threadIdx.x == 0 && p.trace != nullptr) {
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        stamp_cta(p, 7);
+        p.trace[15 * 256 + 8 * 1024 + blockIdx.x] = smid;
+    }
+#endif
     if (p.gangs > 0 && threadIdx.x == 0) {
         // the last CTA out re-zeroes the gang counters for the next launch (every producer has
         // passed its last barrier: a CTA only exits after its producer finished all units)

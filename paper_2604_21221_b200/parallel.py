@@ -196,9 +196,10 @@ class QuerySplitLayout:
         recv = torch.empty((self.replicas * units,) + tuple(send.shape[1:]), dtype=send.dtype, device=send.device)
         if is_dist():
             dist.all_gather_into_tensor(recv, send, group=self._group_pg)
-        else:
+            recv = recv.view((self.replicas,) + tuple(send.shape))
+        else:  # single-process simulation of one rank (tools/strong_rank_sim.py): own rows everywhere
+            recv = recv.view((self.replicas,) + tuple(send.shape))
             recv[:] = send
-        recv = recv.view((self.replicas,) + tuple(send.shape))
         for r, (b, c) in enumerate(self.q_ranges):
             qc_full[:, b: b + c] = recv[r, :, :c]
         return qc_full

@@ -11,6 +11,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2604_21221_b200 as pb  # noqa: E402
 
 U, nqb, b, d, S, nd, nl, k = 12, 78, 60, 128, 546, 234, 312, 78
+U, nqb = int(os.environ.get("U", U)), int(os.environ.get("NQB", nqb))  # e.g. U=3 NQB=39: one rank of N=8
 g = torch.Generator(device="cuda").manual_seed(0)
 kp = torch.zeros(U, S, 64, d, device="cuda", dtype=torch.bfloat16)
 vp = torch.zeros_like(kp)
@@ -27,7 +28,7 @@ un = 0
 sc = sel.cpu()
 for u in range(U):
     for t in range(0, nqb, 2):
-        un += nd + len(set(sc[u, t].tolist()) | set(sc[u, t + 1].tolist()))
+        un += nd + len(set(sc[u, t].tolist()) | (set(sc[u, t + 1].tolist()) if t + 1 < nqb else set()))
 exe = 4.0 * 128 * 64 * d * un
 for sk in ((True,) if os.environ.get("PBSA_SWEEP_SK_ONLY") else (True, False)):
     for _ in range(3):
