@@ -684,14 +684,11 @@ int attend_impl(pbsa_mem* m, const void* q, int k_top, float scale, int mode, vo
         m->last_n_keys = n_keys;
         sel_row0 = split ? part.begin : 0;
     } else if (k > 0) {
-        if (split) {  // this rank's rows of qc_full, compacted into m->qc
-            PBSA_CUDA(cudaMemcpy2DAsync(m->qc, static_cast<size_t>(nq) * d * 4, part.qc_full + static_cast<size_t>(part.begin) * d,
-                                        static_cast<size_t>(bpc) * d * 4, static_cast<size_t>(nq) * d * 4, U,
-                                        cudaMemcpyDeviceToDevice, s));
-        }
-        if (int rc = launch_score_select(m->qc, m->krep, static_cast<int64_t>(m->S) * d, m->dev.l_slot, m->Lcap,
-                                         n_l, 0, n_l, k, nq, U, d, scale, m->sel, nullptr, m->ws,
-                                         m->ws_bytes, s, m->dev.status))
+        // (split form: this rank's rows of qc_full, read in place)
+        if (int rc = launch_score_select(split ? part.qc_full : m->qc, m->krep, static_cast<int64_t>(m->S) * d,
+                                         m->dev.l_slot, m->Lcap, n_l, 0, n_l, k, nq, U, d, scale, m->sel, nullptr,
+                                         m->ws, m->ws_bytes, s, m->dev.status, split ? bpc : 0,
+                                         split ? part.begin : 0))
             return rc;
         sel_rows = nq;
     }
@@ -806,14 +803,10 @@ int pbsa_attend_part_ingest(pbsa_mem* m, const void* q_part, int q_begin, int q_
     if (prof) cudaEventRecord(m->ev_write[static_cast<size_t>(m->prof_write) * 2], s);
     // the whole chunk's K/V into the stage slots + K compression (replicated on every rank holding the
     // head), then the representatives of this rank's query blocks into their rows of qc_full
-    if (int rc = launch_write_chunk(static_cast<const bf16*>(k_chunk), static_cast<const bf16*>(v_chunk), nullptr,
-                                    m->dev.stage, m->bpc, m->b, m->d, m->units, m->S, m->k_pool, m->v_pool, m->krep,
-                                    nullptr, s))
-        return rc;
-    const int b = m->b, d = m->d;
-    if (int rc = launch_compress(static_cast<const bf16*>(q_part), static_cast<int64_t>(q_count) * b * d,
-                                 static_cast<int64_t>(b) * d, nullptr, q_count, m->units, b, d,
-                                 qc_full + static_cast<size_t>(q_begin) * d, static_cast<int64_t>(m->bpc) * d, s))
+    // (one fused pass: the Q blocks of the range are compressed by the same CTAs)
+    if (int rc = launch_write_chunk(static_cast<const bf16*>(k_chunk), static_cast<const bf16*>(v_chunk),
+                                    static_cast<const bf16*>(q_part), m->dev.stage, m->bpc, m->b, m->d, m->units, m->S,
+                                    m->k_pool, m->v_pool, m->krep, qc_full, s, q_begin, q_count))
         return rc;
     if (prof) {
         cudaEventRecord(m->ev_write[static_cast<size_t>(m->prof_write) * 2 + 1], s);

@@ -170,12 +170,15 @@ __global__ void __launch_bounds__(2 * D) write_chunk_bulk_kernel(const bf16* __r
                                                                  const int32_t* __restrict__ stage, int bpc, int b,
                                                                  int units, int n_slots, bf16* __restrict__ kp,
                                                                  bf16* __restrict__ vp, float* __restrict__ krep,
-                                                                 float* __restrict__ qrep) {
+                                                                 float* __restrict__ qrep, int q_begin, int q_count) {
     pdl_wait();  // programmatic dependent launch: upstream outputs are visible from here on
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ __align__(8) uint64_t bar;
     const int tid = threadIdx.x;
     const int u = blockIdx.x / bpc, i = blockIdx.x % bpc;
+    // Q of query blocks [q_begin, q_begin + q_count) only (a rank's range in the batch-1 query
+    // split; the whole chunk otherwise): qcur is [units][q_count * b][D], qrep keeps bpc rows/unit
+    const bool has_q = WITH_Q && i >= q_begin && i < q_begin + q_count;
     const int slot = __ldg(stage + static_cast<int64_t>(u) * bpc + i);
     const uint32_t bytes = static_cast<uint32_t>(b) * D * 2;
     const int64_t src_off = (static_cast<int64_t>(u) * bpc + i) * b * D;
@@ -186,10 +189,10 @@ __global__ void __launch_bounds__(2 * D) write_chunk_bulk_kernel(const bf16* __r
     if (tid == 0) {
         mbar_init(&bar, 1);
         fence_barrier_init();
-        mbar_arrive_expect_tx(&bar, (WITH_Q ? 3u : 2u) * bytes);
+        mbar_arrive_expect_tx(&bar, (has_q ? 3u : 2u) * bytes);
         bulk_g2s(ks, kc + src_off, bytes, &bar);
         bulk_g2s(vs, vc + src_off, bytes, &bar);
-        if (WITH_Q) bulk_g2s(qs, qcur + src_off, bytes, &bar);
+        if (has_q) bulk_g2s(qs, qcur + (static_cast<int64_t>(u) * q_count + (i - q_begin)) * b * D, bytes, &bar);
     }
     __syncthreads();
     mbar_wait(&bar, 0);
@@ -200,7 +203,7 @@ __global__ void __launch_bounds__(2 * D) write_chunk_bulk_kernel(const bf16* __r
     }
     const int c = tid % D;
     const bool is_q = tid >= D;
-    if (!is_q || WITH_Q) {
+    if (!is_q || has_q) {
         const bf16* col = (is_q ? qs : ks) + c;
         double acc = 0.0;
 #pragma unroll 4
@@ -283,7 +286,8 @@ int launch_compress(const bf16* x, int64_t xu, int64_t xb, const int32_t* map, i
 
 int launch_write_chunk(const bf16* kc, const bf16* vc, const bf16* q, const int32_t* stage, int bpc, int b,
                        int d, int units, int n_slots, bf16* kp, bf16* vp, float* krep, float* qrep,
-                       cudaStream_t s) {
+                       cudaStream_t s, int q_begin, int q_count) {
+    if (q_count < 0) q_count = bpc;
     const int64_t warps = static_cast<int64_t>(bpc) * units;
     if (warps == 0) return 0;
     const size_t smem = (q ? 3 : 2) * static_cast<size_t>(b) * d * 2;
@@ -294,7 +298,7 @@ int launch_write_chunk(const bf16* kc, const bf16* vc, const bf16* q, const int3
                                  "write_chunk"))                                                                 \
             return rc;                                                                                           \
         launch_pdl(write_chunk_bulk_kernel<DD, WQ>, dim3(static_cast<unsigned>(warps)), dim3(2 * DD), smem, s, kc,  \
-                   vc, q, stage, bpc, b, units, n_slots, kp, vp, krep, qrep);                                   \
+                   vc, q, stage, bpc, b, units, n_slots, kp, vp, krep, qrep, q_begin, q_count);                 \
     } while (0)
         if (d == 128) {
             if (q) PBSA_WCB(128, true); else PBSA_WCB(128, false);
@@ -304,6 +308,8 @@ int launch_write_chunk(const bf16* kc, const bf16* vc, const bf16* q, const int3
 #undef PBSA_WCB
         return check_launch("write_chunk_bulk_kernel");
     }
+    if (q && (q_begin != 0 || q_count != bpc))
+        return set_error(PBSA_EUNSUPPORTED, "write_chunk: query-block range needs the bulk kernel");
     const int grid = static_cast<int>((warps + 7) / 8);
     count_launch();
 #define PBSA_WC(DD, WQ) write_chunk_kernel<DD, WQ><<<grid, 256, 0, s>>>(kc, vc, q, stage, bpc, b, units, n_slots, kp, vp, krep, qrep)

@@ -70,7 +70,7 @@ int launch_compress(const bf16* x, int64_t x_unit_stride, int64_t x_block_stride
 // q / qrep nullable: with q, the same pass also compresses the current chunk's query blocks
 int launch_write_chunk(const bf16* kc, const bf16* vc, const bf16* q, const int32_t* stage, int bpc, int b,
                        int d, int units, int n_slots, bf16* k_pool, bf16* v_pool, float* krep, float* qrep,
-                       cudaStream_t s);
+                       cudaStream_t s, int q_begin = 0, int q_count = -1);
 // the same fused ingest reading the chunk's K/V/Q latents directly (blockify fused into the TMA box)
 int launch_ingest_latent(const bf16* k_lat, const bf16* v_lat, const bf16* q_lat, const LatentGeom& g,
                          const int32_t* stage, int n_slots, bf16* k_pool, bf16* v_pool, float* krep, float* qrep,
@@ -80,7 +80,8 @@ size_t score_select_workspace(int units, int nqb, int n_keys);
 int launch_score_select(const float* qc, const float* krep, int64_t krep_unit_stride,
                         const int32_t* key_slots, int key_stride, int n_keys, int local_off,
                         int n_local, int k, int nqb, int units, int d, float scale, int32_t* sel,
-                        float* s_t, void* ws, size_t ws_bytes, cudaStream_t s, int* status = nullptr);
+                        float* s_t, void* ws, size_t ws_bytes, cudaStream_t s, int* status = nullptr,
+                        int qc_rows = 0, int qc_row0 = 0);  // qc [units][qc_rows (0: nqb)][d], rows from qc_row0
 // aggregate_scores (Eq. 8): s[u][j] = float(sum_i double(a[u][i][j]) / rows), ascending i
 int launch_aggregate_scores(const float* a, int rows, int cols, int units, float* s, cudaStream_t st);
 // SPEC-op primitives on device f32 matrices (spec_ops.cu; the drop-in C++ API, not the hot path)

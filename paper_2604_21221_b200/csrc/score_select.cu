@@ -40,6 +40,11 @@ struct ScoreParams {
     int32_t* sel;         // [U][nqb][k]
     float* arows;         // [U][nqb][n_keys] or null
     int* status;          // nullable: bit 0 set when a logit row holds NaN (invalid input)
+    int qc_rows = 0, qc_row0 = 0;  // qc is [U][qc_rows][D]; row i of the launch is qc row qc_row0 + i
+    // flat index of row i of unit u in qc (times D = its offset)
+    __device__ __forceinline__ int64_t qidx(int u, int i) const {
+        return static_cast<int64_t>(u) * qc_rows + qc_row0 + i;
+    }
 };
 
 constexpr int kMaxRows = 8;
@@ -95,7 +100,7 @@ __global__ void __launch_bounds__(kLogitKeys) logits_rm_kernel(const ScoreParams
 #pragma unroll
         for (int t = 0; t < Q4 / kLogitKeys; ++t) {
             const int e4 = tid + t * kLogitKeys, r = (e4 * 4) / D;
-            qv[t] = r < nr ? __ldg(reinterpret_cast<const float4*>(p.qc + (static_cast<int64_t>(u) * p.nqb + i0) * D) + e4)
+            qv[t] = r < nr ? __ldg(reinterpret_cast<const float4*>(p.qc + p.qidx(u, i0) * D) + e4)
                            : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
@@ -229,7 +234,7 @@ __global__ void __launch_bounds__(kL32Warps * 32) logits32_kernel(const ScorePar
         for (int c4 = lane; c4 < C4; c4 += 32) cp_async16(ks + kk * C4 + (c4 ^ ((kk >> 2) & 7)), kr + c4);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
-    const float4* qg = reinterpret_cast<const float4*>(p.qc + (static_cast<int64_t>(u) * p.nqb + i0) * D);
+    const float4* qg = reinterpret_cast<const float4*>(p.qc + p.qidx(u, i0) * D);
     for (int e4 = tid; e4 < nr * C4; e4 += kL32Warps * 32) qs[e4] = __ldg(qg + e4);
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
@@ -368,7 +373,7 @@ __global__ void __launch_bounds__(kCertThreads, 3) cert_select_kernel(const Scor
     const int n = p.n_local, k = p.k;
     const int u = static_cast<int>(row / p.nqb);
     float* zg = z + row * n4;
-    const float* q = p.qc + row * D;
+    const float* q = p.qc + p.qidx(u, static_cast<int>(row - static_cast<int64_t>(u) * p.nqb)) * D;
     const int32_t* slots = p.keys + static_cast<int64_t>(u) * p.key_stride + p.local_off;
     const float* kr = p.krep + u * p.kru;
     int32_t* out = p.sel + row * k;
@@ -680,7 +685,7 @@ __global__ void __launch_bounds__(256, 2) logits_t_kernel(const ScoreParams p, f
     const int nr = min(kMaxRows, p.nqb - i0);
     for (int e = threadIdx.x; e < kMaxRows * D; e += blockDim.x) {
         const int r = e / D, c = e % D;
-        qd[e] = r < nr ? static_cast<double>(p.qc[(static_cast<int64_t>(u) * p.nqb + i0 + r) * D + c]) : 0.0;
+        qd[e] = r < nr ? static_cast<double>(p.qc[p.qidx(u, i0 + r) * D + c]) : 0.0;
     }
     __syncthreads();
     const int jb = blockIdx.z * blockDim.x * kKeysPerThread + threadIdx.x;
@@ -907,7 +912,8 @@ static int cert_mode() {
 int launch_score_select(const float* qc, const float* krep, int64_t kru, const int32_t* keys,
                         int key_stride, int n_keys, int local_off, int n_local, int k, int nqb,
                         int units, int d, float scale, int32_t* sel, float* s_t, void* ws,
-                        size_t ws_bytes, cudaStream_t s, int* status) {
+                        size_t ws_bytes, cudaStream_t s, int* status, int qc_rows, int qc_row0) {
+    if (qc_rows <= 0) qc_rows = nqb;
     if (units == 0 || nqb == 0 || n_keys == 0) return 0;
     const bool do_select = k > 0 && n_local > 0;
     if (!do_select && s_t == nullptr) return 0;
@@ -930,6 +936,8 @@ int launch_score_select(const float* qc, const float* krep, int64_t kru, const i
         const int64_t es = (n_local + 1) & ~1;  // 16-byte aligned fp64 scratch rows
         ScoreParams p{qc, krep, kru, keys, key_stride, n_keys, local_off, n_local, k, nqb, units,
                       1, scale, 0, sel, nullptr, status};
+        p.qc_rows = qc_rows;
+        p.qc_row0 = qc_row0;
         dim3 g1((n_local + kLogitKeys - 1) / kLogitKeys, (nqb + kL32Warps * 8 - 1) / (kL32Warps * 8), units);
         const size_t lsmem = static_cast<size_t>(kL32Warps * 8 + kLogitKeys) * d * 4;
         const int v4 = (n_local + 4 * kCertThreads - 1) / (4 * kCertThreads);  // float4 per thread
@@ -952,6 +960,8 @@ int launch_score_select(const float* qc, const float* krep, int64_t kru, const i
         rows = rows < 1 ? 1 : (rows > kMaxRows ? kMaxRows : rows);
         ScoreParams p{qc, krep, kru, keys, key_stride, n_keys, local_off, n_local, do_select ? k : 0, nqb, units,
                       rows, scale, per_warp, sel, arows, status};
+        p.qc_rows = qc_rows;
+        p.qc_row0 = qc_row0;
         if (rows < kMaxRows) {
             // long key lists: key-major logits -> thread-per-row softmax statistics -> warp-per-row select
             const int64_t rt = static_cast<int64_t>(units) * nqb;
