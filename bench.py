@@ -283,7 +283,9 @@ def run_ours(args, rank, world, local_rank):
     sets = [inputs() for _ in range(n_sets)]
     out = torch.empty(Ul, qn * b, d, device=dev, dtype=torch.bfloat16)
     outs2 = [torch.empty(Ul, qn * b, d, device=dev, dtype=torch.bfloat16) for _ in range(2)]
-    gathered = torch.empty(U, nq, d, device=dev, dtype=torch.bfloat16)
+    # two gather targets: the exchange of call j may still be writing while call j + 1 gathers
+    gathered2 = [torch.empty(U, nq, d, device=dev, dtype=torch.bfloat16) for _ in range(2)]
+    gathered = gathered2[0]
     qc_full = torch.zeros(Ul, bpc, d, device=dev, dtype=torch.float32)
     pending = [None, None]  # (work, finish) of the output exchange reading outs2[i]
 
@@ -298,10 +300,10 @@ def run_ours(args, rank, world, local_rank):
             qs.gather_qc(qc_full)
         mem.attend_part(q, qb0, qc_full, k_top, mode, out=o)
 
-    def exchange(o):
+    def exchange(o, i=0):
         if qs is not None:
-            return qs.gather_output(o, b, out=gathered, async_op=True)
-        return lay.exchange(o, out=gathered, async_op=True)
+            return qs.gather_output(o, b, out=gathered2[i], async_op=True)
+        return lay.exchange(o, out=gathered2[i], async_op=True)
 
     def chunk_step(i):
         for j in range(T + 1):
@@ -316,7 +318,7 @@ def run_ours(args, rank, world, local_rank):
                 pending[j & 1][1]()
                 pending[j & 1] = None
             attend(q, kk, vv, mode, o)
-            pending[j & 1] = exchange(o)
+            pending[j & 1] = exchange(o, j & 1)
 
     def drain():
         for i in range(2):

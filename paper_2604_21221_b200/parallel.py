@@ -207,19 +207,35 @@ class QuerySplitLayout:
     def gather_output(self, o_part: torch.Tensor, block_rows: int, out: torch.Tensor | None = None,
                       async_op: bool = False):
         """o_part [heads_per_group, q_count * block_rows, d] -> [heads, bpc * block_rows, d] on every
-        rank (all-gather of the padded shards).  async_op=True returns (work, finish)."""
+        rank (all-gather of the padded shards).  async_op=True returns (work, finish).
+
+        Rank order is (group, replica), so with R = 1 the gathered shards already ARE the output
+        in head order and NCCL writes straight into `out` (no copy); with R > 1 and equal query
+        ranges one permuting copy ([G][R][units][rows] -> [G][units][R * rows]) finishes it;
+        unequal ranges fall back to per-source slice copies."""
         units, _, d = o_part.shape
         mrows = self.max_q * block_rows
         send = o_part
         if o_part.shape[1] != mrows:
             send = torch.zeros(units, mrows, d, dtype=o_part.dtype, device=o_part.device)
             send[:, : o_part.shape[1]] = o_part
-        flat = torch.empty((self.world * units, mrows, d), dtype=o_part.dtype, device=o_part.device)
-        recv = flat.view(self.world, units, mrows, d)
         if out is None:
             out = torch.empty(self.heads, self.bpc * block_rows, d, dtype=o_part.dtype, device=o_part.device)
+        equal = all(c == self.max_q for _, c in self.q_ranges)
+        direct = self.replicas == 1 and equal and out.is_contiguous()
+        if direct:
+            flat = out.view(self.world * units, mrows, d)
+        else:
+            flat = torch.empty((self.world * units, mrows, d), dtype=o_part.dtype, device=o_part.device)
+        recv = flat.view(self.world, units, mrows, d)
 
         def finish():
+            if direct:
+                return out
+            if equal and out.is_contiguous():
+                G, R = self.groups, self.replicas
+                out.view(G, units, R, mrows, d).copy_(recv.view(G, R, units, mrows, d).transpose(1, 2))
+                return out
             for src in range(self.world):
                 g, r = divmod(src, self.replicas)
                 b, c = self.q_ranges[r]
@@ -228,7 +244,9 @@ class QuerySplitLayout:
             return out
 
         if not is_dist() or self.world == 1:
-            recv[0] = send
+            # single process: only this rank's shard is real (tools/strong_rank_sim.py simulates one
+            # rank); a real world-1 layout has one group and one replica, i.e. recv[0] is everything
+            recv[self.rank if self.world > 1 else 0] = send
             return finish() if not async_op else (_Done(), finish)
         work = dist.all_gather_into_tensor(flat, send.contiguous(), async_op=async_op)
         if async_op:

@@ -136,12 +136,12 @@ def test_query_split_layout_partition():
         QuerySplitLayout(12, 1, 8, 0)  # 1 query block cannot be split over 2 replicas
 
 
-def _qs_worker(rank, world, port, q):
+def _qs_worker(rank, world, port, q, heads=12, bpc=7, use_async=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2604_21221_b200.parallel import QuerySplitLayout
-        heads, bpc, b, d = 12, 7, 2, 4
+        b, d = 2, 4
         lay = QuerySplitLayout(heads, bpc, world, rank)
         lay.setup()
         # Q^c: this replica fills only its rows; after the gather every replica of the group holds
@@ -158,22 +158,28 @@ def _qs_worker(rank, world, port, q):
         for i in range(lay.n_local):
             for r in range(lay.q_count * b):
                 o_part[i, r] = 1000.0 * (lay.head0 + i) + lay.q_begin * b + r
-        full = lay.gather_output(o_part, b)
+        if use_async:
+            work, finish = lay.gather_output(o_part, b, async_op=True)
+            work.wait()
+            full = finish()
+        else:
+            full = lay.gather_output(o_part, b)
         want = torch.tensor([[1000.0 * h + r for r in range(bpc * b)] for h in range(heads)])
         q.put((rank, ok_qc, torch.equal(full[:, :, 0], want)))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_gloo_query_split_gathers(world):
-    """world 2 (R = 1: two groups of 6 heads) and world 4 (gcd(4, 12) = 4 groups, R = 1) run the
-    output all-gather; a world-8-like replica split is exercised with world 2 over 1 head group
-    below."""
+@pytest.mark.parametrize("world,heads,bpc,use_async", [(2, 12, 7, False), (4, 12, 7, True), (4, 2, 8, True),
+                                                      (4, 2, 7, False)])
+def test_gloo_query_split_gathers(world, heads, bpc, use_async):
+    """world 2 / 4 over 12 heads (R = 1: NCCL-style direct gather into the output), and 2 heads on
+    4 ranks (2 groups x 2 replicas, the N = 8 shape of config 2 in miniature): equal query ranges
+    (8 blocks: one permuting copy) and unequal ones (7 blocks: 4 + 3, per-source slices)."""
     port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_qs_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_qs_worker, args=(r, world, port, q, heads, bpc, use_async)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in range(world)]

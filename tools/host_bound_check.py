@@ -29,12 +29,25 @@ for n in [int(x) for x in os.environ.get("NS", "1,2,4,8").split(",")]:
     out = torch.empty(Ul, qn * b, d, device=dev, dtype=torch.bfloat16)
     qc_full = torch.zeros(Ul, bpc, d, device=dev, dtype=torch.float32)
 
+    exch = os.environ.get("EXCHANGE") == "1"  # also run the bench's gathers (single-process form)
+    gathered = [torch.empty(U, bpc * b, d, device=dev, dtype=torch.bfloat16) for _ in range(2)]
+    outs = [torch.empty_like(out) for _ in range(2)]
+    ncall = [0]
+
     def call(q, kk, vv, mode):
+        o = outs[ncall[0] & 1] if exch else out
         if not split:
-            mem.attend_qkv(q, kk, vv, k_top, mode, out=out)
+            mem.attend_qkv(q, kk, vv, k_top, mode, out=o)
         else:
             mem.attend_part_ingest(q, qb0, kk, vv, qc_full)
-            mem.attend_part(q, qb0, qc_full, k_top, mode, out=out)
+            if exch and mode == pb.MODE_CACHE_UPDATE:
+                qs.gather_qc(qc_full)
+            mem.attend_part(q, qb0, qc_full, k_top, mode, out=o)
+        if exch:
+            work, finish = qs.gather_output(o, b, out=gathered[ncall[0] & 1], async_op=True)
+            work.wait()
+            finish()
+        ncall[0] += 1
 
     i = 0
     while True:
