@@ -7,7 +7,7 @@
 //
 // Roofline: HBM.  Algorithmic bytes per block = b*d*2 (bf16 read) + d*4 (f32 write).  One warp
 // per block; lane l owns columns [l*C, l*C+C), C = d/32, so each token row is one coalesced
-// 256-byte (d=128) warp load; rows are unrolled 4-deep for memory-level parallelism.  The fp64
+// 256-byte (d=128) warp load; rows are unrolled 16-deep for memory-level parallelism.  The fp64
 // adds (one per element) stay far below the DADD rate at HBM speed.
 #include "internal.h"
 #include "ptx.cuh"
@@ -43,6 +43,7 @@ __global__ void __launch_bounds__(256) compress_kernel(const bf16* __restrict__ 
                                                        const int32_t* __restrict__ map, int nb,
                                                        int units, int b, float* __restrict__ reps,
                                                        int64_t ru) {
+    pdl_wait();  // programmatic dependent launch: upstream outputs are visible from here on
     constexpr int C = D / 32;
     using V = typename Vec<C>::T;
     const int64_t w = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
@@ -54,24 +55,22 @@ __global__ void __launch_bounds__(256) compress_kernel(const bf16* __restrict__ 
     double acc[C];
 #pragma unroll
     for (int c = 0; c < C; ++c) acc[c] = 0.0;
-    int t = 0;
-    for (; t + 4 <= b; t += 4) {
-        V v[4];
+    // 16 token rows in flight per lane (a block is <= 64 rows: at most 4 round trips to memory);
+    // the adds stay in ascending token order
+    constexpr int kDepth = 16;
+    for (int t = 0; t < b; t += kDepth) {
+        V v[kDepth];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) v[r] = __ldg(src + (t + r) * (D / C));
+        for (int r = 0; r < kDepth; ++r)
+            if (t + r < b) v[r] = __ldg(src + (t + r) * (D / C));
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
+        for (int r = 0; r < kDepth; ++r) {
+            if (t + r >= b) break;
             float f[C];
             unpack<C>(v[r], f);
 #pragma unroll
             for (int c = 0; c < C; ++c) acc[c] += static_cast<double>(f[c]);
         }
-    }
-    for (; t < b; ++t) {
-        float f[C];
-        unpack<C>(__ldg(src + t * (D / C)), f);
-#pragma unroll
-        for (int c = 0; c < C; ++c) acc[c] += static_cast<double>(f[c]);
     }
     float* dst = reps + u * ru + static_cast<int64_t>(idx) * D + lane * C;
     const double db = static_cast<double>(b);
@@ -91,6 +90,7 @@ __global__ void __launch_bounds__(256) write_chunk_kernel(const bf16* __restrict
                                                           int b, int units, int n_slots,
                                                           bf16* __restrict__ kp, bf16* __restrict__ vp,
                                                           float* __restrict__ krep, float* __restrict__ qrep) {
+    pdl_wait();  // programmatic dependent launch: upstream outputs are visible from here on
     constexpr int C = D / 32;
     using V = typename Vec<C>::T;
     const int64_t w = static_cast<int64_t>(blockIdx.x) * (blockDim.x / 32) + threadIdx.x / 32;
@@ -269,18 +269,60 @@ __global__ void __launch_bounds__(2 * D) ingest_latent_kernel(const __grid_const
     if (tid == 0) bulk_wait_read0();
 }
 
+// Bulk variant (the hot path's Q compression): CTA per block, thread per column.  The block's b
+// contiguous token rows arrive in ONE bulk copy (every block's bytes in flight at once, where the
+// warp-per-block kernel above needs b / 16 dependent round trips), then each thread sums its
+// column from shared memory in ascending token order -- the same fp64 chain, bit-identical.
+template <int D>
+__global__ void __launch_bounds__(D) compress_bulk_kernel(const bf16* __restrict__ x, int64_t xu, int64_t xb,
+                                                           const int32_t* __restrict__ map, int nb, int b,
+                                                           float* __restrict__ reps, int64_t ru) {
+    pdl_wait();  // programmatic dependent launch: upstream outputs are visible from here on
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ __align__(8) uint64_t bar;
+    const int u = blockIdx.x / nb, i = blockIdx.x % nb;
+    const int idx = map ? __ldg(map + static_cast<int64_t>(u) * nb + i) : i;
+    const uint32_t bytes = static_cast<uint32_t>(b) * D * 2;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_barrier_init();
+        mbar_arrive_expect_tx(&bar, bytes);
+        bulk_g2s(smem, x + u * xu + static_cast<int64_t>(idx) * xb, bytes, &bar);
+    }
+    __syncthreads();
+    mbar_wait(&bar, 0);
+    const bf16* col = reinterpret_cast<const bf16*>(smem) + threadIdx.x;
+    double acc = 0.0;
+#pragma unroll 4
+    for (int t = 0; t < b; ++t) acc += static_cast<double>(__bfloat162float(col[t * D]));
+    reps[u * ru + static_cast<int64_t>(idx) * D + threadIdx.x] = __double2float_rn(__ddiv_rn(acc, static_cast<double>(b)));
+}
+
 }  // namespace
 
 int launch_compress(const bf16* x, int64_t xu, int64_t xb, const int32_t* map, int nb, int units,
                     int b, int d, float* reps, int64_t ru, cudaStream_t s) {
     const int64_t warps = static_cast<int64_t>(nb) * units;
     if (warps == 0) return 0;
+    // bulk copies need 16-byte aligned, 16-byte multiple block rows (always true for d = 64 / 128
+    // block-major inputs)
+    const bool bulk = (reinterpret_cast<uintptr_t>(x) & 15u) == 0 && (xu % 8) == 0 && (xb % 8) == 0 &&
+                      warps < (int64_t(1) << 31);
+    if (bulk) {
+        const size_t smem = static_cast<size_t>(b) * d * 2;
+        if (d == 128)
+            launch_pdl(compress_bulk_kernel<128>, dim3(static_cast<unsigned>(warps)), dim3(128), smem, s, x, xu, xb,
+                       map, nb, b, reps, ru);
+        else
+            launch_pdl(compress_bulk_kernel<64>, dim3(static_cast<unsigned>(warps)), dim3(64), smem, s, x, xu, xb,
+                       map, nb, b, reps, ru);
+        return check_launch("compress_bulk_kernel");
+    }
     const int grid = static_cast<int>((warps + 7) / 8);
-    count_launch();
     if (d == 128)
-        compress_kernel<128><<<grid, 256, 0, s>>>(x, xu, xb, map, nb, units, b, reps, ru);
+        launch_pdl(compress_kernel<128>, dim3(grid), dim3(256), 0, s, x, xu, xb, map, nb, units, b, reps, ru);
     else
-        compress_kernel<64><<<grid, 256, 0, s>>>(x, xu, xb, map, nb, units, b, reps, ru);
+        launch_pdl(compress_kernel<64>, dim3(grid), dim3(256), 0, s, x, xu, xb, map, nb, units, b, reps, ru);
     return check_launch("compress_kernel");
 }
 
