@@ -325,7 +325,9 @@ inline void plan_schedule(BsaParams& p, int slots, int D) {
         const int64_t tail = p.n_tiles - p.tail_base;
         p.vtotal = tail * p.vlen;
         // at most ~cap slots share a tail tile (the merge handles up to 8 fragments)
-        static const int cap = getenv("PBSA_K3_TAILCAP") ? atoi(getenv("PBSA_K3_TAILCAP")) : 4;
+        // (PBSA_K3_TAILCAP: experiments and tests; 4 measured best, tools/host_bound_check.py)
+        const char* cap_env = getenv("PBSA_K3_TAILCAP");
+        const int cap = cap_env && atoi(cap_env) >= 1 && atoi(cap_env) <= 8 ? atoi(cap_env) : 4;
         int64_t g = slots;
         if (g > p.vtotal) g = p.vtotal;
         if (g > cap * tail) g = cap * tail;

@@ -290,6 +290,20 @@ def test_bsa_fwd_unit_gang_schedule(pb, monkeypatch, units, nqb):
         assert plan.schedule == 2 and plan.gangs >= 1, (plan.schedule, plan.gangs)
 
 
+@pytest.mark.parametrize("cap", [2, 4, 5, 8])
+def test_bsa_fwd_split_tiles_parallel_merge(pb, monkeypatch, cap):
+    """Few tiles, long lists: every tile is split into up to `cap` fragments (cap 5: fragment
+    ranges cross tile boundaries, so CTAs hold two split tiles) and each fragment's CTA merges its
+    slice of the tile's rows.  Back-to-back launches check that the tile counters (nf arrivals,
+    then nf merges) re-zero."""
+    monkeypatch.setenv("PBSA_K3_TAILCAP", str(cap))
+    for rep in range(2):
+        _bsa_case(pb, 2, 7, 60, 128, 30, 60, 20, seed=140 + cap + rep)
+        plan = pb.bsa_fwd_last_plan()
+        assert plan.schedule == 1, plan.schedule  # stream-K
+        assert plan.grid <= cap * 8, (plan.grid, cap)
+
+
 def test_bsa_fwd_hybrid_two_waves_and_tail(pb):
     """Two full waves of whole tiles (2 x 296 CTA slots on a B200) then a stream-K tail."""
     _bsa_case(pb, 70, 17, 60, 128, 5, 12, 3, seed=22)
