@@ -56,8 +56,8 @@ struct Layout {
     static constexpr uint32_t kOffV = kOffK + NSK * kKVBytes;
     static constexpr uint32_t kOffBar = kOffV + NSV * kKVBytes;
     // q_full, q_empty, k_full/empty[NSK], v_full/empty[NSV], s_full[2], p_full[2], o_done[2],
-    // o_free, list_full[2], list_empty[2]
-    static constexpr int kNumBars = 2 + 2 * NSK + 2 * NSV + 6 + 1 + 4;
+    // o_free, list_full[2], list_empty[2], merge
+    static constexpr int kNumBars = 2 + 2 * NSK + 2 * NSV + 6 + 1 + 4 + 1;
     static constexpr uint32_t kOffMeta = kOffBar + kNumBars * 8;
     static constexpr uint32_t kOffMisc = kOffMeta + 2 * sizeof(FragMeta);
     static constexpr uint32_t kOffList = kOffMisc + 16;
@@ -114,6 +114,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     uint64_t* o_free = o_done + 2;
     uint64_t* list_full = o_free + 1;
     uint64_t* list_empty = list_full + 2;
+    uint64_t* merge_bar = list_empty + 2;
     FragMeta* meta = reinterpret_cast<FragMeta*>(smem + L::kOffMeta);
     uint32_t* misc = reinterpret_cast<uint32_t*>(smem + L::kOffMisc);  // [0] tmem base
     // visible lists, double-buffered: [2][max_list] entries of 4 bytes (slot | mask << 24) or, when
@@ -147,6 +148,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             mbar_init(list_empty + s, 5);  // MMA warp + 4 softmax warps
         }
         mbar_init(o_free, 4);
+        mbar_init(merge_bar, 1);
         fence_barrier_init();
         tma_prefetch(&tm_q);
         tma_prefetch(&tm_k);
@@ -573,16 +575,21 @@ __global__ void __launch_bounds__(kThreads, 2)
         // unwritten, and the co-resident grid cannot deadlock.  The K ring is idle by now (every
         // fragment's MMAs completed) and holds the per-row merge weights.  The tile counter counts
         // nf partial arrivals, then nf merge completions; the last merger re-zeroes it.
-        float* wsm = reinterpret_cast<float*>(k_smem);  // [8][128] weights, [8 * 128 + r] 1 / sum, [9 * 128 + q] slots
+#ifdef PBSA_K3_TRACE
+        if (t == 0 && p.trace != nullptr) p.trace[15 * 256 + 9 * 1024 + blockIdx.x] = jg;  // list entries processed
+#endif
+        // Q, K ring and V ring are idle by now (every fragment's loads were consumed by its MMAs):
+        // the slice's partial rows are staged there by bulk copies (one per fragment, all in flight
+        // together), the per-row weights after them
+        constexpr uint32_t kStageBytes = L::kOffBar;                 // [0, kOffBar): Q + K + V rings
+        float* stage = reinterpret_cast<float*>(smem);              // [nf][nrows][D] fp32
+        float* wsm = stage + (128 + 8) * D;                         // [8][128] weights, [8 * 128 + r] 1 / sum,
+        static_assert((128 + 8) * D * 4 + (9 * 128 + 8) * 4 <= kStageBytes, "merge staging");  // [9 * 128 + q] slots
         for (int i = 0; i < npend; ++i) {
             const FragMeta pm = pend[i];
             const int nfr = pm.nf < 8 ? pm.nf : 8;
             const int q = cta - pm.first_cta;
             const int r0 = q * 128 / nfr, nrows = (q + 1) * 128 / nfr - r0;
-            if (t == 0) {
-                while (ld_acquire_gpu(p.counters + pm.tile) < nfr) __nanosleep(32);
-                stamp_cta(p, 5);
-            }
             int* sl = reinterpret_cast<int*>(wsm + 9 * 128);  // partial slot of fragment q2
             if (t < nfr) {
                 const int c2 = pm.first_cta + t;
@@ -590,6 +597,17 @@ __global__ void __launch_bounds__(kThreads, 2)
                 sl[t] = 2 * c2 + (pm.tile == first2 ? 0 : 1);
             }
             named_bar_sync(1, 128);
+            if (t == 0) {
+                while (ld_acquire_gpu(p.counters + pm.tile) < nfr) __nanosleep(32);
+                stamp_cta(p, 5);
+                fence_proxy_async_global();
+                const uint32_t bytes = static_cast<uint32_t>(nrows) * D * 4;
+                mbar_arrive_expect_tx(merge_bar, bytes * nfr);
+                for (int q2 = 0; q2 < nfr; ++q2)
+                    bulk_g2s(stage + q2 * nrows * D, p.part_o + (static_cast<int64_t>(sl[q2]) * 128 + r0) * D, bytes,
+                             merge_bar);
+            }
+            named_bar_sync(1, 128);  // the tile's partials are complete (t == 0 acquired the counter)
             if (t < nrows) {
                 const int row = r0 + t;
                 float mf[8], lf[8];
@@ -611,54 +629,30 @@ __global__ void __launch_bounds__(kThreads, 2)
                     p.lse[(static_cast<int64_t>(pm.u) * p.nqb + qb2) * p.b + rr2] =
                         Ls > 0.0f ? (M + __log2f(Ls)) * 0.69314718055994531f : -INFINITY;
             }
+            mbar_wait(merge_bar, i & 1);
             named_bar_sync(1, 128);
-            // the slice as (row, float4 column) items, 8 per thread in flight per fragment: a warp
-            // reads one 512-byte partial row per load instruction
+            // (row, float4 column) items: a warp covers one 512-byte row per step
             constexpr int C4 = D / 4;
             const int items = nrows * C4;
-            for (int base = 0; base < items; base += 128 * 8) {
-                float4 acc[8];
-#pragma unroll
-                for (int k8 = 0; k8 < 8; ++k8) acc[k8] = make_float4(0.f, 0.f, 0.f, 0.f);
-                // two fragments per round: 16 loads in flight per thread
-                for (int q2 = 0; q2 < nfr; q2 += 2) {
-                    float4 x[2][8];
-#pragma unroll
-                    for (int h2 = 0; h2 < 2; ++h2)
-#pragma unroll
-                        for (int k8 = 0; k8 < 8; ++k8) {
-                            const int it = base + k8 * 128 + t;
-                            x[h2][k8] = (it < items && q2 + h2 < nfr)
-                                            ? __ldcg(reinterpret_cast<const float4*>(
-                                                         p.part_o + (static_cast<int64_t>(sl[q2 + h2]) * 128 + r0 + it / C4) * D) +
-                                                     it % C4)
-                                            : make_float4(0.f, 0.f, 0.f, 0.f);
-                        }
-#pragma unroll
-                    for (int h2 = 0; h2 < 2; ++h2)
-#pragma unroll
-                        for (int k8 = 0; k8 < 8; ++k8) {  // fragment order: q2, then q2 + 1
-                            const int it = base + k8 * 128 + t;
-                            const float w = (it < items && q2 + h2 < nfr) ? wsm[(q2 + h2) * 128 + it / C4] : 0.0f;
-                            acc[k8].x += w * x[h2][k8].x;
-                            acc[k8].y += w * x[h2][k8].y;
-                            acc[k8].z += w * x[h2][k8].z;
-                            acc[k8].w += w * x[h2][k8].w;
-                        }
+            for (int it = t; it < items; it += 128) {
+                const int rl = it / C4, c4 = it % C4;
+                float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int q2 = 0; q2 < nfr; ++q2) {  // fragment order
+                    const float w = wsm[q2 * 128 + rl];
+                    const float4 x = reinterpret_cast<const float4*>(stage + (q2 * nrows + rl) * D)[c4];
+                    acc.x += w * x.x;
+                    acc.y += w * x.y;
+                    acc.z += w * x.z;
+                    acc.w += w * x.w;
                 }
-#pragma unroll
-                for (int k8 = 0; k8 < 8; ++k8) {
-                    const int it = base + k8 * 128 + t;
-                    if (it >= items) continue;
-                    const int rl = it / C4, row = r0 + rl;
-                    const int qb2 = pm.qb0 + (row >> 6), rr2 = row & 63;
-                    if (rr2 >= p.b || qb2 >= p.nqb) continue;
-                    const float inv = wsm[8 * 128 + rl];
-                    uint2 w2;
-                    w2.x = pack_bf16x2(acc[k8].x * inv, acc[k8].y * inv);
-                    w2.y = pack_bf16x2(acc[k8].z * inv, acc[k8].w * inv);
-                    *reinterpret_cast<uint2*>(p.o + orow_offset(pm.u, qb2, rr2) + (it % C4) * 4) = w2;
-                }
+                const int row = r0 + rl;
+                const int qb2 = pm.qb0 + (row >> 6), rr2 = row & 63;
+                if (rr2 >= p.b || qb2 >= p.nqb) continue;
+                const float inv = wsm[8 * 128 + rl];
+                uint2 w2;
+                w2.x = pack_bf16x2(acc.x * inv, acc.y * inv);
+                w2.y = pack_bf16x2(acc.z * inv, acc.w * inv);
+                *reinterpret_cast<uint2*>(p.o + orow_offset(pm.u, qb2, rr2) + c4 * 4) = w2;
             }
             named_bar_sync(1, 128);  // wsm is rewritten by the next merge
             if (t == 0) {

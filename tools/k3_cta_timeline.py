@@ -48,7 +48,7 @@ while True:
     i += 1
 for _ in range(3):
     call(*sets[0], pb.MODE_DENOISE)
-buf = torch.zeros(15 * 256 + 8 * 1024 + 1024, dtype=torch.int64, device=dev)
+buf = torch.zeros(15 * 256 + 10 * 1024, dtype=torch.int64, device=dev)
 fn = _capi.LIB.pbsa_debug_trace_buffer
 fn.argtypes = [ctypes.c_void_p]
 torch.cuda.synchronize()
@@ -83,3 +83,13 @@ if len(mv):
     print(f"merge duration: min {mv.min():.1f} med {np.median(mv):.1f} max {mv.max():.1f} us")
 ep = rel[:, 4] - rel[:, 3]
 print(f"last P -> partial written: med {np.median(ep[rel[:, 4] >= 0]) if (rel[:, 4] >= 0).any() else -1:.1f} us")
+ent = buf[15 * 256 + 9 * 1024: 15 * 256 + 9 * 1024 + grid].cpu().numpy()
+print(f"entries per CTA: min {ent.min()} med {int(np.median(ent))} max {ent.max()}")
+rate = work / np.maximum(ent, 1) * 1e3
+print(f"ns per entry (first S -> last P): min {rate.min():.0f} med {np.median(rate):.0f} max {rate.max():.0f}")
+# SMs hosting two CTAs: per-SM total entries and the later CTA's finish time
+tot = {sm: sum(int(ent[c]) for c in cs) for sm, cs in per_sm.items()}
+fin = {sm: max(rel[c, 3] for c in cs) for sm, cs in per_sm.items()}
+v = np.array([tot[s] for s in per_sm]); f = np.array([fin[s] for s in per_sm])
+print(f"per-SM entries: min {v.min()} med {int(np.median(v))} max {v.max()}; per-SM last P: min {f.min():.1f} med {np.median(f):.1f} max {f.max():.1f}")
+print("corr(per-SM entries, per-SM finish):", float(np.corrcoef(v, f)[0, 1]))
