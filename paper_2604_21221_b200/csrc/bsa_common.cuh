@@ -36,7 +36,7 @@ struct BsaParams {
     int lat;        // q / o are chunk latents (LatentGeom lg), not block-major [units][n_q][d]
     LatentGeom lg;
     long long* trace;  // perf experiments only: per-event clock64 stamps of CTA 0 (null = off)
-    int ablate;  // perf experiments only (PBSA_ABLATE): 1 no softmax math, 2 no K/V loads, 3 no MMAs
+    int ablate;  // perf experiments only (PBSA_ABLATE): bit 0 no softmax math, bit 1 no K/V loads, bit 2 no MMAs
     // schedule: `whole_waves` rounds of one whole tile per CTA (tile = cta + w * grid), then the
     // remaining tiles [tail_base, n_tiles) split stream-K over the first tail_grid CTAs
     int tiles_per_unit, n_tiles, grid;

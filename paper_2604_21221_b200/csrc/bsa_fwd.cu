@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                         mbar_wait(v_empty + s, ((j / NSV) & 1) ^ 1);
                         const int row0 = (fm.u * p.n_slots + list_slot<L16>(list, fm.e0 + idx)) * 64;
                         if (elect_one()) {
-                            if (p.ablate == 2) {  // experiment: no K/V traffic
+                            if (p.ablate & 2) {  // experiment: no K/V traffic
                                 mbar_arrive(v_full + s);
                             } else {
                                 mbar_arrive_expect_tx(v_full + s, L::kKVBytes);
@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                         mbar_wait(k_empty + s, ((j / NSK) & 1) ^ 1);
                         const int row0 = (fm.u * p.n_slots + list_slot<L16>(list, fm.e0 + idx)) * 64;
                         if (elect_one()) {
-                            if (p.ablate == 2) {
+                            if (p.ablate & 2) {
                                 mbar_arrive(k_full + s);
                             } else {
                                 mbar_arrive_expect_tx(k_full + s, L::kKVBytes);
@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         {
             constexpr uint32_t idesc_s = idesc_bf16_f32(128, 64, 0, 0);
             constexpr uint32_t idesc_o = idesc_bf16_f32(128, D, 0, 1);
-            const bool do_mma = p.ablate != 3;
+            const bool do_mma = (p.ablate & 4) == 0;
             const uint64_t qdesc = smem_desc_sw128(smem_u32(q_smem), 16, 1024);
             const uint64_t kdesc = smem_desc_sw128(smem_u32(k_smem), 16, 1024);
             const uint64_t vdesc = smem_desc_sw128(smem_u32(v_smem), 8192, 1024);
@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 const uint32_t t_s = t_o + L::kSColBase + buf * 64;
                 // rows of one warp all lie in one half -> visibility is warp-uniform
                 const uint32_t ent = L16 ? ld_shared_u16(list_s + idx * 2) : ld_shared_u32(list_s + idx * 4);
-                const bool vis = ((ent >> (mshift + half)) & 1) && p.ablate != 1;
+                const bool vis = ((ent >> (mshift + half)) & 1) && (p.ablate & 1) == 0;
                 if (vis) {
                     uint32_t pk[32];
                     float sv[64];

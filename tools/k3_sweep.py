@@ -4,6 +4,8 @@
 PBSA_ABLATE=1 makes the softmax warps skip their math (pipeline / tensor-core upper bound)."""
 import os
 import sys
+import threading
+import time
 
 import torch
 
@@ -35,12 +37,28 @@ for sk in ((True,) if os.environ.get("PBSA_SWEEP_SK_ONLY") else (True, False)):
         pb.attention_sparse(q, kp, vp, dense, local, sel, b, stream_k=sk)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
-    reps = 20
+    reps = int(os.environ.get("REPS", 20))
+    clk = []
+    stop = threading.Event()
+
+    def sample():  # SM clock under load (power capping shows here, not in the max clock)
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
+        while not stop.is_set():
+            clk.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+            time.sleep(0.002)
+
+    th = threading.Thread(target=sample)
+    th.start()
     e0.record()
     for _ in range(reps):
         pb.attention_sparse(q, kp, vp, dense, local, sel, b, stream_k=sk)
     e1.record()
     torch.cuda.synchronize()
+    stop.set()
+    th.join()
     ms = e0.elapsed_time(e1) / reps
     print(f"ablate={os.environ.get('PBSA_ABLATE', '0')} stream_k={sk} ms={ms:.4f} alg_TFLOPs={alg / ms / 1e9:.1f} "
-          f"exec_TFLOPs={exe / ms / 1e9:.1f} exec/alg={exe / alg:.3f}")
+          f"exec_TFLOPs={exe / ms / 1e9:.1f} exec/alg={exe / alg:.3f} "
+          f"sm_mhz_median={sorted(clk)[len(clk) // 2] if clk else 0}")
