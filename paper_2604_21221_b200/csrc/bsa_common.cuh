@@ -288,7 +288,7 @@ inline int encode_k3_maps(const bf16* q, const bf16* kp, const bf16* vp, const B
     }
     const uint64_t dims[2] = {static_cast<uint64_t>(D), static_cast<uint64_t>(p.units) * p.n_slots * 64};
     const uint64_t strides[1] = {static_cast<uint64_t>(D) * 2};
-    const uint32_t box[2] = {64, 64};
+    const uint32_t box[2] = {64, static_cast<uint32_t>(p.b)};  // the b valid rows of a 64-row slot
     if (!encode_tmap_bf16(tk, kp, 2, dims, strides, box, &err)) return set_error(PBSA_ECUDA, "tensor map K: " + err);
     if (!encode_tmap_bf16(tv, vp, 2, dims, strides, box, &err)) return set_error(PBSA_ECUDA, "tensor map V: " + err);
     return PBSA_OK;

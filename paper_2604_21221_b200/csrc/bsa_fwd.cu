@@ -165,6 +165,13 @@ __global__ void __launch_bounds__(kThreads, 2)
             if ((row & 63) >= p.b)
                 *reinterpret_cast<uint4*>(q_smem + h * 16384 + row * 128 + chunk * 16) = make_uint4(0, 0, 0, 0);
         }
+        // likewise the rows >= b of every K and V ring slot: the K/V boxes carry the b valid rows of a
+        // pool slot only (6 % less L2 -> SM traffic at b = 60); zero rows keep S finite and P V exact
+        for (int e = t; e < (NSK + NSV) * L::kHalves * 64 * 8; e += 128) {
+            const int chunk = e & 7, row = (e >> 3) & 63, sh = e >> 9;  // sh = ring slot * kHalves + half
+            if (row >= p.b)
+                *reinterpret_cast<uint4*>(k_smem + sh * 8192 + row * 128 + chunk * 16) = make_uint4(0, 0, 0, 0);
+        }
         fence_proxy_async_smem();
     }
     tc_fence_before();
@@ -183,6 +190,9 @@ __global__ void __launch_bounds__(kThreads, 2)
             // The producer also builds each fragment's visible list (double-buffered): list f+1 is
             // built while the MMA / softmax warps still work on the last blocks of fragment f.
             int jg = 0, q_uses = 0;
+            // a K / V box covers the slot's b valid rows only (rows >= b of the ring slots were zeroed
+            // at setup and are never written by TMA)
+            const uint32_t kv_tx = static_cast<uint32_t>(L::kHalves) * static_cast<uint32_t>(p.b) * 128u;
             for (int f = 0; f < n_frag; ++f) {
                 const int lb = f & 1;
                 mbar_wait(list_empty + lb, ((f >> 1) & 1) ^ 1);
@@ -228,7 +238,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                             if (p.ablate & 2) {  // experiment: no K/V traffic
                                 mbar_arrive(v_full + s);
                             } else {
-                                mbar_arrive_expect_tx(v_full + s, L::kKVBytes);
+                                mbar_arrive_expect_tx(v_full + s, kv_tx);
                                 for (int h = 0; h < L::kHalves; ++h)
                                     tma_load_2d(v_smem + s * L::kKVBytes + h * 8192, &tm_v, v_full + s, h * 64, row0);
                             }
@@ -244,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                             if (p.ablate & 2) {
                                 mbar_arrive(k_full + s);
                             } else {
-                                mbar_arrive_expect_tx(k_full + s, L::kKVBytes);
+                                mbar_arrive_expect_tx(k_full + s, kv_tx);
                                 for (int h = 0; h < L::kHalves; ++h)
                                     tma_load_2d(k_smem + s * L::kKVBytes + h * 8192, &tm_k, k_full + s, h * 64, row0);
                             }
@@ -791,6 +801,15 @@ int launch_bsa_fwd(const bf16* q, const bf16* k_pool, const bf16* v_pool, int n_
     return l16 ? launch_impl<DD, NS, NS, BB, kPolyMask, true>(q, k_pool, v_pool, p, s)            \
                : launch_impl<DD, NS, NS, BB, kPolyMask, false>(q, k_pool, v_pool, p, s)
     if (d == 128) {
+#ifdef PBSA_K3_POLY_EXPERIMENT
+        {
+            static const int pm = getenv("PBSA_K3_POLY") ? atoi(getenv("PBSA_K3_POLY")) : 0;
+            if (b == 60 && pm == 1) return launch_impl<128, 2, 2, 60, 0x00010001u, false>(q, k_pool, v_pool, p, s);
+            if (b == 60 && pm == 2) return launch_impl<128, 2, 2, 60, 0x01010101u, false>(q, k_pool, v_pool, p, s);
+            if (b == 60 && pm == 3) return launch_impl<128, 2, 2, 60, 0x11111111u, false>(q, k_pool, v_pool, p, s);
+            if (b == 60 && pm == 4) return launch_impl<128, 2, 2, 60, 0x10001000u, false>(q, k_pool, v_pool, p, s);
+        }
+#endif
         if (b == 60) PBSA_K3(128, 2, 60);
         if (b == 64) PBSA_K3(128, 2, 64);
         PBSA_K3(128, 2, 0);

@@ -27,7 +27,7 @@ dense, local = perm[:, :nd].contiguous(), perm[:, nd:nd + nl].contiguous()
 sel = torch.stack([torch.stack([torch.randperm(nl, device="cuda", generator=g)[:k].sort().values
                                 for _ in range(nqb)]) for _ in range(U)]).int().contiguous()
 args = (q, kp, vp, dense, local, sel, b)
-o, lse = pb.attention_sparse(*args, want_lse=True)
+o, lse = pb.attention_sparse(*args, want_lse=True, validate=False)
 buf = torch.zeros(10 * 256, dtype=torch.int64, device="cuda")
 fn = _capi.LIB.pbsa_debug_bwd_trace_buffer
 fn.argtypes = [ctypes.c_void_p]

@@ -57,18 +57,18 @@ def union_stats(s):
     return round(sz.mean().item(), 1), round(inter / len(sizes), 1), round(sz.std().item(), 1), per_unit_max
 
 
-ms_real = timeit(lambda: pb.attention_sparse(q, kp, vp, dense, local, sel, b), reps=3, warm=1)
+ms_real = timeit(lambda: pb.attention_sparse(q, kp, vp, dense, local, sel, b, validate=False), reps=3, warm=1)
 print("real tables: ms", ms_real, "plan", pb.bsa_fwd_last_plan().schedule, "union mean / intersection / union std / mean per-unit max union", union_stats(sel))
 S = kp.shape[1]
 sd, sl, ss = synth_tables(U, S, nd, inf.n_l, bpc, k, g)
-ms_syn = timeit(lambda: pb.attention_sparse(q, kp, vp, sd, sl, ss, b), reps=3, warm=1)
+ms_syn = timeit(lambda: pb.attention_sparse(q, kp, vp, sd, sl, ss, b, validate=False), reps=3, warm=1)
 print("synthetic tables (same pools): ms", ms_syn, "union/intersection per tile", union_stats(ss))
-ms_mix = timeit(lambda: pb.attention_sparse(q, kp, vp, dense, local, ss, b), reps=3, warm=1)
+ms_mix = timeit(lambda: pb.attention_sparse(q, kp, vp, dense, local, ss, b, validate=False), reps=3, warm=1)
 print("real slot lists + synthetic selections: ms", ms_mix)
 os.environ["PBSA_K3_GANG"] = "0"
 print("no gangs: real %.1f ms, synthetic %.1f ms" % (
-    timeit(lambda: pb.attention_sparse(q, kp, vp, dense, local, sel, b), reps=2, warm=1),
-    timeit(lambda: pb.attention_sparse(q, kp, vp, dense, local, ss, b), reps=2, warm=1)))
+    timeit(lambda: pb.attention_sparse(q, kp, vp, dense, local, sel, b, validate=False), reps=2, warm=1),
+    timeit(lambda: pb.attention_sparse(q, kp, vp, dense, local, ss, b, validate=False), reps=2, warm=1)))
 del os.environ["PBSA_K3_GANG"]
 # how often each local block is selected across a unit's query blocks
 s0 = sel[0].flatten().cpu()

@@ -21,6 +21,8 @@ kp[:, :, :b] = torch.randn(U, S, b, d, device="cuda", generator=g).bfloat16()
 vp[:, :, :b] = torch.randn(U, S, b, d, device="cuda", generator=g).bfloat16()
 q = torch.randn(U, nqb * b, d, device="cuda", generator=g).bfloat16()
 perm = torch.stack([torch.randperm(S, device="cuda", generator=g) for _ in range(U)]).int()
+if os.environ.get("SEQ_SLOTS"):  # dense = slots [0, nd), local = [nd, nd + nl) in order (a Memory's layout)
+    perm = torch.arange(S, device="cuda", dtype=torch.int32).repeat(U, 1)
 dense = perm[:, :nd].contiguous()
 local = perm[:, nd:nd + nl].contiguous()
 sel = torch.stack([torch.stack([torch.randperm(nl, device="cuda", generator=g)[:k].sort().values
@@ -34,11 +36,11 @@ for u in range(U):
 exe = 4.0 * 128 * 64 * d * un
 for sk in ((True,) if os.environ.get("PBSA_SWEEP_SK_ONLY") else (True, False)):
     for _ in range(3):
-        pb.attention_sparse(q, kp, vp, dense, local, sel, b, stream_k=sk)
+        pb.attention_sparse(q, kp, vp, dense, local, sel, b, stream_k=sk, validate=False)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     reps = int(os.environ.get("REPS", 20))
-    clk = []
+    clk, pw = [], []
     stop = threading.Event()
 
     def sample():  # SM clock under load (power capping shows here, not in the max clock)
@@ -47,18 +49,31 @@ for sk in ((True,) if os.environ.get("PBSA_SWEEP_SK_ONLY") else (True, False)):
         h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
         while not stop.is_set():
             clk.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+            pw.append(pynvml.nvmlDeviceGetPowerUsage(h) / 1000.0)
             time.sleep(0.002)
 
     th = threading.Thread(target=sample)
     th.start()
-    e0.record()
-    for _ in range(reps):
-        pb.attention_sparse(q, kp, vp, dense, local, sel, b, stream_k=sk)
-    e1.record()
-    torch.cuda.synchronize()
+    gap = int(os.environ.get("GAP_CYCLES", 0))  # idle gap between launches (power / clock study)
+    if gap:
+        ev = [(torch.cuda.Event(True), torch.cuda.Event(True)) for _ in range(reps)]
+        for a, z in ev:
+            torch.cuda._sleep(gap)
+            a.record()
+            pb.attention_sparse(q, kp, vp, dense, local, sel, b, stream_k=sk, validate=False)
+            z.record()
+        torch.cuda.synchronize()
+        ms = sorted(a.elapsed_time(z) for a, z in ev)[reps // 2]
+    else:
+        e0.record()
+        for _ in range(reps):
+            pb.attention_sparse(q, kp, vp, dense, local, sel, b, stream_k=sk, validate=False)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
     stop.set()
     th.join()
-    ms = e0.elapsed_time(e1) / reps
     print(f"ablate={os.environ.get('PBSA_ABLATE', '0')} stream_k={sk} ms={ms:.4f} alg_TFLOPs={alg / ms / 1e9:.1f} "
           f"exec_TFLOPs={exe / ms / 1e9:.1f} exec/alg={exe / alg:.3f} "
-          f"sm_mhz_median={sorted(clk)[len(clk) // 2] if clk else 0}")
+          f"sm_mhz_median={sorted(clk)[len(clk) // 2] if clk else 0} "
+          f"power_w_median={sorted(pw)[len(pw) // 2] if pw else 0:.0f}")

@@ -35,7 +35,7 @@ o, lse = pb.attention_sparse(q, kp, vp, dense, local, sel, b, want_lse=True)
 grads = pb.attention_sparse_backward(q, kp, vp, dense, local, sel, b, o, lse, do)
 # unit-gang K3 schedule (forced) and a 16-bit-list launch
 os.environ["PBSA_K3_GANG"] = "1"
-pb.attention_sparse(q, kp, vp, dense, local, sel, b)
+pb.attention_sparse(q, kp, vp, dense, local, sel, b, validate=False)
 del os.environ["PBSA_K3_GANG"]
 # query-split calls (2 replicas of the same heads) and the drop-sink fault path of K4
 parts = [pb.Memory(U, C, W, bpc, b, d) for _ in range(2)]
