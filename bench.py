@@ -360,7 +360,9 @@ def run_ours(args, rank, world, local_rank):
     time.sleep(0.3)
 
     # ---------------------------------------------------------------- timed: device-resident
-    mem.profile(True, max_calls=(T + 1) * args.steps + 8)
+    # Pass 1 (the headline): the K chunk steps exactly as a caller issues them -- no instrumentation
+    # inside the region (per-stage events between the kernels cost ~0.15 ms per chunk: they break
+    # the programmatic-dependent-launch chain ingest -> K2 -> K3 -> K4).
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     torch.cuda.synchronize()
@@ -375,6 +377,20 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     ms_total = max_over_ranks(e0.elapsed_time(e1))
     gpu_launches = int(_LIB.pbsa_launch_count() - launches0)  # the library's kernels in the timed region
+    # Pass 2 (the roofline and stage shares): the same K steps again with the library's per-stage
+    # CUDA events on the launching stream (pbsa_mem_profile) -- K3's average launch duration
+    mem.profile(True, max_calls=(T + 1) * args.steps + 8)
+    barrier()
+    torch.cuda.synchronize()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for s in range(args.steps):
+        chunk_step(args.steps + s)
+    drain()
+    e3.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms_total_prof = max_over_ranks(e2.elapsed_time(e3))
     prof = mem.profile_read()
     mem.profile(False)
     ms_step = ms_total / args.steps
@@ -410,14 +426,17 @@ def run_ours(args, rank, world, local_rank):
                 "traffic": traffic, "traffic_source": traffic_src,
                 "peak_kind": "burst bf16 (short timed region at max SM clock), " + peaks["source"],
                 "peak_sustained": peaks["bf16_sustained"], "frac_of_sustained": k3_alg / peaks["bf16_sustained"],
-                "avg_launch_ms": k3_ms, "algorithmic_flops_per_launch": alg_flops_call_rank,
+                "avg_launch_ms": k3_ms, "launch_timing": "CUDA events around every K3 launch on its stream, "
+                "in a second timed pass of the same K steps (the headline pass has no events between kernels)",
+                "ms_per_step_profiled_pass": ms_total_prof / args.steps,
+                "algorithmic_flops_per_launch": alg_flops_call_rank,
                 "algorithmic_flops_rule": "4*b*d per (query token, visible key token) pair, valid tokens "
                                           "only (SPEC flop_count sparse term, SURVEY 8(d))"}
     if exec_flops_call:
         roofline["executed_flops_per_launch"] = exec_flops_call
         roofline["achieved_executed"] = exec_flops_call / (k3_ms * 1e-3) / 1e12
         roofline["frac_executed"] = roofline["achieved_executed"] / peaks["bf16"]
-    stage_share = {k: v / ms_total for k, v in prof["ms"].items()}
+    stage_share = {k: v / ms_total_prof for k, v in prof["ms"].items()}
 
     # ---------------------------------------------------------------- timed: end to end (host buffers)
     e2e = None
