@@ -697,8 +697,6 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
 }
 
-#include "bsa_fwd_pair.cuh"
-
 template <int D, int NSK, int NSV, int B, uint32_t POLY, bool L16>
 int launch_impl(const bf16* q, const bf16* kp, const bf16* vp, BsaParams p, cudaStream_t s) {
     using L = Layout<D, NSK, NSV>;
@@ -794,24 +792,6 @@ int launch_bsa_fwd(const bf16* q, const bf16* k_pool, const bf16* v_pool, int n_
         p.part_ml = p.part_o + slots * 128 * d;
         p.counters = reinterpret_cast<int*>(p.part_ml + slots * 256);
         p.gang_ctr = p.counters + p.n_tiles;
-    }
-    // paired-block variant (bsa_fwd_pair.cuh): PBSA_K3_PAIR=1 forces it, 0 forbids it
-    {
-        static const char* env = getenv("PBSA_K3_PAIR");
-        const int want = env ? atoi(env) : 0;
-        if (want == 1 && d == 128) {
-            const size_t sm32 = PairLayout<128, 2, 4>::bytes(p.max_list, p.bm_words, 4);
-            const bool l16p = n_slots < 16384 && sm32 > 227 * 1024;
-            static const int pm = getenv("PBSA_K3_POLY") ? atoi(getenv("PBSA_K3_POLY")) : 0;
-            if (b == 60 && !l16p && pm == 1) return launch_pair_impl<128, 2, 4, 60, 0x11111111u, false>(q, k_pool, v_pool, p, s);
-            if (b == 60 && !l16p && pm == 2) return launch_pair_impl<128, 2, 4, 60, 0x55555555u, false>(q, k_pool, v_pool, p, s);
-            if (b == 60 && !l16p && pm == 3) return launch_pair_impl<128, 2, 4, 60, 0x01010101u, false>(q, k_pool, v_pool, p, s);
-            if (b == 60)
-                return l16p ? launch_pair_impl<128, 2, 4, 60, 0u, true>(q, k_pool, v_pool, p, s)
-                            : launch_pair_impl<128, 2, 4, 60, 0u, false>(q, k_pool, v_pool, p, s);
-            return l16p ? launch_pair_impl<128, 2, 4, 0, 0u, true>(q, k_pool, v_pool, p, s)
-                        : launch_pair_impl<128, 2, 4, 0, 0u, false>(q, k_pool, v_pool, p, s);
-        }
     }
     // 16-bit visible-list entries only where 32-bit lists would cost the second CTA per SM (long
     // lists, e.g. config 5) and the pool is small enough to index with 14 bits
