@@ -103,6 +103,8 @@ def cpu_sample(n_qb=4, seed=0):
     (coarse + memory work + the fine attention scaled from n_qb to 78 query blocks)."""
     import numpy as np
     from oracle import oracle as orc
+    # every host core this process may use (torchrun exports OMP_NUM_THREADS=1 to its ranks)
+    orc.set_num_threads(len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1))
     g = GEOM
     rng = np.random.default_rng(seed)
     n_dense = g["C"] + g["bpc"]
