@@ -671,14 +671,14 @@ __global__ void __launch_bounds__(kCertThreads, 3) cert_select_kernel(const Scor
 //   logits_t_kernel  8 query rows x 4 keys per thread (4x fewer shared-memory q reads per DFMA than
 //                    one key per thread), logits stored key-major: zt[j][R], R = u*nqb + i, so that
 //   row_denom_kernel thread per row R: fp32 max and the ascending-j fp64 denominator (the only
-//                    sequential part), with the next 8 logits loaded ahead of the add chain
+//                    sequential part; at the k=0 pass row_denom2_kernel does the local-window and the
+//                    full-row statistics in one pass), with the next 8 logits loaded ahead of the
+//                    add chain
 //   row_prob_kernel  fully parallel fp32 probabilities, row-major through a 32x32 smem transpose
 //   topk_rows_kernel warp per row: radix select over the row's probability bits.
 // The operation sequence per row is the same as warp_softmax / warp_topk above (and the oracle).
-constexpr int kKeysPerThread = 4;
-
-template <int D>
-__global__ void __launch_bounds__(256, 2) logits_t_kernel(const ScoreParams p, float* __restrict__ zt) {
+template <int D, int kKeysPerThread, int kMinBlocks>
+__global__ void __launch_bounds__(256, kMinBlocks) logits_t_kernel(const ScoreParams p, float* __restrict__ zt) {
     pdl_wait();  // programmatic dependent launch: upstream outputs are visible from here on
     __shared__ __align__(16) double qd[kMaxRows * D];
     const int u = blockIdx.y, i0 = blockIdx.x * kMaxRows;
@@ -802,6 +802,88 @@ __global__ void __launch_bounds__(128) row_denom_kernel(const float* __restrict_
     for (; j < n; ++j) denom = __dadd_rn(denom, exp(static_cast<double>(__ldg(z + j * rt)) - dm));
     mrow[R] = m;
     drow[R] = denom;
+}
+
+// The k=0 pass needs two softmaxes of every row: over the local window [off, off + nl) (for the
+// Top-K) and over all n keys (A_t for s_t).  One thread per row R computes both maxima in one pass
+// over the key-major logits and both ascending fp64 denominators in a second pass -- the same
+// operation sequences as two row_denom_kernel launches, with half the logit traffic.
+__global__ void __launch_bounds__(128) row_denom2_kernel(const float* __restrict__ zt, int64_t rt, int off, int nl,
+                                                         int n, float* __restrict__ mrow_l, double* __restrict__ drow_l,
+                                                         float* __restrict__ mrow_f, double* __restrict__ drow_f,
+                                                         int* status) {
+    pdl_wait();  // programmatic dependent launch: upstream outputs are visible from here on
+    const int lane = threadIdx.x & 31;
+    const int64_t R = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const bool live = R < rt;
+    const float* z = zt + (live ? R : 0);
+    float ml = -FLT_MAX, mf = -FLT_MAX;
+    bool bad = false;
+    if (live) {
+        // maxima: [0, off) and [off + nl, n) feed the full row only, [off, off + nl) both
+        auto seg_max = [&](int j0, int j1) {
+            float mq[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) mq[q] = -FLT_MAX;
+            int j = j0;
+            for (; j + 8 <= j1; j += 8) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const float a = __ldg(z + static_cast<int64_t>(j + q) * rt);
+                    bad |= a != a;
+                    mq[q] = fmaxf(mq[q], a);
+                }
+            }
+            float m = -FLT_MAX;
+            for (; j < j1; ++j) {
+                const float a = __ldg(z + static_cast<int64_t>(j) * rt);
+                bad |= a != a;
+                m = fmaxf(m, a);
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) m = fmaxf(m, mq[q]);  // max is exact: order-free
+            return m;
+        };
+        const float m0 = seg_max(0, off), m1 = seg_max(off, off + nl), m2 = seg_max(off + nl, n);
+        ml = m1;
+        mf = fmaxf(fmaxf(m0, m1), m2);
+    }
+    if (status != nullptr && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(status, 1);
+    if (!live) return;
+    const double dl = static_cast<double>(ml), df = static_cast<double>(mf);
+    double sl = 0.0, sf = 0.0;
+    // ascending j; inside the window both chains advance, each in its own ascending order
+    auto seg_sum = [&](int j0, int j1, bool both) {
+        int j = j0;
+        for (; j + 8 <= j1; j += 8) {
+            float zc[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) zc[q] = __ldg(z + static_cast<int64_t>(j + q) * rt);
+            double ef[8], el[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                ef[q] = exp(static_cast<double>(zc[q]) - df);
+                el[q] = both ? exp(static_cast<double>(zc[q]) - dl) : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                sf = __dadd_rn(sf, ef[q]);
+                if (both) sl = __dadd_rn(sl, el[q]);
+            }
+        }
+        for (; j < j1; ++j) {
+            const double zj = static_cast<double>(__ldg(z + static_cast<int64_t>(j) * rt));
+            sf = __dadd_rn(sf, exp(zj - df));
+            if (both) sl = __dadd_rn(sl, exp(zj - dl));
+        }
+    };
+    seg_sum(0, off, false);
+    seg_sum(off, off + nl, true);
+    seg_sum(off + nl, n, false);
+    mrow_l[R] = ml;
+    drow_l[R] = sl;
+    mrow_f[R] = mf;
+    drow_f[R] = sf;
 }
 
 // p[R][j] = float(exp(double(z[j][R]) - double(m_R)) / denom_R), fully parallel: a CTA converts a
@@ -967,9 +1049,10 @@ int launch_score_select(const float* qc, const float* krep, int64_t kru, const i
             const int64_t rt = static_cast<int64_t>(units) * nqb;
             float* zt = static_cast<float*>(ws) + static_cast<size_t>(rt) * n_keys;
             float* prob = zt + static_cast<size_t>(rt) * n_keys;
-            dim3 g1((nqb + kMaxRows - 1) / kMaxRows, units, (n_keys + 256 * kKeysPerThread - 1) / (256 * kKeysPerThread));
-            if (d == 128) launch_pdl(logits_t_kernel<128>, g1, dim3(256), 0, s, p, zt);
-            else launch_pdl(logits_t_kernel<64>, g1, dim3(256), 0, s, p, zt);
+            // 4 keys x 8 rows per thread at two CTAs per SM (2 keys at three CTAs measured slower)
+            dim3 g1((nqb + kMaxRows - 1) / kMaxRows, units, (n_keys + 256 * 4 - 1) / (256 * 4));
+            if (d == 128) launch_pdl(logits_t_kernel<128, 4, 2>, g1, dim3(256), 0, s, p, zt);
+            else launch_pdl(logits_t_kernel<64, 4, 2>, g1, dim3(256), 0, s, p, zt);
             if (int rc = check_launch("logits_t_kernel")) return rc;
             float* mrow = prob + static_cast<size_t>(rt) * n_keys;
             double* drow = reinterpret_cast<double*>(mrow + ((rt + 1) & ~int64_t(1)));
@@ -982,14 +1065,34 @@ int launch_score_select(const float* qc, const float* krep, int64_t kru, const i
                            static_cast<const float*>(mrow), static_cast<const double*>(drow), out);
                 return check_launch("row_prob_kernel");
             };
-            if (do_select) {
-                if (int rc = softmax_rows(local_off, n_local, prob, status)) return rc;
+            if (do_select && arows != nullptr) {
+                // k=0 pass: both softmaxes' statistics in one pass over the logits
+                float* mrow_f = reinterpret_cast<float*>(drow + ((rt + 1) & ~int64_t(1)));
+                double* drow_f = reinterpret_cast<double*>(mrow_f + ((rt + 1) & ~int64_t(1)));
+                launch_pdl(row_denom2_kernel, dim3(gr), dim3(128), 0, s, static_cast<const float*>(zt), rt, local_off,
+                           n_local, n_keys, mrow, drow, mrow_f, drow_f, status);
+                if (int rc = check_launch("row_denom2_kernel")) return rc;
+                dim3 g2((n_local + 31) / 32, static_cast<unsigned>((rt + 31) / 32));
+                launch_pdl(row_prob_kernel, g2, dim3(256), 0, s, static_cast<const float*>(zt), rt, local_off, n_local,
+                           static_cast<const float*>(mrow), static_cast<const double*>(drow), prob);
+                if (int rc = check_launch("row_prob_kernel")) return rc;
                 launch_pdl(topk_rows_kernel, dim3(static_cast<unsigned>((rt + 7) / 8)), dim3(256), 0, s,
                            static_cast<const float*>(prob), n_local, k, rt, sel);
                 if (int rc = check_launch("topk_rows_kernel")) return rc;
-            }
-            if (arows != nullptr) {
-                if (int rc = softmax_rows(0, n_keys, arows, do_select ? nullptr : status)) return rc;
+                dim3 g3((n_keys + 31) / 32, static_cast<unsigned>((rt + 31) / 32));
+                launch_pdl(row_prob_kernel, g3, dim3(256), 0, s, static_cast<const float*>(zt), rt, 0, n_keys,
+                           static_cast<const float*>(mrow_f), static_cast<const double*>(drow_f), arows);
+                if (int rc = check_launch("row_prob_kernel")) return rc;
+            } else {
+                if (do_select) {
+                    if (int rc = softmax_rows(local_off, n_local, prob, status)) return rc;
+                    launch_pdl(topk_rows_kernel, dim3(static_cast<unsigned>((rt + 7) / 8)), dim3(256), 0, s,
+                               static_cast<const float*>(prob), n_local, k, rt, sel);
+                    if (int rc = check_launch("topk_rows_kernel")) return rc;
+                }
+                if (arows != nullptr) {
+                    if (int rc = softmax_rows(0, n_keys, arows, do_select ? nullptr : status)) return rc;
+                }
             }
         } else {
             // row-major logits into the workspace (after the A_t rows), then warp-per-row select
