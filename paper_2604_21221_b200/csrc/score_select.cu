@@ -716,17 +716,23 @@ __global__ void __launch_bounds__(256, kMinBlocks) logits_t_kernel(const ScorePa
             kd[q][2] = kv.z;
             kd[q][3] = kv.w;
         }
+        // column by column: the 8 x kKeysPerThread DFMAs of one column are independent (one per
+        // accumulator), so consecutive DFMAs never wait on each other; each accumulator still adds
+        // its columns in ascending c (3.88 -> 3.56 ms at config 5).  Staging the key rows through
+        // shared memory with cp.async instead measured slower (4.30 ms).
 #pragma unroll
-        for (int r = 0; r < kMaxRows; ++r) {
-            const double2 qa = *reinterpret_cast<const double2*>(qd + r * D + 4 * c4);
-            const double2 qb = *reinterpret_cast<const double2*>(qd + r * D + 4 * c4 + 2);
+        for (int h = 0; h < 2; ++h) {
+            double2 qv[kMaxRows];
 #pragma unroll
-            for (int q = 0; q < kKeysPerThread; ++q) {  // ascending c per (row, key)
-                acc[q][r] = __fma_rn(qa.x, kd[q][0], acc[q][r]);
-                acc[q][r] = __fma_rn(qa.y, kd[q][1], acc[q][r]);
-                acc[q][r] = __fma_rn(qb.x, kd[q][2], acc[q][r]);
-                acc[q][r] = __fma_rn(qb.y, kd[q][3], acc[q][r]);
-            }
+            for (int r = 0; r < kMaxRows; ++r) qv[r] = *reinterpret_cast<const double2*>(qd + r * D + 4 * c4 + 2 * h);
+#pragma unroll
+            for (int r = 0; r < kMaxRows; ++r)
+#pragma unroll
+                for (int q = 0; q < kKeysPerThread; ++q) acc[q][r] = __fma_rn(qv[r].x, kd[q][2 * h], acc[q][r]);
+#pragma unroll
+            for (int r = 0; r < kMaxRows; ++r)
+#pragma unroll
+                for (int q = 0; q < kKeysPerThread; ++q) acc[q][r] = __fma_rn(qv[r].y, kd[q][2 * h + 1], acc[q][r]);
         }
     }
     const int64_t rt = static_cast<int64_t>(p.units) * p.nqb;
