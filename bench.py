@@ -401,15 +401,19 @@ def run_ours(args, rank, world, local_rank):
 
     # executed FLOPs of K3 from the union lists of the last call
     sel, _ = mem.last_selection()
+    pairs = mem.last_tile_pairs()  # K3 tiles (query blocks paired by Top-K overlap), None: (2t, 2t + 1)
     exec_flops_call = None
     if sel is not None:
         s_np = sel.cpu().numpy()
         if s_np.shape[1] == bpc and qn != bpc:
             s_np = s_np[:, qb0:qb0 + qn]  # the k=0 pass selects every row; this rank attends its own
+        p_np = pairs.cpu().numpy() if pairs is not None else None
         total_blocks = 0
         for u in range(Ul):
-            for t in range(0, qn, 2):
-                un = set(s_np[u, t].tolist()) | (set(s_np[u, t + 1].tolist()) if t + 1 < qn else set())
+            tiles = ([tuple(x) for x in p_np[u]] if p_np is not None else
+                     [(t, t + 1 if t + 1 < qn else -1) for t in range(0, qn, 2)])
+            for a_, b_ in tiles:
+                un = set(s_np[u, a_].tolist()) | (set(s_np[u, b_].tolist()) if b_ >= 0 else set())
                 total_blocks += n_dense + len(un)
         exec_flops_call = 4.0 * 128 * 64 * d * total_blocks
     n_calls = prof["attend_calls"]

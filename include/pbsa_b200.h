@@ -124,6 +124,15 @@ int pbsa_blockify(const float* x, int t, int h, int w, int d, int b_t, int b_h, 
  * (ranked lowest, as K4 does). */
 int pbsa_topc_select(const int64_t* ids, const float* scores, int n, int slots, uint8_t* keep, int* status,
                      void* stream);
+/* K3 tile pairing (scheduling, not a SPEC op; what pbsa_attend runs between K2 and K3): per unit, the
+ * query blocks sel_row0 .. sel_row0 + nq - 1 of sel [units][sel_rows][k] (local indices < n_local) are
+ * paired greedily by Top-K overlap (repeatedly the free pair with the largest overlap, ties to the lowest
+ * i * nq + j); pairs [units][(nq + 1) / 2][2] lists each tile's query blocks (relative to sel_row0) in
+ * that order, an odd leftover last with -1.  PBSA_EUNSUPPORTED when nq > 255, k > 32767 or the
+ * bitsets exceed shared memory.  pbsa_attend pairs automatically for windows of >= 1024 blocks
+ * (PBSA_TILE_PAIRING=0 never, =1 always). */
+int pbsa_pair_tiles(const int32_t* sel, int sel_rows, int sel_row0, int nq, int k, int n_local, int units,
+                    int32_t* pairs, void* stream);
 
 /* Device memory for callers that hold no CUDA runtime of their own (the header-only C++ API):
  * cudaMalloc / cudaFree, cudaMemcpyAsync(cudaMemcpyDefault) and cudaStreamSynchronize. */
@@ -261,6 +270,11 @@ int pbsa_attend_part(pbsa_mem* m, const void* q_part, int q_begin, int q_count, 
 int pbsa_last_selection_rows(const pbsa_mem* m, int* rows);
 int pbsa_last_selection(const pbsa_mem* m, const int32_t** sel, int* k, const float** s_t,
                         int* n_keys);
+/* K3 tiles of the last attend call (device): [units][tiles_per_unit][2] query blocks of the call per
+ * tile (second -1 when the tile has one), paired by largest Top-K overlap; *pairs = NULL when the
+ * call used the natural pairs (2t, 2t + 1) (no selection, or PBSA_TILE_PAIRING=0).  Scheduling
+ * only: the outputs do not depend on it. */
+int pbsa_last_tile_pairs(const pbsa_mem* m, const int32_t** pairs, int* tiles_per_unit);
 
 /* Stage timing with CUDA events recorded on the call's stream (no host sync inside calls).
  * enable: allocate a pool for max_calls calls and reset the sums; 0 disables.  read: waits for

@@ -7,6 +7,7 @@ from .pbsa import (MODE_CACHE_UPDATE, MODE_DENOISE, Memory, PbsaCudaError, PbsaE
                    attention_scale, attention_sparse, attention_sparse_backward, compress_blocks, debug_tile, score_select,
                    latent_blocks, latent_geom, topk_count, TensorIoError, write_tensor,
                    read_tensor, tensor_dims, load_bf16, bsa_fwd_last_plan, debug_set_fault,
-                   matmul, masked_softmax_rows, aggregate_scores, select_topk, blockify, unblockify, topc_select)
+                   matmul, masked_softmax_rows, aggregate_scores, select_topk, blockify, unblockify, topc_select,
+                   pair_tiles)
 
 __version__ = "0.1.0"

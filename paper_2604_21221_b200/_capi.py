@@ -84,6 +84,8 @@ _SIGS = {
     "pbsa_attend_part_ingest": (_i32, [_vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp]),
     "pbsa_attend_part": (_i32, [_vp, _vp, _i32, _i32, _vp, _i32, _f32, _i32, _vp, _vp, _vp]),
     "pbsa_last_selection_rows": (_i32, [_vp, C.POINTER(_i32)]),
+    "pbsa_last_tile_pairs": (_i32, [_vp, C.POINTER(_vp), C.POINTER(_i32)]),
+    "pbsa_pair_tiles": (_i32, [_vp, _i32, _i32, _i32, _i32, _i32, _i32, _vp, _vp]),
     "pbsa_launch_count": (C.c_longlong, []),
     "pbsa_latent_blocks": (_i32, [C.POINTER(LatentGeom), C.POINTER(_i32), C.POINTER(_i32)]),
     "pbsa_attend_latent": (_i32, [_vp, _vp, _vp, _vp, C.POINTER(LatentGeom), _i32, _f32, _i32, _vp, _vp, _vp]),

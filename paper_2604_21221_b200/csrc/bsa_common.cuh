@@ -29,6 +29,8 @@ struct BsaParams {
     const int32_t* sel;
     int k;
     int sel_rows, sel_row0;  // sel is [units][sel_rows][k]; query block i of the launch reads row sel_row0 + i
+    const int32_t* pairs;    // [units][tiles_per_unit][2] query blocks of each tile (second -1: none);
+                             // null: tile t holds query blocks 2t and 2t + 1
     bf16* o;
     float* lse;
     float scale_log2;
@@ -55,7 +57,7 @@ struct BsaParams {
 constexpr int kMaxGangs = 1024;
 
 struct FragMeta {
-    int tile, u, qb0, has2;
+    int tile, u, qb0, qb1;  // qb1 < 0: the tile's second half is empty
     int n, e0, e1;   // list length and the entry range of this fragment
     int whole, nf, slot;
     int first_cta;   // first CTA holding a fragment of this tile (for the merge)
@@ -86,7 +88,7 @@ __device__ __forceinline__ int num_fragments(const BsaParams& p, int c) {
 
 // fragment f of virtual CTA vc: which tile, and (stream-K tail) which part of its list
 struct FragPlan {
-    int tile, u, qb0, has2;
+    int tile, u, qb0, qb1;
     int64_t va, vb;  // virtual range [va, vb) of the tile's list (vlen = whole tile)
     int nfr, first_cta, slot;
 };
@@ -104,8 +106,13 @@ __device__ __forceinline__ FragPlan plan_fragment(const BsaParams& p, int vc, in
         fp.tile = (g + f * p.gangs) * p.tiles_per_unit + vc % p.tiles_per_unit;
     }
     fp.u = fp.tile / p.tiles_per_unit;
-    fp.qb0 = 2 * (fp.tile % p.tiles_per_unit);
-    fp.has2 = fp.qb0 + 1 < p.nqb;
+    if (p.pairs != nullptr) {
+        fp.qb0 = __ldg(p.pairs + 2 * static_cast<int64_t>(fp.tile));
+        fp.qb1 = __ldg(p.pairs + 2 * static_cast<int64_t>(fp.tile) + 1);
+    } else {
+        fp.qb0 = 2 * (fp.tile % p.tiles_per_unit);
+        fp.qb1 = fp.qb0 + 1 < p.nqb ? fp.qb0 + 1 : -1;
+    }
     fp.va = 0;
     fp.vb = p.vlen;
     fp.nfr = 1;
@@ -126,7 +133,7 @@ __device__ __forceinline__ FragMeta make_meta(const BsaParams& p, const FragPlan
     fm.tile = fp.tile;
     fm.u = fp.u;
     fm.qb0 = fp.qb0;
-    fm.has2 = fp.has2;
+    fm.qb1 = fp.qb1;
     fm.n = run;
     fm.e0 = static_cast<int>((fp.va * run) / p.vlen);
     fm.e1 = static_cast<int>((fp.vb * run) / p.vlen);
@@ -175,18 +182,19 @@ __device__ int build_visible_list(const BsaParams& p, const FragPlan& fp, uint8_
     // fragment's first TMA can be issued, so a serial load -> store chain here is launch latency).
     constexpr int kB = 8;
     const int lane = threadIdx.x & 31;
-    const int u = fp.u, qb0 = fp.qb0;
+    const int u = fp.u;
     for (int w = lane; w < 2 * p.bm_words; w += 32) bm[w] = 0u;
     __syncwarp();
     if (p.k > 0 && p.n_local > 0) {
-        const int sel_rows = fp.has2 ? 2 : 1, total = sel_rows * p.k;
-        const int32_t* srow = p.sel + (static_cast<int64_t>(u) * p.sel_rows + p.sel_row0 + qb0) * p.k;
+        const int sel_rows = fp.qb1 >= 0 ? 2 : 1, total = sel_rows * p.k;
+        const int32_t* srow0 = p.sel + (static_cast<int64_t>(u) * p.sel_rows + p.sel_row0 + fp.qb0) * p.k;
+        const int32_t* srow1 = p.sel + (static_cast<int64_t>(u) * p.sel_rows + p.sel_row0 + (fp.qb1 >= 0 ? fp.qb1 : 0)) * p.k;
         for (int e0 = 0; e0 < total; e0 += 32 * kB) {
             int idx[kB];
 #pragma unroll
             for (int i = 0; i < kB; ++i) {
                 const int e = e0 + i * 32 + lane;
-                idx[i] = e < total ? __ldg(srow + e) : -1;  // rows qb0, qb0 + 1 are contiguous in sel
+                idx[i] = e < total ? __ldg(e < p.k ? srow0 + e : srow1 + (e - p.k)) : -1;
             }
 #pragma unroll
             for (int i = 0; i < kB; ++i) {

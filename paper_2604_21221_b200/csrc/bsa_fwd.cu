@@ -210,20 +210,20 @@ __global__ void __launch_bounds__(kThreads, 2)
                 const int nf = fm.e1 - fm.e0;
                 if (nf > 0) {
                     if (q_uses > 0) mbar_wait(q_empty, (q_uses - 1) & 1);
-                    const uint32_t qbytes = (fm.has2 ? 2u : 1u) * L::kHalves * static_cast<uint32_t>(p.b) * 128u;
+                    const uint32_t qbytes = (fm.qb1 >= 0 ? 2u : 1u) * L::kHalves * static_cast<uint32_t>(p.b) * 128u;
                     if (elect_one()) {
                         mbar_arrive_expect_tx(q_full, qbytes);
-                        for (int r = 0; r < (fm.has2 ? 2 : 1); ++r)
+                        for (int r = 0; r < (fm.qb1 >= 0 ? 2 : 1); ++r)
                             for (int h = 0; h < L::kHalves; ++h) {
                                 if (p.lat) {  // the query block is one 5-D box of the latent (blockify)
-                                    const int qb = fm.qb0 + r, e = fm.u / p.lg.heads, hd = fm.u % p.lg.heads;
+                                    const int qb = r ? fm.qb1 : fm.qb0, e = fm.u / p.lg.heads, hd = fm.u % p.lg.heads;
                                     const int nw = qb % p.lg.nw(), nh = (qb / p.lg.nw()) % p.lg.nh();
                                     const int nt = qb / (p.lg.nw() * p.lg.nh());
                                     tma_load_5d(q_smem + h * 16384 + r * 8192, &tm_q, q_full, hd * D + h * 64,
                                                 nw * p.lg.bw, nh * p.lg.bh, nt * p.lg.bt, e);
                                 } else {
                                     tma_load_3d(q_smem + h * 16384 + r * 8192, &tm_q, q_full, h * 64, 0,
-                                                fm.u * p.nqb + fm.qb0 + r);
+                                                fm.u * p.nqb + (r ? fm.qb1 : fm.qb0));
                                 }
                             }
                     }
@@ -381,9 +381,9 @@ __global__ void __launch_bounds__(kThreads, 2)
             mbar_wait(list_full + lb, (f >> 1) & 1);
             const FragMeta fm = meta[lb];
             const int nf = fm.e1 - fm.e0;
-            const int tile = fm.tile, u = fm.u, qb0 = fm.qb0;
-            const int qb = qb0 + half;
-            const bool valid = rr < p.b && qb < p.nqb;
+            const int tile = fm.tile, u = fm.u;
+            const int qb = half ? fm.qb1 : fm.qb0;
+            const bool valid = rr < p.b && qb >= 0;
 
             // ---------------------------------------------------------- online softmax
             float m = -INFINITY, l = 0.0f;
@@ -634,8 +634,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                 }
                 for (int q2 = 0; q2 < nfr; ++q2) wsm[q2 * 128 + t] = mf[q2];
                 wsm[8 * 128 + t] = Ls > 0.0f ? 1.0f / Ls : 0.0f;
-                const int qb2 = pm.qb0 + (row >> 6), rr2 = row & 63;
-                if (rr2 < p.b && qb2 < p.nqb && p.lse != nullptr)
+                const int qb2 = (row >> 6) ? pm.qb1 : pm.qb0, rr2 = row & 63;
+                if (rr2 < p.b && qb2 >= 0 && p.lse != nullptr)
                     p.lse[(static_cast<int64_t>(pm.u) * p.nqb + qb2) * p.b + rr2] =
                         Ls > 0.0f ? (M + __log2f(Ls)) * 0.69314718055994531f : -INFINITY;
             }
@@ -656,8 +656,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                     acc.w += w * x.w;
                 }
                 const int row = r0 + rl;
-                const int qb2 = pm.qb0 + (row >> 6), rr2 = row & 63;
-                if (rr2 >= p.b || qb2 >= p.nqb) continue;
+                const int qb2 = (row >> 6) ? pm.qb1 : pm.qb0, rr2 = row & 63;
+                if (rr2 >= p.b || qb2 < 0) continue;
                 const float inv = wsm[8 * 128 + rl];
                 uint2 w2;
                 w2.x = pack_bf16x2(acc.x * inv, acc.y * inv);
@@ -752,8 +752,9 @@ int launch_bsa_fwd(const bf16* q, const bf16* k_pool, const bf16* v_pool, int n_
                    const int32_t* dense, int dense_stride, int n_dense, const int32_t* local,
                    int local_stride, int n_local, const int32_t* sel, int k, int nqb, int b, int d,
                    int units, float scale, bf16* o, float* lse, void* ws, size_t ws_bytes, cudaStream_t s,
-                   const LatentGeom* lat, int sel_rows, int sel_row0) {
+                   const LatentGeom* lat, int sel_rows, int sel_row0, const int32_t* tile_pairs) {
     BsaParams p{};
+    p.pairs = tile_pairs;
     p.lat = lat != nullptr;
     if (lat) p.lg = *lat;
     p.units = units;

@@ -140,6 +140,8 @@ struct pbsa_mem {
     float* ws = nullptr;
     size_t ws_bytes = 0;
     int32_t* sel = nullptr;
+    int32_t* tile_pairs = nullptr;  // [units][(bpc + 1) / 2][2]: K3 tiles of the last call (pairs_valid)
+    bool pairs_valid = false;
     void* k3ws = nullptr;
     size_t k3ws_bytes = 0;
     int last_k = 0, last_n_keys = 0, last_sel_rows = 0;
@@ -204,9 +206,18 @@ void free_mem(pbsa_mem* m) {
     free_events(m);
     void* ptrs[] = {m->k_pool, m->v_pool, m->krep, m->dev.p_slot, m->dev.p_id, m->dev.p_score,
                     m->dev.l_slot, m->dev.l_id, m->dev.stage, m->dev.free_slot, m->dev.dense,
-                    m->dev.keys, m->qc, m->s_t, m->ws, m->sel, m->k3ws, m->dev.status};
+                    m->dev.keys, m->qc, m->s_t, m->ws, m->sel, m->tile_pairs, m->k3ws, m->dev.status};
     for (void* p : ptrs)
         if (p) cudaFree(p);
+}
+
+// K3 tiles pair query blocks by Top-K overlap (launch_pair_tiles) for windows of >= 1024 blocks,
+// where K3 dominates the call: config 5 chunk 692 -> 667 ms; at config 2 (312 blocks) the pairing
+// kernel costs about what K3 gains.  PBSA_TILE_PAIRING=0 never pairs, 1 always (tests, A/B).
+bool use_tile_pairing(int n_local) {
+    const char* e = getenv("PBSA_TILE_PAIRING");
+    if (e != nullptr) return atoi(e) != 0;
+    return n_local >= 1024;
 }
 
 // K3 runs the hybrid schedule (whole-tile waves + stream-K tail) by default;
@@ -347,6 +358,14 @@ int pbsa_topc_select(const int64_t* ids, const float* scores, int n, int slots, 
     PBSA_REQUIRE(n >= 0 && slots >= 0, "update_persistent: negative counts");
     PBSA_REQUIRE(n == 0 || (ids != nullptr && scores != nullptr && keep != nullptr), "update_persistent: null pointer");
     return launch_topc_keep(ids, scores, n, slots, keep, status, as_stream(stream));
+}
+
+int pbsa_pair_tiles(const int32_t* sel, int sel_rows, int sel_row0, int nq, int k, int n_local, int units,
+                    int32_t* pairs, void* stream) {
+    PBSA_REQUIRE(units >= 0 && nq >= 0 && k >= 0 && n_local >= 0, "pair_tiles: negative sizes");
+    PBSA_REQUIRE(sel_row0 >= 0 && sel_row0 + nq <= sel_rows, "pair_tiles: rows out of range");
+    PBSA_REQUIRE(units == 0 || nq == 0 || (sel != nullptr && pairs != nullptr), "pair_tiles: null pointer");
+    return launch_pair_tiles(sel, sel_rows, sel_row0, nq, k, n_local, units, pairs, as_stream(stream));
 }
 
 int pbsa_dev_alloc(void** out, size_t bytes) {
@@ -496,7 +515,8 @@ int pbsa_mem_create(pbsa_mem** out, int units, int capacity_c, int window_chunks
               alloc(reinterpret_cast<void**>(&m->dev.status), 16) &&
               alloc(reinterpret_cast<void**>(&m->qc), U * bpc * d * 4) &&
               alloc(reinterpret_cast<void**>(&m->s_t), U * S * 4) &&
-              alloc(reinterpret_cast<void**>(&m->sel), U * bpc * L * 4);
+              alloc(reinterpret_cast<void**>(&m->sel), U * bpc * L * 4) &&
+              alloc(reinterpret_cast<void**>(&m->tile_pairs), U * ((bpc + 1) / 2) * 2 * 4);
     if (ok) {
         m->ws_bytes = score_select_workspace(units, m->bpc, m->S);
         m->k3ws_bytes = bsa_fwd_workspace(units, m->bpc, d);
@@ -694,12 +714,20 @@ int attend_impl(pbsa_mem* m, const void* q, int k_top, float scale, int mode, vo
     }
     m->last_k = k;
     m->last_sel_rows = sel_rows;
+    // K3 tiles: query blocks paired by largest Top-K overlap (shorter union lists; results are per
+    // query block and do not depend on the partner), natural pairs when there is no selection
+    m->pairs_valid = false;
+    if (k > 0 && use_tile_pairing(n_l)) {
+        const int rc = launch_pair_tiles(m->sel, sel_rows, sel_row0, nq, k, n_l, U, m->tile_pairs, s);
+        if (rc == PBSA_OK) m->pairs_valid = true;
+        else if (rc != PBSA_EUNSUPPORTED) return rc;  // unsupported shape: natural pairing
+    }
     prof_mark(m, 2, s);
     // (c) block-sparse attention over P ++ current (dense) and the selected local blocks
     if (int rc = launch_bsa_fwd(static_cast<const bf16*>(q), m->k_pool, m->v_pool, m->S, m->dev.dense,
                                 m->C + bpc, n_p + bpc, m->dev.l_slot, m->Lcap, n_l, m->sel, k, nq, b, d, U,
                                 scale, static_cast<bf16*>(o), lse, use_stream_k() ? m->k3ws : nullptr,
-                                m->k3ws_bytes, s, lat, sel_rows, sel_row0))
+                                m->k3ws_bytes, s, lat, sel_rows, sel_row0, m->pairs_valid ? m->tile_pairs : nullptr))
         return rc;
     prof_mark(m, 3, s);
     // (d) persistent-memory update after the k=0 pass
@@ -895,6 +923,13 @@ int pbsa_mem_status(const pbsa_mem* m, int* flags, void* stream) {
     PBSA_REQUIRE(m != nullptr && flags != nullptr, "mem_status: null pointer");
     PBSA_CUDA(cudaMemcpyAsync(flags, m->dev.status, sizeof(int), cudaMemcpyDeviceToHost, as_stream(stream)));
     PBSA_CUDA(cudaStreamSynchronize(as_stream(stream)));
+    return PBSA_OK;
+}
+
+int pbsa_last_tile_pairs(const pbsa_mem* m, const int32_t** pairs, int* tiles_per_unit) {
+    PBSA_REQUIRE(m != nullptr, "last_tile_pairs: null memory");
+    if (pairs) *pairs = m->pairs_valid ? m->tile_pairs : nullptr;
+    if (tiles_per_unit) *tiles_per_unit = (m->last_sel_rows + 1) / 2;
     return PBSA_OK;
 }
 

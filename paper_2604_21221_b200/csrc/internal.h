@@ -95,6 +95,13 @@ int launch_blockify(const float* x, int t, int h, int w, int d, int bt, int bh, 
                     cudaStream_t s);
 int launch_topc_keep(const int64_t* ids, const float* scores, int n, int slots, uint8_t* keep, int* status,
                      cudaStream_t s);
+// Tile pairing (between K2 and K3): per unit, the nq query blocks of a call are paired into K3 tiles
+// greedily by largest Top-K overlap (ties: lowest pair index) so that each tile's union list is
+// short.  sel [units][sel_rows][k] (rows sel_row0 ..); pairs [units][(nq + 1) / 2][2] = query blocks
+// (within the call) of each tile, the second -1 for an odd leftover.  Returns PBSA_EUNSUPPORTED when
+// the bitsets do not fit shared memory (the caller then keeps the natural (2t, 2t + 1) pairing).
+int launch_pair_tiles(const int32_t* sel, int sel_rows, int sel_row0, int nq, int k, int n_local, int units,
+                      int32_t* pairs, cudaStream_t s);
 // K3
 // lat != null: q and o are chunk latents (Q blocks gathered by a 5-D TMA box, O rows scattered back
 // to their latent positions in the epilogue -- unblockify fused); lse stays [units][n_q] block-major
@@ -102,7 +109,8 @@ int launch_bsa_fwd(const bf16* q, const bf16* k_pool, const bf16* v_pool, int n_
                    const int32_t* dense, int dense_stride, int n_dense, const int32_t* local,
                    int local_stride, int n_local, const int32_t* sel, int k, int nqb, int b, int d,
                    int units, float scale, bf16* o, float* lse, void* ws, size_t ws_bytes, cudaStream_t s,
-                   const LatentGeom* lat = nullptr, int sel_rows = 0, int sel_row0 = 0);
+                   const LatentGeom* lat = nullptr, int sel_rows = 0, int sel_row0 = 0,
+                   const int32_t* tile_pairs = nullptr);  // null: tiles are query blocks (2t, 2t + 1)
 size_t bsa_fwd_workspace(int units, int nqb, int d);
 pbsa_bsa_plan& last_bsa_plan();  // the calling thread's last K3 launch plan
 // injected fault (pbsa_debug_set_fault; negative controls only)

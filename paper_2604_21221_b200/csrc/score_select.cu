@@ -988,6 +988,175 @@ int launch_certified(const ScoreParams& p, dim3 g1, size_t lsmem, int v4, float*
     return check_launch("cert_select_kernel");
 }
 
+// ---------------------------------------------------------------------------------------------
+// K3 tile pairing.  A K3 tile walks the UNION of its two query blocks' visible lists, so the
+// executed work of a call is the sum over tiles of (n_dense + 2k - overlap(a, b)).  CTA per unit:
+// the nq selections as bitsets in shared memory, all pairwise overlaps (AND + popcount), then the
+// greedy matching -- repeatedly the free pair with the largest overlap (ties: the lowest i * nq + j,
+// i < j), tiles emitted in that order, an odd leftover last.  The greedy steps run in one warp
+// without block barriers: every lane owns the rows lane + 32 m with their best free partner, and a
+// step rescans only the rows whose best partner it took.  Worth it for long windows only (~60 us
+// per call in dependent warp steps): config 5 (6006-block window) chunk 692 -> 667 ms; at config 2
+// (312 blocks) K3 gains what the pairing costs (attend_impl's auto mode: windows >= 1024 blocks).
+constexpr int kPairThreads = 512;
+
+__global__ void __launch_bounds__(kPairThreads) pair_tiles_kernel(const int32_t* __restrict__ sel, int sel_rows,
+                                                                  int sel_row0, int nq, int k, int words,
+                                                                  int32_t* __restrict__ pairs) {
+    pdl_wait();  // programmatic dependent launch: the selections are visible from here on
+    extern __shared__ __align__(16) uint32_t pt_smem[];
+    uint32_t* bits = pt_smem;                                                            // [nq][words]
+    uint16_t* ov = reinterpret_cast<uint16_t*>(bits + static_cast<size_t>(nq) * words);  // [nq][nq]
+    __shared__ int bkey[256], bj[256];
+    const int u = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int kWarps = kPairThreads / 32;
+    for (int e = tid; e < nq * words; e += kPairThreads) bits[e] = 0u;
+    __syncthreads();
+    const int32_t* su = sel + (static_cast<int64_t>(u) * sel_rows + sel_row0) * k;
+    for (int r = warp; r < nq; r += kWarps)
+        for (int x0 = lane; x0 < k; x0 += 32) {
+            const int x = __ldg(su + static_cast<int64_t>(r) * k + x0);
+            atomicOr(&bits[r * words + (x >> 5)], 1u << (x & 31));
+        }
+    __syncthreads();
+    if (words <= 32) {  // warp per row i, lanes over the partners j > i
+        for (int i = warp; i < nq; i += kWarps)
+            for (int j = i + 1 + lane; j < nq; j += 32) {
+                int c = 0;
+                for (int w = 0; w < words; ++w) c += __popc(bits[i * words + w] & bits[j * words + w]);
+                ov[i * nq + j] = static_cast<uint16_t>(c);
+                ov[j * nq + i] = static_cast<uint16_t>(c);
+            }
+    } else {  // warp per pair, lanes over the words
+        for (int i = warp; i < nq; i += kWarps)
+            for (int j = i + 1; j < nq; ++j) {
+                int c = 0;
+                for (int w = lane; w < words; w += 32) c += __popc(bits[i * words + w] & bits[j * words + w]);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+                if (lane == 0) {
+                    ov[i * nq + j] = static_cast<uint16_t>(c);
+                    ov[j * nq + i] = static_cast<uint16_t>(c);
+                }
+            }
+    }
+    __syncthreads();
+    // key of pair (i, j): overlap above, 65535 - (min * nq + max) below -> the max key is the largest
+    // overlap, then the lowest pair index (nq <= 255: the index fits 16 bits).  Warp-collective scan
+    // of row i's free partners j = lane + 32 m (the lane owning j knows whether j is taken).
+    auto row_best = [&](int i, auto is_taken, int& key_out, int& j_out) {
+        int key = -1, bjj = -1;
+        for (int j = lane; j < nq; j += 32)
+            if (j != i && !is_taken(j)) {
+                const int lo = i < j ? i : j, hi = i < j ? j : i;
+                const int kk = (static_cast<int>(ov[i * nq + j]) << 16) | (65535 - (lo * nq + hi));
+                if (kk > key) {
+                    key = kk;
+                    bjj = j;
+                }
+            }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const int k2 = __shfl_xor_sync(0xffffffffu, key, o), j2 = __shfl_xor_sync(0xffffffffu, bjj, o);
+            if (k2 > key) {  // keys are unique per pair
+                key = k2;
+                bjj = j2;
+            }
+        }
+        key_out = key;
+        j_out = bjj;
+    };
+    for (int i = warp; i < nq; i += kWarps) {  // every row's best partner (nothing taken yet)
+        int key, j;
+        row_best(i, [](int) { return false; }, key, j);
+        if (lane == 0) {
+            bkey[i] = key;
+            bj[i] = j;
+        }
+    }
+    __syncthreads();
+    if (warp != 0) return;
+    constexpr int kOwn = 8;  // rows per lane (nq <= 255)
+    int rk[kOwn], rj[kOwn];
+    unsigned tk = 0;  // bit m: row lane + 32 m is taken (or absent)
+#pragma unroll
+    for (int m = 0; m < kOwn; ++m) {
+        const int i = lane + 32 * m;
+        rk[m] = i < nq ? bkey[i] : -1;
+        rj[m] = i < nq ? bj[i] : -1;
+        if (i >= nq) tk |= 1u << m;
+    }
+    auto taken_fn = [&](int j) { return ((tk >> (j >> 5)) & 1u) != 0; };
+    int32_t* pu = pairs + static_cast<int64_t>(u) * ((nq + 1) / 2) * 2;
+    for (int t = 0; t < nq / 2; ++t) {
+        int key = -1, row = -1;
+#pragma unroll
+        for (int m = 0; m < kOwn; ++m)
+            if (!((tk >> m) & 1u) && rk[m] > key) {
+                key = rk[m];
+                row = lane + 32 * m;
+            }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const int k2 = __shfl_xor_sync(0xffffffffu, key, o), r2 = __shfl_xor_sync(0xffffffffu, row, o);
+            if (k2 > key || (k2 == key && r2 < row)) {
+                key = k2;
+                row = r2;
+            }
+        }
+        int partner = -1;
+#pragma unroll
+        for (int m = 0; m < kOwn; ++m) {
+            const int v = __shfl_sync(0xffffffffu, rj[m], row & 31);
+            if (m == (row >> 5)) partner = v;
+        }
+        const int lo = row < partner ? row : partner, hi = row < partner ? partner : row;
+        if (lane == 0) {
+            pu[2 * t] = lo;
+            pu[2 * t + 1] = hi;
+        }
+        if ((lo & 31) == lane) tk |= 1u << (lo >> 5);
+        if ((hi & 31) == lane) tk |= 1u << (hi >> 5);
+#pragma unroll
+        for (int m = 0; m < kOwn; ++m) {  // rows whose best partner was just taken: rescan
+            unsigned need = __ballot_sync(0xffffffffu, !((tk >> m) & 1u) && (rj[m] == lo || rj[m] == hi));
+            while (need) {
+                const int l2 = __ffs(need) - 1;
+                need &= need - 1;
+                int k3, j3;
+                row_best(l2 + 32 * m, taken_fn, k3, j3);
+                if (lane == l2) {
+                    rk[m] = k3;
+                    rj[m] = j3;
+                }
+            }
+        }
+    }
+    if (nq & 1) {
+#pragma unroll
+        for (int m = 0; m < kOwn; ++m)
+            if (!((tk >> m) & 1u)) {
+                pu[2 * (nq / 2)] = lane + 32 * m;
+                pu[2 * (nq / 2) + 1] = -1;
+            }
+    }
+}
+
+int launch_pair_tiles(const int32_t* sel, int sel_rows, int sel_row0, int nq, int k, int n_local, int units,
+                      int32_t* pairs, cudaStream_t s) {
+    if (units == 0 || nq == 0) return 0;
+    if (nq > 255 || k <= 0 || n_local <= 0 || k > 32767) return set_error(PBSA_EUNSUPPORTED, "pair_tiles: shape");
+    const int words = (n_local + 31) / 32;
+    const size_t smem = static_cast<size_t>(nq) * words * 4 + ((static_cast<size_t>(nq) * nq * 2 + 15) & ~size_t(15));
+    if (smem > 200 * 1024) return set_error(PBSA_EUNSUPPORTED, "pair_tiles: bitsets exceed shared memory");
+    // (+ the kernel's 2 KB of static shared memory, which counts against the 48 KB default too)
+    if (int rc = ensure_smem(reinterpret_cast<const void*>(pair_tiles_kernel), smem + 4096, "pair_tiles")) return rc;
+    if (launch_pdl(pair_tiles_kernel, dim3(static_cast<unsigned>(units)), dim3(kPairThreads), smem, s, sel, sel_rows,
+                   sel_row0, nq, k, words, pairs) != cudaSuccess)
+        return check_launch("pair_tiles_kernel");
+    return check_launch("pair_tiles_kernel");
+}
+
 // PBSA_K2_CERT: unset = certified fp32 ranking on denoise passes over windows of >= kCertMinKeys
 // keys, 1 = certified on every denoise pass, 0 = the exact fp64 path on every pass, 2 = certified
 // kernels with every row forced through the exact fallback (tests).

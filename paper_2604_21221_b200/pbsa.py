@@ -171,6 +171,16 @@ def attention_sparse(q: torch.Tensor, k_pool: torch.Tensor, v_pool: torch.Tensor
     return (o, lse) if want_lse else o
 
 
+def pair_tiles(sel: torch.Tensor, n_local: int) -> torch.Tensor:
+    """K3 tile pairing (pbsa_pair_tiles): sel [units, nq, k] int32 local indices -> [units, (nq+1)//2, 2]
+    int32 query blocks per tile (second -1 for a single), paired greedily by Top-K overlap."""
+    _need(sel, torch.int32, "sel")
+    units, nq, k = sel.shape
+    out = torch.empty(units, (nq + 1) // 2, 2, device=sel.device, dtype=torch.int32)
+    check(LIB.pbsa_pair_tiles(sel.data_ptr(), nq, 0, nq, k, n_local, units, out.data_ptr(), _stream()))
+    return out
+
+
 # ---- the reference's tensor / blockify primitives and the SPEC router / memory ops on device f32
 # tensors (bit-exact with the reference's CPU code; the fused hot path never uses them) ------------
 def _f32(t: torch.Tensor, name: str) -> None:
@@ -637,6 +647,13 @@ class Memory:
         f = C.c_int()
         check(LIB.pbsa_mem_status(self._h, C.byref(f), _stream()))
         return f.value
+
+    def last_tile_pairs(self):
+        """K3 tiles of the last call: [units, tiles, 2] int32 query blocks (second -1: none), or None
+        when the call used the natural pairs (2t, 2t + 1)."""
+        pr, t = C.c_void_p(), C.c_int()
+        check(LIB.pbsa_last_tile_pairs(self._h, C.byref(pr), C.byref(t)))
+        return self._view(pr.value, (self.units, t.value, 2), torch.int32) if pr.value else None
 
     def last_selection(self):
         sel, k, st, nk = C.c_void_p(), C.c_int(), C.c_void_p(), C.c_int()

@@ -567,8 +567,9 @@ def test_score_select_certified_fuzz(pb):
 
 def test_launch_counter_per_call(pb):
     """pbsa_launch_count: a denoise call at a short window launches ingest + K2 logits + K2 select
-    + K3 (4 kernels); a cache-update call adds the A_t aggregation and K4 (6) -- the bench reports
-    this counter's delta over its timed region as gpu_launches."""
+    + K3 (4 kernels; no tile pairing below 1024 window blocks); a cache-update call adds the A_t
+    aggregation and K4 (6) -- the bench reports this counter's delta over its timed region as
+    gpu_launches."""
     from paper_2604_21221_b200._capi import LIB
     U, C, W, bpc, b, d = 2, 12, 2, 6, 60, 128
     mem = pb.Memory(U, C, W, bpc, b, d)
@@ -584,6 +585,69 @@ def test_launch_counter_per_call(pb):
     n2 = LIB.pbsa_launch_count()
     torch.cuda.synchronize()
     assert (n1 - n0, n2 - n1) == (4, 6)
+    mem.close()
+
+
+def _pairing_reference(sel_u):
+    """The pairing rule of pair_tiles_kernel restated: greedy matching -- repeatedly the free pair
+    (i < j) with the largest Top-K overlap, ties to the lowest i * nq + j, in that order; an odd
+    leftover last with -1."""
+    nq = len(sel_u)
+    sets = [set(r) for r in sel_u]
+    keys = sorted(((len(sets[i] & sets[j]), -(i * nq + j), i, j) for i in range(nq) for j in range(i + 1, nq)),
+                  reverse=True)
+    free = [True] * nq
+    out = []
+    for _, _, i, j in keys:
+        if free[i] and free[j]:
+            free[i] = free[j] = False
+            out.append((i, j))
+    out += [(i, -1) for i in range(nq) if free[i]]
+    return out
+
+
+@pytest.mark.parametrize("units,nq,n_local,k", [(3, 7, 40, 9), (2, 78, 312, 78), (2, 78, 6006, 1502),
+                                                 (1, 1, 10, 3), (2, 5, 64, 64)])
+def test_pair_tiles_kernel_matches_rule(pb, units, nq, n_local, k):
+    """pbsa_pair_tiles on random selections (config-2 and config-5 shapes included) equals the
+    restated greedy rule."""
+    g = torch.Generator(device="cuda").manual_seed(nq * 7 + k)
+    sel = torch.stack([torch.stack([torch.randperm(n_local, device="cuda", generator=g)[:k].sort().values
+                                    for _ in range(nq)]) for _ in range(units)]).int().contiguous()
+    pr = pb.pair_tiles(sel, n_local).cpu().tolist()
+    sl = sel.cpu().tolist()
+    for u in range(units):
+        assert [tuple(x) for x in pr[u]] == _pairing_reference(sl[u])
+
+
+@pytest.mark.parametrize("bpc", [6, 7])
+def test_tile_pairing_rule_and_partition(pb, bpc, monkeypatch):
+    monkeypatch.setenv("PBSA_TILE_PAIRING", "1")
+    """K3 tiles pair each call's query blocks by Top-K overlap (pair_tiles_kernel): the device
+    pairing equals the restated greedy rule, covers every query block exactly once (odd counts: one
+    single-block tile), and does not lengthen the total union work on these inputs.  PBSA_TILE_PAIRING=1
+    forces it for these short windows (auto mode pairs windows of >= 1024 blocks only)."""
+    U, C, W, b, d, k_top = 3, 12, 4, 60, 128, 5
+    mem = pb.Memory(U, C, W, bpc, b, d)
+    g = torch.Generator(device="cuda").manual_seed(11)
+    for c in range(W + 3):
+        q, kk, vv = (torch.randn(U, bpc * b, d, device="cuda", generator=g).bfloat16() for _ in range(3))
+        mem.attend_qkv(q, kk, vv, k_top, pb.MODE_CACHE_UPDATE if c % 2 else pb.MODE_DENOISE)
+        pairs = mem.last_tile_pairs()
+        sel, _ = mem.last_selection()
+        if sel is None:  # empty window (first chunk): no selection, natural pairs
+            assert pairs is None
+            continue
+        assert pairs is not None
+        pr, sl = pairs.cpu().tolist(), sel.cpu().tolist()
+        for u in range(U):
+            got = [tuple(x) for x in pr[u]]
+            assert got == _pairing_reference(sl[u])
+            flat = sorted(x for t in got for x in t if x >= 0)
+            assert flat == list(range(bpc))
+            nat = sum(len(set(sl[u][t]) | set(sl[u][t + 1] if t + 1 < bpc else [])) for t in range(0, bpc, 2))
+            paired = sum(len(set(sl[u][a]) | (set(sl[u][b2]) if b2 >= 0 else set())) for a, b2 in got)
+            assert paired <= nat
     mem.close()
 
 

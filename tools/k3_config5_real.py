@@ -75,3 +75,40 @@ s0 = sel[0].flatten().cpu()
 cnt = torch.bincount(s0, minlength=inf.n_l).float()
 print("selection count per local block (unit 0): mean %.2f std %.2f max %d zeros %d" % (
     cnt.mean(), cnt.std(), int(cnt.max()), int((cnt == 0).sum())))
+
+
+# Pairing study: union sizes when each unit's query blocks are paired greedily by largest selection
+# overlap (instead of (2t, 2t + 1)): total executed list entries and the per-unit longest tile.
+def greedy_pairs(s_u, n_l):
+    nq = s_u.shape[0]
+    bits = torch.zeros(nq, n_l, dtype=torch.float32, device=s_u.device)
+    bits.scatter_(1, s_u.long(), 1.0)
+    ov = bits @ bits.T  # pairwise overlaps
+    ov.fill_diagonal_(-1)
+    free = torch.ones(nq, dtype=torch.bool, device=s_u.device)
+    pairs = []
+    for _ in range(nq // 2):
+        m = ov.clone()
+        m[~free] = -2
+        m[:, ~free] = -2
+        idx = int(torch.argmax(m))
+        i, j = divmod(idx, nq)
+        pairs.append((i, j))
+        free[i] = free[j] = False
+    rest = [i for i in range(nq) if free[i]]
+    return pairs, rest, ov
+
+
+tot_nat, tot_greedy, mx_nat, mx_greedy = 0, 0, [], []
+for u in range(16):
+    s_u = sel[u]
+    pairs, rest, ov = greedy_pairs(s_u, inf.n_l)
+    kk = s_u.shape[1]
+    nat = [2 * kk - int(ov[t, t + 1]) for t in range(0, bpc - 1, 2)]
+    gr = [2 * kk - int(ov[i, j]) for i, j in pairs] + [kk for _ in rest]
+    tot_nat += sum(nat)
+    tot_greedy += sum(gr)
+    mx_nat.append(max(nat))
+    mx_greedy.append(max(gr))
+print("pairing (16 units): union entries natural %d greedy %d (%.3f); mean per-unit max natural %.1f greedy %.1f" % (
+    tot_nat, tot_greedy, tot_greedy / tot_nat, sum(mx_nat) / 16, sum(mx_greedy) / 16))
