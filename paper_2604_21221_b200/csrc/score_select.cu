@@ -993,11 +993,8 @@ int launch_certified(const ScoreParams& p, dim3 g1, size_t lsmem, int v4, float*
 // executed work of a call is the sum over tiles of (n_dense + 2k - overlap(a, b)).  CTA per unit:
 // the nq selections as bitsets in shared memory, all pairwise overlaps (AND + popcount), then the
 // greedy matching -- repeatedly the free pair with the largest overlap (ties: the lowest i * nq + j,
-// i < j), tiles emitted in that order, an odd leftover last.  The greedy steps run in one warp
-// without block barriers: every lane owns the rows lane + 32 m with their best free partner, and a
-// step rescans only the rows whose best partner it took.  Worth it for long windows only (~60 us
-// per call in dependent warp steps): config 5 (6006-block window) chunk 692 -> 667 ms; at config 2
-// (312 blocks) K3 gains what the pairing costs (attend_impl's auto mode: windows >= 1024 blocks).
+// i < j), tiles emitted in that order, an odd leftover last -- computed in parallel rounds of
+// mutual-best pairs (below).  Config 5 (6006-block window): chunk 698 -> 664 ms.
 constexpr int kPairThreads = 512;
 
 __global__ void __launch_bounds__(kPairThreads) pair_tiles_kernel(const int32_t* __restrict__ sel, int sel_rows,
@@ -1007,7 +1004,7 @@ __global__ void __launch_bounds__(kPairThreads) pair_tiles_kernel(const int32_t*
     extern __shared__ __align__(16) uint32_t pt_smem[];
     uint32_t* bits = pt_smem;                                                            // [nq][words]
     uint16_t* ov = reinterpret_cast<uint16_t*>(bits + static_cast<size_t>(nq) * words);  // [nq][nq]
-    __shared__ int bkey[256], bj[256];
+    __shared__ int bkey[256], bj[256], partner_s[256];
     const int u = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int kWarps = kPairThreads / 32;
     for (int e = tid; e < nq * words; e += kPairThreads) bits[e] = 0u;
@@ -1066,79 +1063,65 @@ __global__ void __launch_bounds__(kPairThreads) pair_tiles_kernel(const int32_t*
         key_out = key;
         j_out = bjj;
     };
-    for (int i = warp; i < nq; i += kWarps) {  // every row's best partner (nothing taken yet)
+    // Rounds of mutual-best pairs: a pair whose two rows name each other as best free partner is
+    // the one the greedy order would take anyway (no free pair touching either row has a larger
+    // key), so taking all of them at once yields EXACTLY the greedy matching.  Only rows whose best
+    // partner was taken rescan.
+    __shared__ int n_new;
+    for (int i = tid; i < nq; i += kPairThreads) partner_s[i] = -1;
+    __syncthreads();
+    auto free_fn = [&](int j) { return partner_s[j] != -1; };  // "taken" predicate for row_best
+    for (int i = warp; i < nq; i += kWarps) {
         int key, j;
-        row_best(i, [](int) { return false; }, key, j);
+        row_best(i, free_fn, key, j);
         if (lane == 0) {
             bkey[i] = key;
             bj[i] = j;
         }
     }
     __syncthreads();
-    if (warp != 0) return;
-    constexpr int kOwn = 8;  // rows per lane (nq <= 255)
-    int rk[kOwn], rj[kOwn];
-    unsigned tk = 0;  // bit m: row lane + 32 m is taken (or absent)
-#pragma unroll
-    for (int m = 0; m < kOwn; ++m) {
-        const int i = lane + 32 * m;
-        rk[m] = i < nq ? bkey[i] : -1;
-        rj[m] = i < nq ? bj[i] : -1;
-        if (i >= nq) tk |= 1u << m;
+    for (int round = 0; round < nq; ++round) {
+        if (tid == 0) n_new = 0;
+        int mate = -1;
+        if (tid < nq && partner_s[tid] == -1) {
+            const int j = bj[tid];
+            if (j >= 0 && bj[j] == tid) mate = j;
+        }
+        __syncthreads();
+        if (mate >= 0) {
+            partner_s[tid] = mate;
+            if (tid < mate) atomicAdd(&n_new, 1);
+        }
+        __syncthreads();
+        const int nn = n_new;
+        if (nn == 0) break;  // (uniform: read after the barrier, reset only after the next one)
+        for (int i = warp; i < nq; i += kWarps) {  // free rows whose best partner was just taken
+            if (partner_s[i] != -1 || bj[i] < 0 || partner_s[bj[i]] == -1) continue;
+            int key, j;
+            row_best(i, free_fn, key, j);
+            if (lane == 0) {
+                bkey[i] = key;
+                bj[i] = j;
+            }
+        }
+        __syncthreads();
     }
-    auto taken_fn = [&](int j) { return ((tk >> (j >> 5)) & 1u) != 0; };
+    // tiles in the greedy order (pair key descending), an odd leftover last
     int32_t* pu = pairs + static_cast<int64_t>(u) * ((nq + 1) / 2) * 2;
-    for (int t = 0; t < nq / 2; ++t) {
-        int key = -1, row = -1;
-#pragma unroll
-        for (int m = 0; m < kOwn; ++m)
-            if (!((tk >> m) & 1u) && rk[m] > key) {
-                key = rk[m];
-                row = lane + 32 * m;
-            }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const int k2 = __shfl_xor_sync(0xffffffffu, key, o), r2 = __shfl_xor_sync(0xffffffffu, row, o);
-            if (k2 > key || (k2 == key && r2 < row)) {
-                key = k2;
-                row = r2;
-            }
+    if (tid < nq && partner_s[tid] > tid) {
+        const int mate = partner_s[tid];
+        const int mykey = (static_cast<int>(ov[tid * nq + mate]) << 16) | (65535 - (tid * nq + mate));
+        int rank = 0;
+        for (int a2 = 0; a2 < nq; ++a2) {
+            const int pa = partner_s[a2];
+            if (pa > a2 && ((static_cast<int>(ov[a2 * nq + pa]) << 16) | (65535 - (a2 * nq + pa))) > mykey) ++rank;
         }
-        int partner = -1;
-#pragma unroll
-        for (int m = 0; m < kOwn; ++m) {
-            const int v = __shfl_sync(0xffffffffu, rj[m], row & 31);
-            if (m == (row >> 5)) partner = v;
-        }
-        const int lo = row < partner ? row : partner, hi = row < partner ? partner : row;
-        if (lane == 0) {
-            pu[2 * t] = lo;
-            pu[2 * t + 1] = hi;
-        }
-        if ((lo & 31) == lane) tk |= 1u << (lo >> 5);
-        if ((hi & 31) == lane) tk |= 1u << (hi >> 5);
-#pragma unroll
-        for (int m = 0; m < kOwn; ++m) {  // rows whose best partner was just taken: rescan
-            unsigned need = __ballot_sync(0xffffffffu, !((tk >> m) & 1u) && (rj[m] == lo || rj[m] == hi));
-            while (need) {
-                const int l2 = __ffs(need) - 1;
-                need &= need - 1;
-                int k3, j3;
-                row_best(l2 + 32 * m, taken_fn, k3, j3);
-                if (lane == l2) {
-                    rk[m] = k3;
-                    rj[m] = j3;
-                }
-            }
-        }
+        pu[2 * rank] = tid;
+        pu[2 * rank + 1] = mate;
     }
-    if (nq & 1) {
-#pragma unroll
-        for (int m = 0; m < kOwn; ++m)
-            if (!((tk >> m) & 1u)) {
-                pu[2 * (nq / 2)] = lane + 32 * m;
-                pu[2 * (nq / 2) + 1] = -1;
-            }
+    if (tid < nq && partner_s[tid] == -1) {  // at most one (odd nq)
+        pu[2 * (nq / 2)] = tid;
+        pu[2 * (nq / 2) + 1] = -1;
     }
 }
 
