@@ -67,6 +67,15 @@ pb.select_topk(sm, 17)
 lat = torch.randn(3, 30, 52, 8, device="cuda", generator=g)
 pb.unblockify(pb.blockify(lat, (1, 15, 4)), lat.shape, (1, 15, 4))
 pb.topc_select(torch.arange(40, device="cuda"), torch.rand(40, device="cuda", generator=g), 13)
+# K3 tile pairing: standalone, and inside attend (forced for these short windows)
+selp = torch.stack([torch.stack([torch.randperm(40, device="cuda", generator=g)[:9].sort().values
+                                 for _ in range(7)]) for _ in range(2)]).int().contiguous()
+pb.pair_tiles(selp, 40)
+os.environ["PBSA_TILE_PAIRING"] = "1"
+for c in range(3):
+    q6, k6, v6 = (torch.randn(U, bpc * b, d, device="cuda", generator=g).bfloat16() for _ in range(3))
+    parts[1].attend_qkv(q6, k6, v6, 3, pb.MODE_DENOISE if c % 2 else pb.MODE_CACHE_UPDATE)
+del os.environ["PBSA_TILE_PAIRING"]
 torch.cuda.synchronize()
 print("sanitize paths ok", mem.status(), [t.shape for t in grads])
 for m in [mem] + parts:
