@@ -1099,6 +1099,7 @@ __global__ void __launch_bounds__(kPairThreads) pair_tiles_kernel(const int32_t*
             if (partner_s[i] != -1 || bj[i] < 0 || partner_s[bj[i]] == -1) continue;
             int key, j;
             row_best(i, free_fn, key, j);
+            __syncwarp();  // every lane has read bj[i] before lane 0 rewrites it
             if (lane == 0) {
                 bkey[i] = key;
                 bj[i] = j;
