@@ -802,15 +802,6 @@ int launch_bsa_fwd(const bf16* q, const bf16* k_pool, const bf16* v_pool, int n_
     return l16 ? launch_impl<DD, NS, NS, BB, kPolyMask, true>(q, k_pool, v_pool, p, s)            \
                : launch_impl<DD, NS, NS, BB, kPolyMask, false>(q, k_pool, v_pool, p, s)
     if (d == 128) {
-#ifdef PBSA_K3_POLY_EXPERIMENT
-        {
-            static const int pm = getenv("PBSA_K3_POLY") ? atoi(getenv("PBSA_K3_POLY")) : 0;
-            if (b == 60 && pm == 1) return launch_impl<128, 2, 2, 60, 0x00010001u, false>(q, k_pool, v_pool, p, s);
-            if (b == 60 && pm == 2) return launch_impl<128, 2, 2, 60, 0x01010101u, false>(q, k_pool, v_pool, p, s);
-            if (b == 60 && pm == 3) return launch_impl<128, 2, 2, 60, 0x11111111u, false>(q, k_pool, v_pool, p, s);
-            if (b == 60 && pm == 4) return launch_impl<128, 2, 2, 60, 0x10001000u, false>(q, k_pool, v_pool, p, s);
-        }
-#endif
         if (b == 60) PBSA_K3(128, 2, 60);
         if (b == 64) PBSA_K3(128, 2, 64);
         PBSA_K3(128, 2, 0);
