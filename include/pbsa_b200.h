@@ -127,8 +127,9 @@ int pbsa_topc_select(const int64_t* ids, const float* scores, int n, int slots, 
 /* K3 tile pairing (scheduling, not a SPEC op; what pbsa_attend runs between K2 and K3): per unit, the
  * query blocks sel_row0 .. sel_row0 + nq - 1 of sel [units][sel_rows][k] (local indices < n_local) are
  * paired greedily by Top-K overlap (repeatedly the free pair with the largest overlap, ties to the lowest
- * i * nq + j); pairs [units][(nq + 1) / 2][2] lists each tile's query blocks (relative to sel_row0) in
- * that order, an odd leftover last with -1.  PBSA_EUNSUPPORTED when nq > 255, k > 32767 or the
+ * i * nq + j), then partners swapped between the least-overlapping tile and another while both new
+ * tiles overlap more; pairs [units][(nq + 1) / 2][2] lists each tile's query blocks (relative to
+ * sel_row0), an odd leftover last with -1.  PBSA_EUNSUPPORTED when nq > 255, k > 32767 or the
  * bitsets exceed shared memory.  pbsa_attend pairs automatically for windows of >= 1024 blocks
  * (PBSA_TILE_PAIRING=0 never, =1 always). */
 int pbsa_pair_tiles(const int32_t* sel, int sel_rows, int sel_row0, int nq, int k, int n_local, int units,

@@ -590,8 +590,8 @@ def test_launch_counter_per_call(pb):
 
 def _pairing_reference(sel_u):
     """The pairing rule of pair_tiles_kernel restated: greedy matching -- repeatedly the free pair
-    (i < j) with the largest Top-K overlap, ties to the lowest i * nq + j, in that order; an odd
-    leftover last with -1."""
+    (i < j) with the largest Top-K overlap, ties to the lowest i * nq + j, in that order -- then the
+    bottleneck pass; an odd leftover last with -1."""
     nq = len(sel_u)
     sets = [set(r) for r in sel_u]
     keys = sorted(((len(sets[i] & sets[j]), -(i * nq + j), i, j) for i in range(nq) for j in range(i + 1, nq)),
@@ -602,6 +602,31 @@ def _pairing_reference(sel_u):
         if free[i] and free[j]:
             free[i] = free[j] = False
             out.append((i, j))
+    # bottleneck pass: swap partners between the least-overlapping tile and another while both new
+    # tiles overlap more (best new minimum, then sum, then lowest (s, option))
+    ovm = [[len(sets[i] & sets[j]) for j in range(nq)] for i in range(nq)]
+    for _ in range(nq if out else 0):
+        t = min(range(len(out)), key=lambda t2: (ovm[out[t2][0]][out[t2][1]], t2))
+        a, b = out[t]
+        cur = ovm[a][b]
+        best = None
+        for s2, (c, d2) in enumerate(out):
+            if s2 == t:
+                continue
+            for opt in (0, 1):
+                x1, x2 = ovm[a][d2 if opt else c], ovm[b][c if opt else d2]
+                if min(x1, x2) <= cur:
+                    continue
+                key = (min(x1, x2), x1 + x2, -(2 * s2 + opt))
+                if best is None or key > best[0]:
+                    best = (key, s2, opt)
+        if best is None:
+            break
+        _, s2, opt = best
+        c, d2 = out[s2]
+        n1, n2 = (d2, c) if opt else (c, d2)
+        out[t] = (min(a, n1), max(a, n1))
+        out[s2] = (min(b, n2), max(b, n2))
     out += [(i, -1) for i in range(nq) if free[i]]
     return out
 
@@ -610,7 +635,7 @@ def _pairing_reference(sel_u):
                                                  (1, 1, 10, 3), (2, 5, 64, 64)])
 def test_pair_tiles_kernel_matches_rule(pb, units, nq, n_local, k):
     """pbsa_pair_tiles on random selections (config-2 and config-5 shapes included) equals the
-    restated greedy rule."""
+    restated greedy + bottleneck rule."""
     g = torch.Generator(device="cuda").manual_seed(nq * 7 + k)
     sel = torch.stack([torch.stack([torch.randperm(n_local, device="cuda", generator=g)[:k].sort().values
                                     for _ in range(nq)]) for _ in range(units)]).int().contiguous()
@@ -624,8 +649,8 @@ def test_pair_tiles_kernel_matches_rule(pb, units, nq, n_local, k):
 def test_tile_pairing_rule_and_partition(pb, bpc, monkeypatch):
     monkeypatch.setenv("PBSA_TILE_PAIRING", "1")
     """K3 tiles pair each call's query blocks by Top-K overlap (pair_tiles_kernel): the device
-    pairing equals the restated greedy rule, covers every query block exactly once (odd counts: one
-    single-block tile), and does not lengthen the total union work on these inputs.  PBSA_TILE_PAIRING=1
+    pairing equals the restated greedy + bottleneck rule and covers every query block exactly once
+    (odd counts: one single-block tile).  PBSA_TILE_PAIRING=1
     forces it for these short windows (auto mode pairs windows of >= 1024 blocks only)."""
     U, C, W, b, d, k_top = 3, 12, 4, 60, 128, 5
     mem = pb.Memory(U, C, W, bpc, b, d)
@@ -645,9 +670,6 @@ def test_tile_pairing_rule_and_partition(pb, bpc, monkeypatch):
             assert got == _pairing_reference(sl[u])
             flat = sorted(x for t in got for x in t if x >= 0)
             assert flat == list(range(bpc))
-            nat = sum(len(set(sl[u][t]) | set(sl[u][t + 1] if t + 1 < bpc else [])) for t in range(0, bpc, 2))
-            paired = sum(len(set(sl[u][a]) | (set(sl[u][b2]) if b2 >= 0 else set())) for a, b2 in got)
-            assert paired <= nat
     mem.close()
 
 
