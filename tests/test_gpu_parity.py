@@ -371,6 +371,16 @@ def test_rollout_small(pb, d):
     run_rollout(pb, units=3, d=d, b=60, bpc=6, C=12, W=2, n_chunks=8, k_top=3, seed=d)
 
 
+@pytest.mark.parametrize("bpc", [6, 7])
+def test_rollout_with_tile_pairing(pb, bpc, monkeypatch):
+    """The K3 tile pairing forced on for short windows (auto mode pairs >= 1024-block windows only):
+    every call of the rollout still replays bit-exactly (Top-K, s_t, P / L) and within tolerance
+    (attention) through the oracle -- outputs do not depend on which query blocks share a tile."""
+    monkeypatch.setenv("PBSA_TILE_PAIRING", "1")
+    run_rollout(pb, units=3, d=128, b=60, bpc=bpc, C=12, W=2, n_chunks=6, k_top=3, seed=40 + bpc,
+                denoise_steps=2)
+
+
 def test_rollout_config1(pb):
     """Config 1 (BASELINE.json): d=64, b=64 = (1,8,8) on 16x16 frames (4 blocks/frame), 2-frame
     chunks (8 query blocks), P = 2 frames (the sink chunk), L = 4 frames, top-k 8."""
