@@ -204,23 +204,62 @@ class QuerySplitLayout:
             qc_full[:, b: b + c] = recv[r, :, :c]
         return qc_full
 
+    def _gather_output_p2p(self, o_part, block_rows, out, async_op):
+        """R > 1: every (source, head) shard is one contiguous token range of one head in `out`, so
+        the shards are received straight into place by point-to-point transfers (one per source and
+        head) -- no rank-major staging buffer and no permuting copy after an all-gather."""
+        units = o_part.shape[0]
+        ops = []
+        for src in range(self.world):
+            g, r = divmod(src, self.replicas)
+            b, c = self.q_ranges[r]
+            h0 = g * self.heads_per_group
+            if src == self.rank:
+                out[h0: h0 + units, b * block_rows: (b + c) * block_rows].copy_(o_part[:, : c * block_rows])
+                continue
+            for h in range(units):
+                ops.append(dist.P2POp(dist.irecv, out[h0 + h, b * block_rows: (b + c) * block_rows], src))
+        for dst in range(self.world):
+            if dst == self.rank:
+                continue
+            for h in range(units):
+                ops.append(dist.P2POp(dist.isend, o_part[h].contiguous(), dst))
+        works = dist.batch_isend_irecv(ops) if ops else []
+
+        class _All:
+            def wait(self):
+                for w in works:
+                    w.wait()
+                return True
+
+        if async_op:
+            return _All(), (lambda: out)
+        _All().wait()
+        return out
+
     def gather_output(self, o_part: torch.Tensor, block_rows: int, out: torch.Tensor | None = None,
                       async_op: bool = False):
         """o_part [heads_per_group, q_count * block_rows, d] -> [heads, bpc * block_rows, d] on every
         rank (all-gather of the padded shards).  async_op=True returns (work, finish).
 
         Rank order is (group, replica), so with R = 1 the gathered shards already ARE the output
-        in head order and NCCL writes straight into `out` (no copy); with R > 1 and equal query
-        ranges one permuting copy ([G][R][units][rows] -> [G][units][R * rows]) finishes it;
-        unequal ranges fall back to per-source slice copies."""
+        in head order and NCCL writes straight into `out` (no copy); with R > 1 (distributed) the
+        shards are received in place point to point (`_gather_output_p2p`); the single-process
+        simulation with R > 1 and equal query ranges uses one permuting copy ([G][R][units][rows]
+        -> [G][units][R * rows]), unequal ranges per-source slice copies."""
         units, _, d = o_part.shape
+        if out is None:
+            out = torch.empty(self.heads, self.bpc * block_rows, d, dtype=o_part.dtype, device=o_part.device)
+        # point-to-point in place: NCCL, or host tensors (gloo's send / recv take CPU tensors only;
+        # the one-GPU gloo diagnostic of tools/multi_rank_check.sh keeps the all-gather below)
+        if (self.replicas > 1 and is_dist() and self.world > 1 and out.is_contiguous()
+                and (dist.get_backend() == "nccl" or not o_part.is_cuda)):
+            return self._gather_output_p2p(o_part, block_rows, out, async_op)
         mrows = self.max_q * block_rows
         send = o_part
         if o_part.shape[1] != mrows:
             send = torch.zeros(units, mrows, d, dtype=o_part.dtype, device=o_part.device)
             send[:, : o_part.shape[1]] = o_part
-        if out is None:
-            out = torch.empty(self.heads, self.bpc * block_rows, d, dtype=o_part.dtype, device=o_part.device)
         equal = all(c == self.max_q for _, c in self.q_ranges)
         direct = self.replicas == 1 and equal and out.is_contiguous()
         if direct:
