@@ -10,6 +10,8 @@ consumer (the output projection) runs.
 """
 from __future__ import annotations
 
+import os
+
 import torch
 import torch.distributed as dist
 
@@ -253,7 +255,8 @@ class QuerySplitLayout:
         # point-to-point in place: NCCL, or host tensors (gloo's send / recv take CPU tensors only;
         # the one-GPU gloo diagnostic of tools/multi_rank_check.sh keeps the all-gather below)
         if (self.replicas > 1 and is_dist() and self.world > 1 and out.is_contiguous()
-                and (dist.get_backend() == "nccl" or not o_part.is_cuda)):
+                and (dist.get_backend() == "nccl" or not o_part.is_cuda)
+                and os.environ.get("PBSA_GATHER_P2P", "1") != "0"):  # 0: all-gather + permute
             return self._gather_output_p2p(o_part, block_rows, out, async_op)
         mrows = self.max_q * block_rows
         send = o_part
