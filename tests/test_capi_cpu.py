@@ -70,6 +70,11 @@ def test_argument_errors_need_no_gpu():
     rc = lib.pbsa_attend_qkv_host(None, None, None, None, 4, 0.0, 0, None, None)
     assert rc == _capi.PBSA_EINVAL and b"attend_qkv_host" in lib.pbsa_last_error()
     assert lib.pbsa_mem_host_sync(None) == _capi.PBSA_EINVAL
+    rc = lib.pbsa_pair_tiles(None, 4, 2, 4, 3, 10, 1, None, None)  # rows 2..5 of a 4-row sel
+    assert rc == _capi.PBSA_EINVAL and b"pair_tiles" in lib.pbsa_last_error()
+    rc = lib.pbsa_pair_tiles(None, 4, 0, 4, 3, 10, 1, None, None)
+    assert rc == _capi.PBSA_EINVAL and b"null pointer" in lib.pbsa_last_error()
+    assert lib.pbsa_last_tile_pairs(None, None, None) == _capi.PBSA_EINVAL
     assert lib.pbsa_launch_count() >= 0
 
 
