@@ -196,7 +196,8 @@ int pbsa_mem_write_chunk(pbsa_mem* m, const void* k_chunk, const void* v_chunk, 
 int pbsa_mem_commit(pbsa_mem* m, const float* s_t, void* stream);
 
 /* One full PBSA call of a layer on the current chunk (Alg. 1 line "Apply PBSA with Top-K"):
- * K1(Q) -> K2 -> K3, and for mode PBSA_MODE_CACHE_UPDATE (the k=0 pass) also s_t and K4.
+ * K1(Q) -> K2 -> K3, and for mode PBSA_MODE_CACHE_UPDATE (the k=0 pass) also s_t and K4; for local
+ * windows of >= 1024 blocks the K3 tile pairing (pbsa_pair_tiles) runs between K2 and K3.
  * q [units][blocks_per_chunk*b][d] bf16; o same shape; lse nullable.  k_top = |Omega(q)| in
  * blocks (clipped to the local window); scale <= 0 selects d^-1/2. */
 enum { PBSA_MODE_DENOISE = 0, PBSA_MODE_CACHE_UPDATE = 1 };
