@@ -371,13 +371,13 @@ def test_rollout_small(pb, d):
     run_rollout(pb, units=3, d=d, b=60, bpc=6, C=12, W=2, n_chunks=8, k_top=3, seed=d)
 
 
-@pytest.mark.parametrize("bpc", [6, 7])
-def test_rollout_with_tile_pairing(pb, bpc, monkeypatch):
+@pytest.mark.parametrize("bpc,d", [(6, 128), (7, 128), (7, 64)])
+def test_rollout_with_tile_pairing(pb, bpc, d, monkeypatch):
     """The K3 tile pairing forced on for short windows (auto mode pairs >= 1024-block windows only):
     every call of the rollout still replays bit-exactly (Top-K, s_t, P / L) and within tolerance
     (attention) through the oracle -- outputs do not depend on which query blocks share a tile."""
     monkeypatch.setenv("PBSA_TILE_PAIRING", "1")
-    run_rollout(pb, units=3, d=128, b=60, bpc=bpc, C=12, W=2, n_chunks=6, k_top=3, seed=40 + bpc,
+    run_rollout(pb, units=3, d=d, b=60, bpc=bpc, C=12, W=2, n_chunks=6, k_top=3, seed=40 + bpc + d,
                 denoise_steps=2)
 
 
