@@ -52,7 +52,11 @@ struct BsaParams {
     // producers pass a barrier (gang_ctr[g]) between units so all tiles of a unit stream its pool
     // together (the KV blocks they share are fetched from DRAM once and served from L2)
     int gangs;
-    int* gang_ctr;         // [gangs] + done counter at [kMaxGangs], zero between launches
+    int* gang_ctr;         // [gangs (+1 extra)] + done counter at [kMaxGangs], zero between launches
+    // extra gang (gangs > 0, extra > 0): the `extra` CTA slots left over by the full gangs form one
+    // more gang that takes the last `xunits` units, member m covering tiles m and m + extra of each
+    // (two per unit when extra < tiles_per_unit), with its own unit barrier (gang_ctr[gangs])
+    int extra, xunits;
 };
 constexpr int kMaxGangs = 1024;
 
@@ -76,8 +80,13 @@ __device__ __forceinline__ int64_t range_begin(int c, int64_t W, int G) { return
 __device__ __forceinline__ int num_fragments(const BsaParams& p, int c) {
     if (c >= p.grid) return 0;
     if (p.gangs > 0) {
-        const int g = c / p.tiles_per_unit;
-        return g < p.units ? (p.units - 1 - g) / p.gangs + 1 : 0;
+        const int main_cta = p.gangs * p.tiles_per_unit, main_units = p.units - p.xunits;
+        if (c < main_cta) {
+            const int g = c / p.tiles_per_unit;
+            return g < main_units ? (main_units - 1 - g) / p.gangs + 1 : 0;
+        }
+        const int m = c - main_cta;  // extra-gang member
+        return p.xunits * (m + p.extra < p.tiles_per_unit ? 2 : 1);
     }
     if (p.part_o == nullptr) return c < p.n_tiles ? (p.n_tiles - 1 - c) / p.grid + 1 : 0;
     if (c >= p.tail_grid || p.vtotal == 0) return p.whole_waves;
@@ -102,8 +111,15 @@ __device__ __forceinline__ FragPlan plan_fragment(const BsaParams& p, int vc, in
     FragPlan fp;
     fp.tile = tail_frag ? my_first_tile + (f - p.whole_waves) : vc + f * p.grid;
     if (p.gangs > 0) {
-        const int g = vc / p.tiles_per_unit;
-        fp.tile = (g + f * p.gangs) * p.tiles_per_unit + vc % p.tiles_per_unit;
+        const int main_cta = p.gangs * p.tiles_per_unit;
+        if (vc < main_cta) {
+            const int g = vc / p.tiles_per_unit;
+            fp.tile = (g + f * p.gangs) * p.tiles_per_unit + vc % p.tiles_per_unit;
+        } else {  // extra gang: per unit one or two tiles (m, m + extra)
+            const int m = vc - main_cta, k = m + p.extra < p.tiles_per_unit ? 2 : 1;
+            const int unit = p.units - p.xunits + f / k;
+            fp.tile = unit * p.tiles_per_unit + m + (f % k) * p.extra;
+        }
     }
     fp.u = fp.tile / p.tiles_per_unit;
     if (p.pairs != nullptr) {
@@ -145,16 +161,37 @@ __device__ __forceinline__ FragMeta make_meta(const BsaParams& p, const FragPlan
     return fm;
 }
 
-// unit gangs: lane 0 waits until every member of vc's gang has issued all loads of unit f - 1
+// unit gangs: before its first fragment of a unit, lane 0 waits until every member of vc's gang has
+// issued all loads of the previous unit (members arrive once per unit, after their last fragment of it)
 __device__ __forceinline__ void gang_wait(const BsaParams& p, int vc, int f) {
-    if (p.gangs > 0 && f > 0 && (threadIdx.x & 31) == 0) {
-        const int want = f * p.tiles_per_unit;
-        while (ld_acquire_gpu(p.gang_ctr + vc / p.tiles_per_unit) < want) __nanosleep(64);
+    if (p.gangs > 0 && (threadIdx.x & 31) == 0) {
+        const int main_cta = p.gangs * p.tiles_per_unit;
+        if (vc < main_cta) {
+            if (f > 0) {
+                const int want = f * p.tiles_per_unit;
+                while (ld_acquire_gpu(p.gang_ctr + vc / p.tiles_per_unit) < want) __nanosleep(64);
+            }
+        } else {
+            const int k = (vc - main_cta) + p.extra < p.tiles_per_unit ? 2 : 1;
+            const int i = f / k;
+            if (i > 0 && f % k == 0) {
+                const int want = i * p.extra;
+                while (ld_acquire_gpu(p.gang_ctr + p.gangs) < want) __nanosleep(64);
+            }
+        }
     }
     __syncwarp();
 }
-__device__ __forceinline__ void gang_arrive(const BsaParams& p, int vc) {
-    if (p.gangs > 0 && (threadIdx.x & 31) == 0) red_release_gpu_add(p.gang_ctr + vc / p.tiles_per_unit, 1);
+__device__ __forceinline__ void gang_arrive(const BsaParams& p, int vc, int f) {
+    if (p.gangs > 0 && (threadIdx.x & 31) == 0) {
+        const int main_cta = p.gangs * p.tiles_per_unit;
+        if (vc < main_cta) {
+            red_release_gpu_add(p.gang_ctr + vc / p.tiles_per_unit, 1);
+        } else {
+            const int k = (vc - main_cta) + p.extra < p.tiles_per_unit ? 2 : 1;
+            if (f % k == k - 1) red_release_gpu_add(p.gang_ctr + p.gangs, 1);
+        }
+    }
 }
 
 // The visible list of a tile (warp-collective): dense blocks first (both halves see them), then
@@ -311,6 +348,8 @@ inline void plan_schedule(BsaParams& p, int slots, int D) {
     p.tail_grid = 0;
     p.vtotal = 0;
     p.gangs = 0;
+    p.extra = 0;
+    p.xunits = 0;
     if (p.gang_ctr != nullptr) {
         // unit-gang schedule: many whole-tile waves over a slot pool far larger than L2 (config 5:
         // 12480 tiles, 65 GB) -- tiles of one unit run together so the blocks they share come from
@@ -324,6 +363,22 @@ inline void plan_schedule(BsaParams& p, int slots, int D) {
             p.gangs = gangs < p.units ? gangs : p.units;
             p.grid = p.gangs * p.tiles_per_unit;
             p.part_o = nullptr;
+            // the leftover slots as one extra gang when it can cover a unit in at most two rounds:
+            // it gets the share of the units its rate (1/2 or 1 unit per round) earns
+            // (PBSA_K3_EXTRA_GANG=0: off, experiments)
+            const char* xenv = getenv("PBSA_K3_EXTRA_GANG");
+            int e = slots - p.gangs * p.tiles_per_unit;
+            if (e > p.tiles_per_unit) e = p.tiles_per_unit;
+            if ((xenv == nullptr || atoi(xenv) != 0) && p.gangs == gangs && p.gangs < kMaxGangs &&
+                2 * e >= p.tiles_per_unit) {
+                const double rate = e >= p.tiles_per_unit ? 1.0 : 0.5;
+                const int x = static_cast<int>(p.units * rate / (p.gangs + rate) + 0.5);
+                if (x >= 1 && x < p.units) {
+                    p.extra = e;
+                    p.xunits = x;
+                    p.grid += e;
+                }
+            }
         }
     }
     if (p.part_o != nullptr) {

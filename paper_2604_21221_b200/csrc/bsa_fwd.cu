@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                     load_v(nf - 1);
                     jg += nf;
                 }
-                gang_arrive(p, cta);
+                gang_arrive(p, cta, f);
             }
         }
     } else if (warp == 1) {
@@ -690,7 +690,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         // passed its last barrier: a CTA only exits after its producer finished all units)
         __threadfence();
         if (atomicAdd(p.gang_ctr + kMaxGangs, 1) == static_cast<int>(gridDim.x) - 1) {
-            for (int g = 0; g < p.gangs; ++g) p.gang_ctr[g] = 0;
+            for (int g = 0; g <= p.gangs; ++g) p.gang_ctr[g] = 0;  // (+ the extra gang's)
             p.gang_ctr[kMaxGangs] = 0;
             __threadfence();
         }

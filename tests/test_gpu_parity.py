@@ -278,7 +278,7 @@ def test_bsa_fwd_32bit_lists_selected(pb):
     assert pb.bsa_fwd_last_plan().list_entry_bytes == 4
 
 
-@pytest.mark.parametrize("units,nqb", [(40, 17), (7, 78), (3, 5)])
+@pytest.mark.parametrize("units,nqb", [(40, 17), (7, 78), (3, 5), (33, 78)])
 def test_bsa_fwd_unit_gang_schedule(pb, monkeypatch, units, nqb):
     """Unit-gang schedule (PBSA_K3_GANG=1; the default for config-5-sized launches): gangs of
     tiles_per_unit CTAs walk units in lockstep behind an inter-CTA barrier.  Several rounds per
@@ -288,6 +288,19 @@ def test_bsa_fwd_unit_gang_schedule(pb, monkeypatch, units, nqb):
         _bsa_case(pb, units, nqb, 60, 128, 7, 40, 9, seed=70 + units + rep)
         plan = pb.bsa_fwd_last_plan()
         assert plan.schedule == 2 and plan.gangs >= 1, (plan.schedule, plan.gangs)
+        tpu = (nqb + 1) // 2
+        if units > plan.gangs:  # the leftover slots form the extra gang (two tiles per member)
+            assert plan.grid > plan.gangs * tpu, (plan.grid, plan.gangs, tpu)
+
+
+@pytest.mark.parametrize("units,nqb", [(40, 17), (33, 78)])
+def test_bsa_fwd_extra_gang_off(pb, monkeypatch, units, nqb):
+    """PBSA_K3_EXTRA_GANG=0: the full gangs alone take every unit (the A/B baseline)."""
+    monkeypatch.setenv("PBSA_K3_GANG", "1")
+    monkeypatch.setenv("PBSA_K3_EXTRA_GANG", "0")
+    _bsa_case(pb, units, nqb, 60, 128, 7, 40, 9, seed=90 + units)
+    plan = pb.bsa_fwd_last_plan()
+    assert plan.schedule == 2 and plan.grid == plan.gangs * ((nqb + 1) // 2)
 
 
 @pytest.mark.parametrize("cap", [2, 4, 5, 8])
