@@ -36,6 +36,18 @@ grads = pb.attention_sparse_backward(q, kp, vp, dense, local, sel, b, o, lse, do
 # unit-gang K3 schedule (forced) and a 16-bit-list launch
 os.environ["PBSA_K3_GANG"] = "1"
 pb.attention_sparse(q, kp, vp, dense, local, sel, b, validate=False)
+# 40 units x 17 query blocks: 32 full gangs of 9 tiles + the extra gang (8 members, two tiles each)
+U2, nqb2 = 40, 17
+kp2 = torch.zeros(U2, S, 64, d, device="cuda", dtype=torch.bfloat16)
+vp2 = torch.zeros_like(kp2)
+kp2[:, :, :b] = torch.randn(U2, S, b, d, device="cuda", generator=g).bfloat16()
+vp2[:, :, :b] = torch.randn(U2, S, b, d, device="cuda", generator=g).bfloat16()
+q2 = torch.randn(U2, nqb2 * b, d, device="cuda", generator=g).bfloat16()
+perm2 = torch.stack([torch.randperm(S, device="cuda", generator=g) for _ in range(U2)]).int()
+sel2 = torch.stack([torch.stack([torch.randperm(nl, device="cuda", generator=g)[:kk].sort().values
+                                 for _ in range(nqb2)]) for _ in range(U2)]).int().contiguous()
+pb.attention_sparse(q2, kp2, vp2, perm2[:, :nd].contiguous(), perm2[:, nd:nd + nl].contiguous(), sel2, b,
+                    validate=False)
 del os.environ["PBSA_K3_GANG"]
 # query-split calls (2 replicas of the same heads) and the drop-sink fault path of K4
 parts = [pb.Memory(U, C, W, bpc, b, d) for _ in range(2)]
