@@ -372,7 +372,9 @@ inline void plan_schedule(BsaParams& p, int slots, int D) {
             if ((xenv == nullptr || atoi(xenv) != 0) && p.gangs == gangs && p.gangs < kMaxGangs &&
                 2 * e >= p.tiles_per_unit) {
                 const double rate = e >= p.tiles_per_unit ? 1.0 : 0.5;
-                const int x = static_cast<int>(p.units * rate / (p.gangs + rate) + 0.5);
+                int x = static_cast<int>(p.units * rate / (p.gangs + rate) + 0.5);
+                const char* xu = getenv("PBSA_K3_EXTRA_UNITS");  // experiments: the extra gang's units
+                if (xu != nullptr && atoi(xu) > 0) x = atoi(xu);
                 if (x >= 1 && x < p.units) {
                     p.extra = e;
                     p.xunits = x;
