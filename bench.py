@@ -239,6 +239,34 @@ def emit(line, args):
 
 
 # ------------------------------------------------------------------------------ our arm
+def dense_fmha_reference(heads, n_q, n_k, d, dev):
+    """cuDNN dense FMHA (torch SDPA) at 4 * n_q * n_k * d * heads FLOPs: what a vendor attention
+    kernel reaches on this box at K3's algorithmic FLOP count (None if the backend is missing)."""
+    try:
+        import torch
+        import torch.nn.functional as F
+        from torch.nn.attention import SDPBackend, sdpa_kernel
+        g = torch.Generator(device=dev).manual_seed(1)
+        q, k, v = (torch.randn(1, heads, n, d, device=dev, dtype=torch.bfloat16, generator=g)
+                   for n in (n_q, n_k, n_k))
+        with sdpa_kernel(SDPBackend.CUDNN_ATTENTION):
+            for _ in range(3):
+                F.scaled_dot_product_attention(q, k, v)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(20):
+                F.scaled_dot_product_attention(q, k, v)
+            e1.record()
+            torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 20
+        return {"kernel": "cuDNN FMHA via torch SDPA, dense, bf16", "ms": ms,
+                "tflops": 4.0 * n_q * n_k * d * heads / (ms * 1e-3) / 1e12,
+                "shape": [heads, n_q, n_k, d]}
+    except Exception as ex:  # noqa: BLE001 -- context only
+        return {"unavailable": str(ex).splitlines()[0][:160] if str(ex) else type(ex).__name__}
+
+
 def run_ours(args, rank, world, local_rank):
     import numpy as np
     import torch
@@ -443,6 +471,13 @@ def run_ours(args, rank, world, local_rank):
         roofline["achieved_executed"] = exec_flops_call / (k3_ms * 1e-3) / 1e12
         roofline["frac_executed"] = roofline["achieved_executed"] / peaks["bf16"]
     stage_share = {k: v / ms_total_prof for k, v in prof["ms"].items()}
+    # context, not a peak: the library's dense FMHA (torch SDPA, cuDNN backend) on the dense
+    # equivalent of this rank's K3 launch (same heads / queries / visible tokens / d), same box
+    dense = dense_fmha_reference(Ul, qn * b, (n_dense + k_eff) * b, d, dev)
+    if dense is not None:
+        roofline["dense_fmha_reference"] = dense
+        if roofline.get("achieved_executed") and "tflops" in dense:
+            roofline["executed_vs_dense_fmha"] = roofline["achieved_executed"] / dense["tflops"]
 
     # ---------------------------------------------------------------- timed: end to end (host buffers)
     e2e = None
